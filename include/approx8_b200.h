@@ -1,0 +1,171 @@
+/*
+ * approx8_b200 -- C ABI of the B200-native 8-bit approximation codec.
+ *
+ * Drop-in boundary for the hot path of the reference package `approx8`
+ * (/root/reference/pkg/src/approx8/codecs.py).  The reference is pure
+ * Python/NumPy, so "the FFI a maintainer would bind" is a ctypes binding
+ * from Python; every entry point below names the
+ * reference function it replaces.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; device pointers are CUDA global memory,
+ *     `stream` is a cudaStream_t passed as void*;
+ *   - every call returns an int status (A8_OK or one of the A8_ERR_* codes,
+ *     mirroring approx8/errors.py:16-33); a8_last_error() gives the message;
+ *   - compute entry points are asynchronous on `stream`; the non-finite
+ *     input condition (codecs.py:251-252, InputError) is reported through a
+ *     device status word because detecting it needs the data.
+ *
+ * Flat index space and slab layout (shared by encode and decode)
+ *   A call covers `nseg` segments (tensors).  Segment s occupies flat
+ *   elements [flat_off_s, flat_off_s + n_s); flat_off_s is a multiple of 16.
+ *   The codes for flat element e live at
+ *       codes + (e / block_len) * block_stride + (e % block_len)
+ *   and the float32 scale of segment s as seen from block j at
+ *       scales + j * scale_block_stride + scale_idx_s           (floats)
+ *   For decode, rank r's copy is offset by r * rank_stride bytes (codes and
+ *   scales alike).  One block (block_len >= total) is the plain layout.
+ */
+#ifndef APPROX8_B200_H
+#define APPROX8_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define A8_ABI_VERSION 1
+
+/* status codes: approx8/errors.py:16-33 */
+#define A8_OK 0
+#define A8_ERR_INPUT 1  /* InputError  -- non-finite data (codecs.py:251-252) */
+#define A8_ERR_CONFIG 2 /* ConfigError -- invalid spec (codecs.py:112-123)   */
+#define A8_ERR_USAGE 3  /* UsageError  -- bad call (codecs.py:274-280)        */
+#define A8_ERR_CUDA 4   /* CUDA launch / runtime failure                      */
+
+/* codebook kinds: codecs.py:73-77 (DataTypeKind) */
+#define A8_DYNAMIC_TREE 0
+#define A8_STATIC_TREE 1
+#define A8_LINEAR 2
+#define A8_MANTISSA 3
+
+/* normalisations: codecs.py:80-83 (NormKind) */
+#define A8_NORM_NONE 0
+#define A8_NORM_ABSMAX 1
+#define A8_NORM_DECADE 2
+
+/* device status bits (a8_encode) */
+#define A8_STATUS_NONFINITE 1u
+
+#define A8_LUT_MAX 4096
+
+/* Codebook of one kind: codecs.py:161-204 (Codebook / build_codebook). */
+typedef struct a8_book {
+    double values[128]; /* distinct non-negative values, ascending (codecs.py:194-199) */
+    float table[256];   /* decode table, -0 folded to +0 (codecs.py:189-192)          */
+    uint8_t codes[128]; /* lowest code byte per distinct value (codecs.py:195-200)    */
+    int32_t ndistinct;  /* D: 128, or 114 for mantissa                                 */
+    int32_t kind;
+    int32_t pad[2];
+} a8_book_t;
+
+/* Per-scale decision table.  T[i] is the smallest float32 bit pattern whose
+ * reference decision (codecs.py:260-265) picks a value above index i;
+ * e[] buckets |x| by its top 15 bits (exponent + 7 mantissa bits) with at
+ * most one distinct threshold per bucket.  valid == 0 means the bucket table
+ * does not apply (e.g. subnormal scales) and T[] is searched instead. */
+typedef struct a8_lut {
+    uint32_t len;     /* used entries of e[]            */
+    int32_t kbase;    /* key of e[0]                    */
+    uint32_t valid;   /* 1: bucket table usable         */
+    uint32_t nfinite; /* thresholds below 0x7f800000    */
+    float scale;      /* the scale the table encodes    */
+    uint32_t pad[3];
+    uint32_t T[128];  /* thresholds, padded with 0x7f800000 */
+    uint32_t e[A8_LUT_MAX];
+} a8_lut_t;
+
+/* Encode segment: a float32 tensor (contiguous). */
+typedef struct a8_enc_seg {
+    const float* x;
+    int64_t n;
+    int64_t flat_off;  /* multiple of 16 */
+    int32_t scale_idx; /* slot of this segment's scale in each block's scale array */
+    int32_t pad;
+} a8_enc_seg_t;
+
+/* Decode segment: a float32 output tensor (contiguous). */
+typedef struct a8_dec_seg {
+    float* out;
+    int64_t n;
+    int64_t flat_off;  /* multiple of 16; the piece lies inside one block */
+    int32_t scale_idx;
+    int32_t pad;
+} a8_dec_seg_t;
+
+typedef struct a8_layout {
+    uint8_t* codes;
+    float* scales;
+    int64_t block_len;          /* elements per block, multiple of 16           */
+    int64_t block_stride;       /* bytes between consecutive blocks of codes    */
+    int64_t scale_block_stride; /* floats between consecutive blocks' scales    */
+    int64_t rank_stride;        /* bytes between ranks' copies (decode only)    */
+    int32_t scale_reps;         /* encode: write the scale into blocks [0, reps) */
+    int32_t pad;
+} a8_layout_t;
+
+int a8_abi_version(void);
+const char* a8_last_error(void);
+
+/* build_codebook (codecs.py:186-204): fills `out` on the host. */
+int a8_codebook(int kind, a8_book_t* out);
+
+/* _scale_for (codecs.py:232-241) for the data-independent normalisations:
+ * none -> 1, decade d -> float32(10^d).  absmax is data dependent (device). */
+int a8_fixed_scale(int norm, int decades, float* scale_out);
+
+/* Host construction of the decision table for a fixed scale (used for the
+ * none/decade specs and by the CPU tests of the table logic). */
+int a8_build_lut_host(const a8_book_t* book, float scale, a8_lut_t* out);
+
+/* Device scratch needed by a8_encode / a8_decode for `nseg` segments.
+ * Must be zero-filled once after allocation; the kernels leave it zeroed. */
+size_t a8_workspace_bytes(int nseg);
+
+/* encode_buffer (codecs.py:244-269) for nseg tensors in one launch.
+ *   book_dev    device copy of a8_codebook(kind)
+ *   norm        A8_NORM_ABSMAX: per-segment absmax scale computed on device;
+ *               otherwise `static_lut_dev` (device copy of a8_build_lut_host
+ *               for the fixed scale) is used for every segment.
+ *   segs        host array of nseg descriptors (copied into the launch, or
+ *               into `workspace` when nseg is large)
+ *   status_in   optional device uint32 OR-ed into the result (chaining)
+ *   status_out  device uint32, OVERWRITTEN with this call's A8_STATUS_* bits
+ *               (| *status_in) once the kernel finishes; replicated to
+ *               status_out[k * scale_block_stride] for k < scale_reps      */
+int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_dev, int norm,
+              const void* static_lut_dev, a8_layout_t layout, void* workspace,
+              const uint32_t* status_in, uint32_t* status_out, void* stream);
+
+/* decode_buffer (codecs.py:272-282) fused with the cross-rank reduction:
+ *   out = sum_{r<nranks} table[c_r] * s_r, accumulated in rank order in
+ *   float32 (round-to-nearest, no FMA contraction); op = 1 divides by
+ *   float32(nranks) (the data-parallel average), op = 0 keeps the sum.
+ *   nranks = 1 is exactly decode_buffer.
+ *   status_idx >= 0: status_out = OR of the uint32 words at
+ *   scales[r * rank_stride/4 + j * scale_block_stride + status_idx] for
+ *   r < nranks, j < status_blocks (the encoders' replicated status words). */
+int a8_decode(const a8_dec_seg_t* segs, int nseg, const void* book_dev, a8_layout_t layout,
+              int nranks, int op, int status_idx, int status_blocks, uint32_t* status_out,
+              void* workspace, void* stream);
+
+/* Number of SMs and the persistent grid sizes the kernels use on `device`. */
+int a8_device_info(int device, int* num_sms, int* enc_ctas_per_sm, int* dec_ctas_per_sm);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* APPROX8_B200_H */

@@ -1,0 +1,56 @@
+"""B200-native 8-bit approximation hot path (arXiv 1511.04561), drop-in for the
+codec / exchange subset of the reference package ``approx8``
+(``approx8/__init__.py:9-22`` codec re-exports, ``mlp.py`` hook seams).
+
+Compute runs in hand-written sm_100a kernels behind the C ABI declared in
+``include/approx8_b200.h``; the Python layer mirrors the reference API.
+"""
+
+from .codecs import (
+    CODE_COUNT,
+    PAYLOAD_BITS,
+    SIGN_MASK,
+    Codebook,
+    DataTypeKind,
+    DataTypeSpec,
+    NormKind,
+    QuantizedTensor,
+    build_codebook,
+    decode_buffer,
+    encode_buffer,
+    parse_spec,
+    roundtrip,
+)
+from .errors import ApproxError, ConfigError, InputError, TrainingError, UsageError
+from .exchange import DDPHookState, GradientExchange, a8_comm_hook, exchange
+from .hooks import HookMode, HookStats, QuantHookConfig, default_hook_spec, make_quantizer
+
+__all__ = [
+    "CODE_COUNT",
+    "PAYLOAD_BITS",
+    "SIGN_MASK",
+    "ApproxError",
+    "Codebook",
+    "ConfigError",
+    "DDPHookState",
+    "DataTypeKind",
+    "DataTypeSpec",
+    "GradientExchange",
+    "HookMode",
+    "HookStats",
+    "InputError",
+    "NormKind",
+    "QuantHookConfig",
+    "QuantizedTensor",
+    "TrainingError",
+    "UsageError",
+    "a8_comm_hook",
+    "build_codebook",
+    "decode_buffer",
+    "default_hook_spec",
+    "encode_buffer",
+    "exchange",
+    "make_quantizer",
+    "parse_spec",
+    "roundtrip",
+]

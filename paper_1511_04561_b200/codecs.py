@@ -1,0 +1,413 @@
+"""B200 drop-in for ``approx8.codecs`` (reference: pkg/src/approx8/codecs.py).
+
+Same names, argument meaning and error behaviour as the reference codec API
+(``DataTypeKind``, ``NormKind``, ``DataTypeSpec``, ``Codebook``,
+``build_codebook``, ``QuantizedTensor``, ``encode_buffer``, ``decode_buffer``,
+``roundtrip``); the compute runs in the sm_100a kernels of
+``include/approx8_b200.h`` on the tensor's CUDA device.  There is no CPU
+fallback: without a CUDA device the compute calls raise.
+
+Differences a caller can see:
+  * ``QuantizedTensor.codes`` is a CUDA ``torch.uint8`` tensor (flat, C order);
+    ``scale`` is a Python float fetched lazily (``scale_tensor`` stays on the
+    device, so nothing syncs until it is read).
+  * ``decode_buffer``/``roundtrip`` return a CUDA ``torch.float32`` tensor,
+    or a NumPy array when the input to ``roundtrip`` was a NumPy array.
+  * Inputs are float32.  Other dtypes are converted to float32 first; the
+    reference computes float64 inputs in float64 (codecs.py:254), so for
+    float64 data that float32 cannot represent exactly the codes may differ.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass
+from enum import Enum
+from functools import lru_cache
+from typing import IO, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import ConfigError, InputError, UsageError
+
+SIGN_MASK = 0x80
+PAYLOAD_BITS = 7
+CODE_COUNT = 256
+
+
+class DataTypeKind(str, Enum):
+    DYNAMIC_TREE = "dynamic-tree"
+    STATIC_TREE = "static-tree"
+    LINEAR = "linear"
+    MANTISSA = "mantissa"
+
+
+class NormKind(str, Enum):
+    NONE = "none"
+    ABSMAX = "absmax"
+    DECADE = "decade"
+
+
+# codecs.py:89-94 -- which normalisation fits which codebook family
+_ALLOWED_NORMS = {
+    DataTypeKind.DYNAMIC_TREE: {NormKind.NONE, NormKind.ABSMAX},
+    DataTypeKind.LINEAR: {NormKind.NONE, NormKind.ABSMAX},
+    DataTypeKind.STATIC_TREE: {NormKind.NONE, NormKind.DECADE},
+    DataTypeKind.MANTISSA: {NormKind.NONE, NormKind.DECADE},
+}
+
+DECADE_MIN, DECADE_MAX = -7, 7
+
+
+@dataclass(frozen=True)
+class DataTypeSpec:
+    """One concrete codec: a codebook family plus its normalisation
+    (codecs.py:99-128, same validation and ``ConfigError`` messages)."""
+
+    kind: DataTypeKind
+    normalization: NormKind = NormKind.NONE
+    decades: int = 0
+
+    def __post_init__(self) -> None:
+        try:
+            kind = DataTypeKind(self.kind)
+            norm = NormKind(self.normalization)
+        except ValueError as exc:
+            raise ConfigError(str(exc)) from exc
+        object.__setattr__(self, "kind", kind)
+        object.__setattr__(self, "normalization", norm)
+        if norm not in _ALLOWED_NORMS[kind]:
+            raise ConfigError(f"normalization {norm.value!r} is not supported for {kind.value!r}")
+        if norm is NormKind.DECADE:
+            if not (DECADE_MIN <= self.decades <= DECADE_MAX):
+                raise ConfigError(
+                    f"decade offset must lie in [{DECADE_MIN}, {DECADE_MAX}], got {self.decades}"
+                )
+        elif self.decades != 0:
+            raise ConfigError("decades is only meaningful with decade normalization")
+
+    def label(self) -> str:
+        if self.normalization is NormKind.DECADE:
+            return f"{self.kind.value}/decade{self.decades:+d}"
+        return f"{self.kind.value}/{self.normalization.value}"
+
+    # codes used by the C ABI
+    @property
+    def kind_code(self) -> int:
+        return N.KIND_CODE[self.kind.value]
+
+    @property
+    def norm_code(self) -> int:
+        return N.NORM_CODE[self.normalization.value]
+
+
+def parse_spec(label: str) -> DataTypeSpec:
+    """Inverse of ``DataTypeSpec.label`` ("dynamic-tree/absmax", "mantissa/decade+2")."""
+    kind, _, norm = label.partition("/")
+    norm = norm or "none"
+    if norm.startswith("decade"):
+        return DataTypeSpec(DataTypeKind(kind), NormKind.DECADE, int(norm[6:] or 0))
+    return DataTypeSpec(DataTypeKind(kind), NormKind(norm))
+
+
+# ---------------------------------------------------------------------------
+# codebooks
+
+
+_dev_lock = threading.Lock()
+_dev_cache: dict = {}
+
+
+@dataclass(frozen=True, eq=False)
+class Codebook:
+    """Decode table for all 256 codes plus the encode search structures
+    (codecs.py:161-183).  Host arrays are read-only NumPy views; the device
+    copies (table struct, fixed-scale decision table) are built lazily per
+    CUDA device."""
+
+    spec: DataTypeSpec
+    decode_table: np.ndarray
+    sorted_values: np.ndarray
+    sorted_codes: np.ndarray
+    _book: N.Book = None  # type: ignore[assignment]
+
+    @property
+    def zero_code(self) -> int:
+        return int(self.sorted_codes[0])
+
+    def dump(self, out: IO[str]) -> None:
+        """Write all 256 codes as 'code<TAB>value' lines (codecs.py:180-183)."""
+        for code in range(CODE_COUNT):
+            out.write(f"0x{code:02x}\t{self.decode_table[code]:.9g}\n")
+
+    @property
+    def fixed_scale(self) -> Optional[float]:
+        """The data-independent scale of none/decade specs (codecs.py:232-241)."""
+        if self.spec.normalization is NormKind.ABSMAX:
+            return None
+        s = C.c_float()
+        N.check(N.lib.a8_fixed_scale(self.spec.norm_code, int(self.spec.decades), C.byref(s)))
+        return float(s.value)
+
+    def device_tables(self, device: torch.device):
+        """(book struct bytes, fixed-scale decision table or None) on ``device``."""
+        dev = _cuda_device(device)
+        key = (self.spec, dev.index)
+        with _dev_lock:
+            hit = _dev_cache.get(key)
+            if hit is None:
+                book = torch.frombuffer(bytearray(bytes(self._book)), dtype=torch.uint8).to(dev)
+                lut = None
+                if self.spec.normalization is not NormKind.ABSMAX:
+                    host = N.Lut()
+                    N.check(N.lib.a8_build_lut_host(C.byref(self._book), self.fixed_scale, C.byref(host)))
+                    lut = torch.frombuffer(bytearray(bytes(host)), dtype=torch.uint8).to(dev)
+                hit = (book, lut)
+                _dev_cache[key] = hit
+        return hit
+
+
+@lru_cache(maxsize=None)
+def build_codebook(spec: DataTypeSpec) -> Codebook:
+    """codecs.py:186-204, computed by the library's host builder (a8_codebook)."""
+    book = N.Book()
+    N.check(N.lib.a8_codebook(spec.kind_code, C.byref(book)))
+    d = int(book.ndistinct)
+    table = np.frombuffer(bytes(book.table), dtype=np.float32).copy()
+    values = np.frombuffer(bytes(book.values), dtype=np.float64)[:d].copy()
+    codes = np.frombuffer(bytes(book.codes), dtype=np.uint8)[:d].copy()
+    for arr in (table, values, codes):
+        arr.setflags(write=False)
+    return Codebook(spec=spec, decode_table=table, sorted_values=values, sorted_codes=codes, _book=book)
+
+
+# ---------------------------------------------------------------------------
+# quantized tensors
+
+
+class QuantizedTensor:
+    """Encoded buffer plus everything needed to decode it (codecs.py:207-229).
+
+    ``codes``  CUDA uint8, one byte per element, flat C order
+    ``scale``  float32 normalisation scale as a Python float (lazy)
+    """
+
+    def __init__(
+        self,
+        codes,
+        shape: Sequence[int],
+        spec: Optional[DataTypeSpec],
+        scale: Optional[float] = None,
+        nbits: int = 8,
+        pos_level: float = 0.0,
+        neg_level: float = 0.0,
+        *,
+        scale_tensor: Optional[torch.Tensor] = None,
+        meta: Optional[torch.Tensor] = None,
+    ) -> None:
+        self.codes = codes
+        self.shape = tuple(int(d) for d in shape)
+        self.spec = spec
+        self.nbits = nbits
+        self.pos_level = pos_level
+        self.neg_level = neg_level
+        self._scale = None if scale is None else float(np.float32(scale))
+        self.scale_tensor = scale_tensor
+        self._meta = meta  # int32[2] = [status, scale bits] written by the encoder
+        self._checked = meta is None
+
+    @property
+    def count(self) -> int:
+        n = 1
+        for d in self.shape:
+            n *= d
+        return n
+
+    @property
+    def scale(self) -> float:
+        if self._scale is None:
+            self._finish()
+        return self._scale
+
+    @scale.setter
+    def scale(self, value: float) -> None:
+        self._scale = float(np.float32(value))
+        self.scale_tensor = None
+
+    def _finish(self) -> None:
+        """Sync on the encoder's status word; raise InputError for NaN/Inf
+        input exactly where the reference does (codecs.py:251-252)."""
+        if self._checked and self._scale is not None:
+            return
+        if self._meta is not None:
+            host = self._meta.cpu()
+            status = int(host[0])
+            if status & N.A8_STATUS_NONFINITE:
+                raise InputError("cannot encode non-finite values (NaN or Inf present)")
+            self._scale = float(host[1:].view(torch.float32)[0])
+            self._checked = True
+        elif self.scale_tensor is not None:
+            self._scale = float(self.scale_tensor.float().cpu()[0])
+
+    def device_codes(self, device: torch.device) -> torch.Tensor:
+        c = self.codes
+        if not isinstance(c, torch.Tensor):
+            c = torch.from_numpy(np.ascontiguousarray(np.asarray(c, dtype=np.uint8).ravel()))
+        c = c.to(device).reshape(-1)
+        if not c.is_contiguous() or c.data_ptr() % 16:
+            c = c.clone()
+        return c
+
+    def device_scale(self, device: torch.device) -> torch.Tensor:
+        if self.scale_tensor is not None and self.scale_tensor.device == device:
+            return self.scale_tensor
+        return torch.tensor([self.scale], dtype=torch.float32, device=device)
+
+    def codes_numpy(self) -> np.ndarray:
+        c = self.codes
+        return c.cpu().numpy() if isinstance(c, torch.Tensor) else np.asarray(c, dtype=np.uint8)
+
+    def __repr__(self) -> str:
+        label = self.spec.label() if self.spec is not None else None
+        return f"QuantizedTensor(shape={self.shape}, spec={label}, nbits={self.nbits})"
+
+
+# ---------------------------------------------------------------------------
+# device plumbing
+
+
+def _cuda_device(device) -> torch.device:
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if dev.type != "cuda":
+        raise UsageError(f"the approx8 B200 codec runs on CUDA devices only, got {dev}")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    return dev
+
+
+_ws_lock = threading.Lock()
+_ws_cache: dict = {}
+
+
+def workspace(device: torch.device, stream: int, nseg: int) -> torch.Tensor:
+    """Zero-filled kernel scratch for (device, stream); the kernels leave it
+    zeroed, so it is allocated once and grown on demand."""
+    need = N.workspace_bytes(nseg)
+    key = (device.index, stream)
+    with _ws_lock:
+        ws = _ws_cache.get(key)
+        if ws is None or ws.numel() < need:
+            ws = torch.zeros(need, dtype=torch.uint8, device=device)
+            _ws_cache[key] = ws
+    return ws
+
+
+def as_device_f32(x, device=None) -> tuple[torch.Tensor, tuple]:
+    """Input to a contiguous float32 CUDA tensor (H2D copy for host data)."""
+    if isinstance(x, torch.Tensor):
+        dev = _cuda_device(x.device if x.is_cuda else device)
+        t = x
+        if t.dtype != torch.float32:
+            t = t.to(torch.float32)
+        t = t.to(dev, non_blocking=True).contiguous()
+        return t, tuple(x.shape)
+    arr = np.asarray(x)
+    shape = tuple(arr.shape)
+    if arr.dtype != np.float32:
+        arr = arr.astype(np.float32)
+    dev = _cuda_device(device)
+    t = torch.from_numpy(np.ascontiguousarray(arr).reshape(-1)).to(dev)
+    return t, shape
+
+
+def round16(n: int) -> int:
+    return (int(n) + 15) // 16 * 16
+
+
+def _stream(dev: torch.device) -> int:
+    return torch.cuda.current_stream(dev).cuda_stream
+
+
+# ---------------------------------------------------------------------------
+# codec entry points
+
+
+def encode_buffer(x, codebook: Codebook, *, device=None, sync: bool = True) -> QuantizedTensor:
+    """Quantise ``x`` to the nearest codebook values (codecs.py:244-269).
+
+    Ties go to the smaller magnitude; the sign bit is set only on non-zero
+    values; non-finite input raises ``InputError``.  With ``sync=False`` the
+    call is fully asynchronous and the check happens when ``scale`` is read.
+    """
+    spec = codebook.spec
+    t, shape = as_device_f32(x, device)
+    dev = t.device
+    n = t.numel()
+    if n == 0:  # codecs.py:257-258
+        s = codebook.fixed_scale
+        return QuantizedTensor(torch.empty(0, dtype=torch.uint8, device=dev), shape, spec,
+                               1.0 if s is None else s)
+    book, lut = codebook.device_tables(dev)
+    with torch.cuda.device(dev):
+        stream = _stream(dev)
+        meta = torch.empty(2, dtype=torch.int32, device=dev)  # both words written by the kernel
+        codes = torch.empty(n, dtype=torch.uint8, device=dev)
+        seg = N.EncSeg(t.data_ptr(), n, 0, 0, 0)
+        lay = N.Layout(codes.data_ptr(), meta.data_ptr() + 4, round16(n), round16(n), 0, 0, 1, 0)
+        ws = workspace(dev, stream, 1)
+        N.check(N.lib.a8_encode(C.byref(seg), 1, book.data_ptr(), spec.norm_code,
+                                None if lut is None else lut.data_ptr(), lay, ws.data_ptr(),
+                                None, meta.data_ptr(), stream))
+    q = QuantizedTensor(codes, shape, spec, scale_tensor=meta[1:].view(torch.float32), meta=meta)
+    q._keepalive = t  # input must outlive the asynchronous kernel
+    if sync:
+        q._finish()
+    return q
+
+
+def decode_buffer(q: QuantizedTensor, codebook: Codebook, *, device=None, out=None) -> torch.Tensor:
+    """Map codes back to float32 values, undoing the scale (codecs.py:272-282)."""
+    if q.nbits != 8:
+        raise UsageError("decode_buffer handles 8-bit tensors; use onebit_decode")
+    if q.spec != codebook.spec:
+        raise UsageError(
+            f"tensor was encoded as {q.spec and q.spec.label()}, codebook is {codebook.spec.label()}"
+        )
+    if isinstance(q.codes, torch.Tensor) and q.codes.is_cuda:
+        dev = q.codes.device
+    else:
+        dev = _cuda_device(device)
+    codes = q.device_codes(dev)
+    n = codes.numel()
+    if n != q.count:
+        raise UsageError(f"codes hold {n} elements, shape {q.shape} needs {q.count}")
+    if out is None:
+        out = torch.empty(q.shape, dtype=torch.float32, device=dev)
+    elif out.dtype != torch.float32 or not out.is_contiguous() or out.numel() != n or out.device != dev:
+        raise UsageError("out must be a contiguous float32 tensor of the decoded size on the codes' device")
+    if n == 0:
+        return out
+    book, _ = codebook.device_tables(dev)
+    with torch.cuda.device(dev):
+        stream = _stream(dev)
+        scale_t = q.device_scale(dev)
+        seg = N.DecSeg(out.data_ptr(), n, 0, 0, 0)
+        lay = N.Layout(codes.data_ptr(), scale_t.data_ptr(), round16(n), round16(n), 0, 0, 1, 0)
+        ws = workspace(dev, stream, 1)
+        N.check(N.lib.a8_decode(C.byref(seg), 1, book.data_ptr(), lay, 1, 0, -1, 0, None,
+                                ws.data_ptr(), stream))
+    return out
+
+
+def roundtrip(x, spec: DataTypeSpec, *, device=None):
+    """encode + decode in one step (codecs.py:285-288).  NumPy in -> NumPy out."""
+    cb = build_codebook(spec)
+    q = encode_buffer(x, cb, device=device, sync=False)
+    y = decode_buffer(q, cb)
+    q._finish()
+    if isinstance(x, torch.Tensor):
+        return y
+    return y.cpu().numpy()

@@ -1,0 +1,182 @@
+// Host+device core of the approx8 B200 codec: decision thresholds and the
+// bucketed decision table.  Compiled into the device kernels AND the host
+// builder, so the CPU tests exercise the same arithmetic the GPU runs.
+//
+// The reference decision (approx8/codecs.py:260-265), for sorted distinct
+// values v_0 = 0 < ... < v_{D-1} and y = fl64(|x| / s):
+//     idx  = clip(searchsorted_left(v, y), 1, D-1)
+//     pick = (fl64(y - v[idx-1]) <= fl64(v[idx] - y)) ? idx-1 : idx
+// pick is monotone in |x|, so pick(|x|) = #{ i : T_i <= bits(|x|) } where T_i
+// is the smallest float32 bit pattern for which the pair (v_i, v_{i+1})
+// resolves upward.  T_i is found by a bracketed bisection using the same
+// float64 operations (IEEE round-to-nearest divide and subtract).
+#pragma once
+
+#include <stdint.h>
+#include <string.h>
+
+#include "approx8_b200.h"
+
+#if defined(__CUDACC__)
+#define A8_HD __host__ __device__ __forceinline__
+#else
+#define A8_HD inline
+#endif
+
+namespace a8 {
+
+constexpr uint32_t kInfBits = 0x7f800000u;
+constexpr int kLutMax = A8_LUT_MAX;
+constexpr int kKeyShift = 16;  // bucket key = top 15 bits of |x| (8 exp + 7 mantissa)
+
+A8_HD double f32bits_to_f64(uint32_t a) {
+    if (a < 0x00800000u) return (double)a * 0x1p-149;  // zero and subnormals, exact
+#if defined(__CUDA_ARCH__)
+    return (double)__uint_as_float(a);
+#else
+    float f;
+    memcpy(&f, &a, 4);
+    return (double)f;
+#endif
+}
+
+A8_HD uint32_t f32_bits(float f) {
+#if defined(__CUDA_ARCH__)
+    return __float_as_uint(f);
+#else
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    return u;
+#endif
+}
+
+A8_HD double div_rn(double a, double b) {
+#if defined(__CUDA_ARCH__)
+    return __ddiv_rn(a, b);
+#else
+    return a / b;
+#endif
+}
+
+A8_HD double sub_rn(double a, double b) {
+#if defined(__CUDA_ARCH__)
+    return __dsub_rn(a, b);
+#else
+    return a - b;
+#endif
+}
+
+// true iff the reference rounds |x| (bit pattern a) above v_lo (codecs.py:263-265)
+A8_HD bool picks_upper(uint32_t a, double s, double v_lo, double v_hi) {
+    const double y = div_rn(f32bits_to_f64(a), s);
+    return !(sub_rn(y, v_lo) <= sub_rn(v_hi, y));
+}
+
+// T_i for the pair (v_lo, v_hi) at scale s (s finite, > 0).
+A8_HD uint32_t threshold(double s, double v_lo, double v_hi) {
+    // guess: the real midpoint times s, as float32; the true threshold is a
+    // few ulps away unless the scale is extreme -> verify the bracket
+    const double m = 0.5 * (v_lo + v_hi) * s;
+    uint32_t g;
+    if (!(m < 3.4028234663852886e38)) {
+        g = kInfBits;
+    } else {
+        g = f32_bits((float)m);
+    }
+    uint32_t lo = g > 16u ? g - 16u : 0u;
+    uint32_t hi = g + 16u < kInfBits ? g + 16u : kInfBits;
+    if ((lo != 0u && picks_upper(lo, s, v_lo, v_hi)) ||
+        (hi != kInfBits && !picks_upper(hi, s, v_lo, v_hi))) {
+        lo = 0u;
+        hi = kInfBits;
+    }
+    while (hi - lo > 1u) {
+        const uint32_t mid = lo + ((hi - lo) >> 1);
+        if (picks_upper(mid, s, v_lo, v_hi))
+            hi = mid;
+        else
+            lo = mid;
+    }
+    return hi;
+}
+
+A8_HD bool scale_ok(float s) {
+    const uint32_t b = f32_bits(s);
+    return b != 0u && b < kInfBits;  // positive, finite, non-zero
+}
+
+// Entries [j0, j1) of the bucket table.  T[0..F) are the finite thresholds
+// (non-decreasing).  Returns false if a bucket holds two distinct thresholds.
+A8_HD bool lut_fill(const uint32_t* T, uint32_t F, const uint8_t* canon, int32_t kbase, uint32_t j0,
+                    uint32_t j1, uint32_t* e) {
+    if (j0 >= j1) return true;
+    // lo = #{T < start of bucket j0}
+    const int64_t k0 = (int64_t)kbase + j0;
+    const uint32_t start0 = k0 <= 0 ? 0u : (uint32_t)(k0 << kKeyShift);
+    uint32_t lo = 0, n = F;
+    while (n > 0) {  // lower_bound
+        const uint32_t half = n >> 1;
+        if (T[lo + half] < start0) {
+            lo += half + 1;
+            n -= half + 1;
+        } else {
+            n = half;
+        }
+    }
+    bool ok = true;
+    for (uint32_t j = j0; j < j1; ++j) {
+        const int64_t k = (int64_t)kbase + j;
+        const uint32_t end = (uint32_t)((k + 1) << kKeyShift);  // k+1 <= 0x7f81
+        uint32_t hi = lo;
+        while (hi < F && T[hi] < end) ++hi;
+        uint32_t v;
+        if (hi == lo) {
+            v = (uint32_t)canon[lo] | ((uint32_t)canon[lo] << 8);
+        } else {
+            if (T[lo] != T[hi - 1]) ok = false;
+            v = (uint32_t)canon[lo] | ((uint32_t)canon[hi] << 8) | ((T[lo] & 0xffffu) << 16);
+        }
+        e[j - j0] = v;
+        lo = hi;
+    }
+    return ok;
+}
+
+// Table geometry from the thresholds: keys [kmin-1, kmax+1].
+A8_HD void lut_geometry(const uint32_t* T, uint32_t F, int32_t* kbase, uint32_t* len) {
+    if (F == 0) {
+        *kbase = 0;
+        *len = 1;
+        return;
+    }
+    const int32_t kmin = (int32_t)(T[0] >> kKeyShift);
+    const int32_t kmax = (int32_t)(T[F - 1] >> kKeyShift);
+    *kbase = kmin - 1;
+    *len = (uint32_t)(kmax - kmin + 3);
+}
+
+// One element: |x| bits -> code via the bucket table (codecs.py:262-268).
+A8_HD uint32_t encode_lut(uint32_t b, const uint32_t* e, int32_t kbase, int32_t lenm1) {
+    const uint32_t a = b & 0x7fffffffu;
+    int32_t j = (int32_t)(a >> kKeyShift) - kbase;
+    j = j < 0 ? 0 : (j > lenm1 ? lenm1 : j);
+    const uint32_t v = e[j];
+    uint32_t c = ((a & 0xffffu) >= (v >> 16)) ? (v >> 8) : v;
+    c &= 0xffu;
+    // sign bit only for non-zero values (codecs.py:267-268); code 0 is the
+    // only zero code, and c + 127 carries into bit 7 iff c != 0
+    return c | ((c + 0x7fu) & (b >> 24) & 0x80u);
+}
+
+// One element by binary search over the padded thresholds (paper's method).
+A8_HD uint32_t encode_search(uint32_t b, const uint32_t* T128, const uint8_t* canon128) {
+    const uint32_t a = b & 0x7fffffffu;
+    uint32_t p = 0;
+#pragma unroll
+    for (uint32_t step = 64; step; step >>= 1)
+        if (T128[p + step - 1] <= a) p += step;
+    const uint32_t c = canon128[p];
+    return c | ((c + 0x7fu) & (b >> 24) & 0x80u);
+}
+
+}  // namespace a8

@@ -1,0 +1,385 @@
+"""Compressed gradient exchange (data parallel) over NCCL, 8-bit on the wire.
+
+The reference has no multi-process exchange: its data-parallel seam rounds
+every W and b gradient through encode->decode just before the optimizer step
+(approx8/mlp.py:167-175, 322-325, 367-369), i.e. it simulates "each GPU
+receives the 8-bit gradients of the others".  This module is that exchange
+for real, one process per GPU:
+
+``allgather`` (north star item 4)
+    every rank encodes each tensor with its own per-tensor scale into one
+    slab [codes of all tensors | scales | status], the slabs are all-gathered
+    in place with NCCL over NVLink, and one fused kernel decodes the N slabs,
+    sums them in rank order in float32 and divides by N.
+    Per-rank ingress (N-1)*n bytes (vs 2(N-1)/N*4n for a ring fp32 all-reduce).
+
+``two_round`` (the paper's scatter + broadcast, PAPER.md:380,
+perfmodel.py:246-273)
+    round 1 all-to-all of 8-bit shards, fused decode-average of the N
+    contributions to the local shard, re-encode of the shard with one scale
+    per (tensor x shard) piece, round 2 all-gather of the 8-bit shards, decode.
+    Per-rank ingress 2(N-1)/N*n bytes.
+
+Exchange semantics (the composed oracles in oracle/approx8_oracle.py):
+  * allgather: out = fl32(sum_r decode(encode(g_r))) / N, rank order;
+  * two_round: out = decode(encode(piece of allgather-average)) per piece;
+  * world size 1: out == roundtrip(g) bit for bit.
+
+The codec work goes through a ``SegmentCodec``; the default is the CUDA
+library.  The orchestration (layouts, collectives, status propagation) is
+independent of it, which is what the CPU gloo tests exercise.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import torch
+import torch.distributed as dist
+
+from . import _native as N
+from .codecs import Codebook, DataTypeSpec, build_codebook, round16, workspace
+from .errors import InputError, UsageError
+
+MODES = ("allgather", "two_round")
+OPS = ("avg", "sum")
+
+
+# ---------------------------------------------------------------------------
+# codec backends
+
+
+class SegmentCodec:
+    """Interface of the codec work the exchange needs.  Buffers are uint8
+    tensors; offsets are bytes; strides follow include/approx8_b200.h."""
+
+    def encode(self, xs, flat_offs, scale_idx, cb: Codebook, buf: torch.Tensor, codes_off: int,
+               scales_off: int, block_len: int, block_stride: int, scale_block_stride: int,
+               reps: int, status_off: int, status_in: Optional[torch.Tensor] = None) -> None:
+        raise NotImplementedError
+
+    def decode(self, outs, flat_offs, scale_idx, cb: Codebook, buf: torch.Tensor, codes_off: int,
+               scales_off: int, block_len: int, block_stride: int, scale_block_stride: int,
+               rank_stride: int, nranks: int, op: int, status_idx: int = -1,
+               status_blocks: int = 0, status_out: Optional[torch.Tensor] = None) -> None:
+        raise NotImplementedError
+
+
+class CudaSegmentCodec(SegmentCodec):
+    """a8_encode / a8_decode on the buffers' device and current stream."""
+
+    def encode(self, xs, flat_offs, scale_idx, cb, buf, codes_off, scales_off, block_len,
+               block_stride, scale_block_stride, reps, status_off, status_in=None):
+        dev = buf.device
+        book, lut = cb.device_tables(dev)
+        n = len(xs)
+        segs = (N.EncSeg * n)()
+        for i, (x, off, si) in enumerate(zip(xs, flat_offs, scale_idx)):
+            segs[i] = N.EncSeg(x.data_ptr(), x.numel(), off, si, 0)
+        base = buf.data_ptr()
+        lay = N.Layout(base + codes_off, base + scales_off, block_len, block_stride,
+                       scale_block_stride, 0, reps, 0)
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        ws = workspace(dev, stream, n)
+        N.check(N.lib.a8_encode(segs, n, book.data_ptr(), cb.spec.norm_code,
+                                None if lut is None else lut.data_ptr(), lay, ws.data_ptr(),
+                                None if status_in is None else status_in.data_ptr(),
+                                base + status_off, stream))
+
+    def decode(self, outs, flat_offs, scale_idx, cb, buf, codes_off, scales_off, block_len,
+               block_stride, scale_block_stride, rank_stride, nranks, op, status_idx=-1,
+               status_blocks=0, status_out=None):
+        dev = buf.device
+        book, _ = cb.device_tables(dev)
+        n = len(outs)
+        segs = (N.DecSeg * max(n, 1))()
+        for i, (o, off, si) in enumerate(zip(outs, flat_offs, scale_idx)):
+            segs[i] = N.DecSeg(o.data_ptr(), o.numel(), off, si, 0)
+        base = buf.data_ptr()
+        lay = N.Layout(base + codes_off, base + scales_off, block_len, block_stride,
+                       scale_block_stride, rank_stride, 1, 0)
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        ws = workspace(dev, stream, max(n, 1))
+        N.check(N.lib.a8_decode(segs, n, book.data_ptr(), lay, nranks, op, status_idx,
+                                status_blocks, None if status_out is None else status_out.data_ptr(),
+                                ws.data_ptr(), stream))
+
+
+# ---------------------------------------------------------------------------
+# collectives
+
+
+class TorchDistComm:
+    """Collectives through ``torch.distributed`` (NCCL over NVLink on the GPU
+    box, gloo in the CPU tests).  NCCL runs the all-gather in place."""
+
+    def __init__(self, group=None):
+        self.group = group
+
+    def world(self):
+        if dist.is_available() and dist.is_initialized():
+            return dist.get_world_size(self.group), dist.get_rank(self.group)
+        return 1, 0
+
+    def _inplace(self) -> bool:
+        return dist.get_backend(self.group) == "nccl"
+
+    def all_gather(self, out: torch.Tensor, slot: torch.Tensor) -> None:
+        dist.all_gather_into_tensor(out, slot if self._inplace() else slot.clone(), group=self.group)
+
+    def all_to_all(self, recv: torch.Tensor, send: torch.Tensor) -> None:
+        dist.all_to_all_single(recv, send, group=self.group)
+
+
+# ---------------------------------------------------------------------------
+# layouts
+
+
+@dataclass
+class Piece:
+    tensor: int  # index of the tensor
+    start: int  # first element inside the tensor
+    n: int
+    flat: int  # global flat index of the first element
+    shard: int
+    idx: int  # scale slot inside its shard's block
+
+
+@dataclass
+class Plan:
+    sizes: tuple
+    nranks: int
+    offs: list  # flat offset of each tensor (multiples of 16)
+    flat: int  # padded flat length (allgather: one block)
+    shard: int  # two_round: elements per shard (multiple of 16)
+    gap: int  # bytes of scale+status area per block
+    nseg: int
+    pieces: list = field(default_factory=list)  # two_round pieces, by shard
+
+    @property
+    def status_slot(self) -> int:  # index (in 4-byte words) of the status word in a scale area
+        return self.nseg
+
+    def allgather_block(self) -> int:
+        return self.flat + self.gap
+
+    def two_round_block(self) -> int:
+        return self.shard + self.gap
+
+
+def make_plan(sizes: Sequence[int], nranks: int) -> Plan:
+    offs, pos = [], 0
+    for n in sizes:
+        offs.append(pos)
+        pos += round16(n)
+    flat = max(pos, 16)
+    unit = 16 * nranks
+    shard = -(-flat // unit) * unit // nranks
+    npieces_max = len(sizes) + nranks
+    gap = round16(4 * (max(len(sizes), npieces_max) + 1))
+    plan = Plan(tuple(sizes), nranks, offs, round16(flat), shard, gap, len(sizes))
+    # two_round pieces: tensor ∩ shard
+    per_shard = [0] * nranks
+    for t, n in enumerate(sizes):
+        a = 0
+        while a < n:
+            f = offs[t] + a
+            j = f // shard
+            b = min(n, (j + 1) * shard - offs[t])
+            plan.pieces.append(Piece(t, a, b - a, f, j, per_shard[j]))
+            per_shard[j] += 1
+            a = b
+    return plan
+
+
+# ---------------------------------------------------------------------------
+# the exchange
+
+
+class GradientExchange:
+    """Compressed all-reduce of a list of float32 tensors (in place by default).
+
+    ``spec``   codec spec (the DP seam default is dynamic-tree/absmax,
+               mlp.py:399-411)
+    ``mode``   "allgather" or "two_round"
+    ``op``     "avg" (data-parallel gradient average) or "sum" (model-parallel
+               error-signal sum)
+    ``check``  "deferred": the non-finite status of call k is checked at call
+               k+1 (or ``synchronize()``) without stalling the stream;
+               "sync": checked before returning; "none".
+    Every rank must call it with the same tensor shapes in the same order.
+    """
+
+    def __init__(self, spec: DataTypeSpec, group=None, mode: str = "allgather", op: str = "avg",
+                 check: str = "deferred", codec: Optional[SegmentCodec] = None, comm=None):
+        if mode not in MODES:
+            raise UsageError(f"mode must be one of {MODES}, got {mode!r}")
+        if op not in OPS:
+            raise UsageError(f"op must be one of {OPS}, got {op!r}")
+        if check not in ("deferred", "sync", "none"):
+            raise UsageError("check must be 'deferred', 'sync' or 'none'")
+        self.spec = spec
+        self.cb = build_codebook(spec)
+        self.group = group
+        self.mode = mode
+        self.op = op
+        self.check = check
+        self.codec = codec or CudaSegmentCodec()
+        self.comm = comm or TorchDistComm(group)
+        self._plans: dict = {}
+        self._bufs: dict = {}
+        self._pending = None  # (event or None, host status tensor)
+        self.calls = 0
+
+    # -- distributed context
+    def _world(self):
+        return self.comm.world()
+
+    def _buffer(self, name: str, nbytes: int, device, dtype=torch.uint8) -> torch.Tensor:
+        key = (name, device)
+        b = self._bufs.get(key)
+        if b is None or b.numel() < nbytes:
+            b = torch.zeros(nbytes, dtype=dtype, device=device)
+            self._bufs[key] = b
+        return b[:nbytes]
+
+    # -- status handling
+    def _collect_status(self, word: torch.Tensor):
+        if self.check == "none":
+            return
+        if word.is_cuda:
+            host = torch.empty(1, dtype=torch.int32, pin_memory=True)
+            host.copy_(word.view(torch.int32)[:1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+        else:
+            host, ev = word.view(torch.int32)[:1].clone(), None
+        self._pending = (ev, host, self.calls)
+        if self.check == "sync":
+            self.synchronize()
+
+    def synchronize(self) -> None:
+        """Wait for the last exchange's status and raise InputError if any
+        rank's input held NaN/Inf (codecs.py:251-252)."""
+        if self._pending is None:
+            return
+        ev, host, call = self._pending
+        self._pending = None
+        if ev is not None:
+            ev.synchronize()
+        if int(host[0]) & N.A8_STATUS_NONFINITE:
+            raise InputError(f"exchange call {call}: cannot encode non-finite values (NaN or Inf present)")
+
+    def _poll(self) -> None:
+        if self._pending is not None:
+            ev = self._pending[0]
+            if ev is None or ev.query():
+                self.synchronize()
+
+    # -- main entry
+    def __call__(self, tensors: Sequence[torch.Tensor], out: Optional[Sequence[torch.Tensor]] = None):
+        tensors = list(tensors)
+        if not tensors:
+            return []
+        self._poll()
+        dev = tensors[0].device
+        for t in tensors:
+            if t.dtype != torch.float32 or not t.is_contiguous() or t.device != dev:
+                raise UsageError("exchange needs contiguous float32 tensors on one device")
+        outs = list(out) if out is not None else tensors
+        nranks, rank = self._world()
+        sizes = tuple(t.numel() for t in tensors)
+        key = (sizes, nranks)
+        plan = self._plans.get(key)
+        if plan is None:
+            plan = self._plans[key] = make_plan(sizes, nranks)
+        if self.mode == "allgather" or nranks == 1:
+            self._allgather(tensors, outs, plan, nranks, rank, dev)
+        else:
+            self._two_round(tensors, outs, plan, nranks, rank, dev)
+        self.calls += 1
+        return outs
+
+    def _allgather(self, xs, outs, plan: Plan, nranks, rank, dev):
+        B = plan.allgather_block()
+        gathered = self._buffer("gather", nranks * B, dev)
+        idx = list(range(plan.nseg))
+        mine = rank * B
+        status_off = plan.flat + 4 * plan.status_slot
+        self.codec.encode(xs, plan.offs, idx, self.cb, gathered, mine, mine + plan.flat,
+                          plan.flat, plan.flat, 0, 1, mine + status_off)
+        if nranks > 1:
+            self.comm.all_gather(gathered, gathered[mine:mine + B])
+        status = self._buffer("status", 4, dev)
+        self.codec.decode(outs, plan.offs, idx, self.cb, gathered, 0, plan.flat, plan.flat,
+                          plan.flat, 0, B, nranks, 1 if self.op == "avg" else 0,
+                          plan.status_slot, 1, status)
+        self._collect_status(status)
+
+    def _two_round(self, xs, outs, plan: Plan, nranks, rank, dev):
+        L = plan.shard
+        B = plan.two_round_block()
+        sbs = B // 4  # scale areas are B bytes apart
+        send = self._buffer("send", nranks * B, dev)
+        recv = self._buffer("recv", nranks * B, dev)
+        idx = list(range(plan.nseg))
+        # round 1: per-tensor encode straight into the N send blocks
+        self.codec.encode(xs, plan.offs, idx, self.cb, send, 0, L, L, B, sbs, nranks,
+                          L + 4 * plan.status_slot)
+        self.comm.all_to_all(recv, send)
+        # decode-average the N contributions to my shard
+        mine = [p for p in plan.pieces if p.shard == rank]
+        shard_buf = self._buffer("shard", max(L, 16) * 4, dev).view(torch.float32)
+        pouts = [shard_buf[p.flat - rank * L: p.flat - rank * L + p.n] for p in mine]
+        poffs = [p.flat - rank * L for p in mine]
+        status1 = self._buffer("status1", 4, dev)
+        self.codec.decode(pouts, poffs, [p.tensor for p in mine], self.cb, recv, 0, L, L, B, 0, B,
+                          nranks, 1 if self.op == "avg" else 0, plan.status_slot, 1, status1)
+        # round 2: re-encode my shard, one scale per piece, into my gather slot
+        gathered = self._buffer("gather2", nranks * B, dev)
+        slot = rank * B
+        status_off = slot + L + 4 * plan.status_slot
+        if mine:
+            # round-1 status is chained into the round-2 word by the kernel
+            self.codec.encode(pouts, poffs, [p.idx for p in mine], self.cb, gathered, slot,
+                              slot + L, L, B, 0, 1, status_off, status_in=status1)
+        else:
+            gathered[status_off:status_off + 4].copy_(status1)
+        self.comm.all_gather(gathered, gathered[slot:slot + B])
+        # final decode of every piece straight into the outputs
+        fouts, foffs, fidx = [], [], []
+        for p in plan.pieces:
+            fouts.append(outs[p.tensor].view(-1)[p.start:p.start + p.n])
+            foffs.append(p.flat)
+            fidx.append(p.idx)
+        status = self._buffer("status", 4, dev)
+        self.codec.decode(fouts, foffs, fidx, self.cb, gathered, 0, L, L, B, sbs, 0, 1, 0,
+                          plan.status_slot, nranks, status)
+        self._collect_status(status)
+
+
+def exchange(tensors, spec: DataTypeSpec, group=None, mode: str = "allgather", op: str = "avg"):
+    """One-shot functional form of ``GradientExchange`` (check="sync")."""
+    return GradientExchange(spec, group, mode, op, check="sync")(tensors)
+
+
+# ---------------------------------------------------------------------------
+# DDP communication hook
+
+
+class DDPHookState:
+    def __init__(self, spec: DataTypeSpec, group=None, mode: str = "allgather"):
+        self.exchange = GradientExchange(spec, group, mode, "avg")
+
+
+def a8_comm_hook(state: DDPHookState, bucket) -> torch.futures.Future:
+    """``DistributedDataParallel.register_comm_hook(state, a8_comm_hook)``:
+    the bucket's per-parameter gradient views are exchanged 8-bit with one
+    scale per parameter (the reference's per-tensor seam, mlp.py:367-369)."""
+    grads = [g for g in bucket.gradients()]
+    state.exchange(grads)
+    fut: torch.futures.Future = torch.futures.Future()
+    fut.set_result(bucket.buffer())
+    return fut

@@ -1,0 +1,117 @@
+"""Hook-seam configuration and GPU seams (reference: approx8/mlp.py).
+
+``HookMode``, ``QuantHookConfig`` and ``default_hook_spec`` keep the names,
+defaults and validation of mlp.py:90-121 and mlp.py:399-411.  The seams are
+the places where a tensor crosses a device boundary:
+
+  * data parallel (mlp.py:367-369): every W/b gradient -> ``GradientExchange``
+    (8-bit all-gather + fused decode-average) instead of an fp32 all-reduce;
+  * model parallel (mlp.py:208-215, 247-249): activations shipped forward and
+    error signals shipped back -> ``make_quantizer`` (encode -> decode round
+    trip on the GPU, the single-process seam) or ``ModelParallelFC`` (the
+    real sharded FC layer of BASELINE config 5).
+
+Hook statistics (mlp.py:140-164) are accumulated on the device.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from enum import Enum
+from typing import Callable, Optional, Union
+
+import torch
+
+from .codecs import DataTypeKind, DataTypeSpec, NormKind, build_codebook, decode_buffer, encode_buffer
+from .errors import ConfigError
+
+ONEBIT = "onebit"
+
+
+class HookMode(str, Enum):
+    NONE = "none"
+    DATA_PARALLEL = "data-parallel"
+    MODEL_PARALLEL = "model-parallel"
+
+
+@dataclass(frozen=True)
+class QuantHookConfig:
+    """What gets quantised during training, and with which codec (mlp.py:97-121)."""
+
+    mode: HookMode = HookMode.NONE
+    spec: Union[DataTypeSpec, str, None] = None  # DataTypeSpec or "onebit"
+
+    def __post_init__(self) -> None:
+        object.__setattr__(self, "mode", HookMode(self.mode))
+        if isinstance(self.spec, str) and self.spec != ONEBIT:
+            raise ConfigError(f"string spec must be {ONEBIT!r}, got {self.spec!r}")
+        if self.spec == ONEBIT and self.mode is HookMode.MODEL_PARALLEL:
+            raise ConfigError("onebit quantization only supports data-parallel mode")
+
+    @property
+    def active(self) -> bool:
+        return self.mode is not HookMode.NONE and self.spec is not None
+
+    def label(self) -> str:
+        if not self.active:
+            return "32-bit"
+        name = ONEBIT if self.spec == ONEBIT else self.spec.label()
+        return f"{name} [{self.mode.value}]"
+
+
+def default_hook_spec(kind: DataTypeKind, mode: HookMode) -> DataTypeSpec:
+    """Normalisation defaults per codec and seam (mlp.py:399-411): tree/linear
+    use absmax; exponent codecs read gradients unscaled and activations with
+    a two-decade offset."""
+    kind = DataTypeKind(kind)
+    if kind in (DataTypeKind.DYNAMIC_TREE, DataTypeKind.LINEAR):
+        return DataTypeSpec(kind, NormKind.ABSMAX)
+    if HookMode(mode) is HookMode.MODEL_PARALLEL:
+        return DataTypeSpec(kind, NormKind.DECADE, 2)
+    return DataTypeSpec(kind, NormKind.NONE)
+
+
+class HookStats:
+    """Per (site, layer) sums of |x - q(x)| and |x - q(x)|/|x| over non-zero
+    x, accumulated on the device (mlp.py:140-164); ``summary`` syncs."""
+
+    def __init__(self) -> None:
+        self._acc: dict = {}
+
+    def record(self, site: str, layer: int, before: torch.Tensor, after: torch.Tensor) -> None:
+        b = before.reshape(-1).to(torch.float64)
+        d = (b - after.reshape(-1).to(torch.float64)).abs()
+        nz = b != 0
+        rel = torch.where(nz, d / b.abs().clamp_min(torch.finfo(torch.float64).tiny), torch.zeros_like(d))
+        row = torch.stack([d.sum(), rel.sum(), nz.sum().to(torch.float64)])
+        key = (site, layer)
+        if key in self._acc:
+            acc, n = self._acc[key]
+            self._acc[key] = (acc + row, n + b.numel())
+        else:
+            self._acc[key] = (row, b.numel())
+
+    def summary(self) -> dict:
+        out: dict = {}
+        for (site, layer) in sorted(self._acc):
+            row, n = self._acc[(site, layer)]
+            abs_sum, rel_sum, nnz = (float(v) for v in row.cpu())
+            out.setdefault(site, []).append(
+                (abs_sum / n if n else 0.0, 100.0 * rel_sum / nnz if nnz else 0.0)
+            )
+        return out
+
+
+def make_quantizer(spec: DataTypeSpec, stats: Optional[HookStats] = None, site: str = "gradient") -> Callable:
+    """GPU form of ``_make_quantizer`` (mlp.py:167-175): returns
+    ``quantize(x, layer) -> decode(encode(x))`` running in the sm_100a kernels."""
+    cb = build_codebook(spec)
+
+    def quantize(x: torch.Tensor, layer: int) -> torch.Tensor:
+        q = encode_buffer(x, cb, sync=False)
+        y = decode_buffer(q, cb).to(x.dtype)
+        if stats is not None:
+            stats.record(site, layer, x, y)
+        return y
+
+    return quantize

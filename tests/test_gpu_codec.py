@@ -1,0 +1,224 @@
+"""GPU parity of the sm_100a codec against the reference goldens and the oracle.
+
+Bar: codes bit-exact; scales bit-exact; decoded values bit-exact (a single
+float32 round-to-nearest multiply, codecs.py:281).  Sizes run from the
+reference's own cases up to BASELINE config sizes, where size-independent
+properties (sign symmetry, idempotence, order, power-of-two invariance,
+oracle agreement on large seeded inputs) are checked.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from helpers import O, acceptance_inputs, fullrange_cases, golden, golden_cases, sha, tag
+
+import paper_1511_04561_b200 as A
+
+pytestmark = pytest.mark.gpu
+
+ALL_SPECS = [("dynamic-tree", "none", 0), ("dynamic-tree", "absmax", 0), ("linear", "none", 0),
+             ("linear", "absmax", 0), ("static-tree", "none", 0), ("static-tree", "decade", 1),
+             ("mantissa", "none", 0), ("mantissa", "decade", 2), ("mantissa", "decade", -1)]
+
+
+def S(spec):
+    return A.DataTypeSpec(*spec)
+
+
+def enc(x, spec, dev):
+    cb = A.build_codebook(S(spec))
+    q = A.encode_buffer(torch.from_numpy(np.ascontiguousarray(x)).to(dev), cb)
+    return q.codes.cpu().numpy(), q.scale, q, cb
+
+
+@pytest.mark.parametrize("case", golden_cases(), ids=lambda c: c[0])
+def test_codes_match_reference_vectors(case, cuda):
+    name, spec, x, ref = case
+    codes, s, q, cb = enc(x, spec, cuda)
+    assert np.array_equal(codes, ref), f"{name}: {(codes != ref).sum()} mismatches"
+    assert s == O.encode(x, *spec)[1]
+    dec = A.decode_buffer(q, cb).cpu().numpy()
+    assert dec.tobytes() == O.decode(ref, s, spec[0]).tobytes(), name
+
+
+def test_fullrange_buffers(cuda):
+    for base, spec, xs, cs, scales in fullrange_cases():
+        for x, c, s in zip(xs, cs, scales):
+            codes, gs, _, _ = enc(x, spec, cuda)
+            assert np.array_equal(codes, c), base
+            assert gs == s, base
+
+
+def test_acceptance_100k_digests(cuda):
+    """test_acceptance.py:116-129 inputs, compared by digest with the reference."""
+    _, meta = golden()
+    for spec, x in acceptance_inputs():
+        m = meta["acceptance"][tag(spec)]
+        codes, s, q, cb = enc(x, spec, cuda)
+        assert sha(codes) == m["sha_codes"], tag(spec)
+        assert s == m["scale"]
+        assert sha(A.decode_buffer(q, cb).cpu().numpy()) == m["sha_decoded"], tag(spec)
+
+
+def test_config1_digests(cuda):
+    """BASELINE config 1: errorbench.sample(normal, 2**20, seed 0)."""
+    _, meta = golden()
+    x = O.sample_normal(2**20, 0)
+    for t, m in meta["c1"].items():
+        if t == "sha_x":
+            continue
+        kind, norm = t.split("/")
+        spec = (kind, "decade", int(norm[6:])) if norm.startswith("decade") else (kind, norm, 0)
+        codes, s, q, cb = enc(x, spec, cuda)
+        assert sha(codes) == m["sha_codes"], t
+        assert s == m["scale"], t
+        assert sha(A.decode_buffer(q, cb).cpu().numpy()) == m["sha_decoded"], t
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 15, 16, 17, 63, 1000, 4095, 4096, 4097, 8191, 12289,
+                               65536 + 7, 2**20 + 3])
+@pytest.mark.parametrize("spec", [ALL_SPECS[1], ALL_SPECS[3], ALL_SPECS[5], ALL_SPECS[7]], ids=tag)
+def test_sizes_and_tails(n, spec, cuda):
+    rng = np.random.default_rng(n)
+    x = (rng.normal(size=n) * 10.0 ** rng.integers(-6, 2, size=n)).astype(np.float32)
+    codes, s, q, cb = enc(x, spec, cuda)
+    ref, rs = O.encode(x, *spec)
+    assert s == rs
+    assert np.array_equal(codes, ref)
+    assert A.decode_buffer(q, cb).cpu().numpy().tobytes() == O.decode(ref, s, spec[0]).tobytes()
+
+
+@pytest.mark.parametrize("spec", ALL_SPECS, ids=tag)
+def test_peak_position_and_misaligned_views(spec, cuda):
+    rng = np.random.default_rng(11)
+    base = rng.normal(size=3 * 4096 + 50).astype(np.float32)
+    for pos in (0, 4095, 4096, 12287, base.size - 1):
+        x = base.copy()
+        x[pos] = -7.5  # the peak in different chunks, including the tail
+        codes, s, _, _ = enc(x, spec, cuda)
+        assert np.array_equal(codes, O.encode(x, *spec)[0]), pos
+    t = torch.from_numpy(base).to(cuda)
+    for off in (1, 2, 3, 5):  # not 16-byte aligned: scalar path
+        v = t[off:]
+        cb = A.build_codebook(S(spec))
+        q = A.encode_buffer(v, cb)
+        assert np.array_equal(q.codes.cpu().numpy(), O.encode(base[off:], *spec)[0]), off
+
+
+def test_empty_zero_and_shape(cuda):
+    cb = A.build_codebook(A.DataTypeSpec("linear", "absmax"))
+    q = A.encode_buffer(torch.empty((0, 3), device=cuda), cb)
+    assert q.codes.numel() == 0 and q.scale == 1.0
+    assert tuple(A.decode_buffer(q, cb).shape) == (0, 3)
+    cbd = A.build_codebook(A.DataTypeSpec("mantissa", "decade", 2))
+    assert A.encode_buffer(torch.empty(0, device=cuda), cbd).scale == np.float32(100.0)
+    for spec in ALL_SPECS:
+        cb = A.build_codebook(S(spec))
+        q = A.encode_buffer(torch.zeros(4097, device=cuda), cb)
+        assert int(q.codes.max()) == 0
+        if spec[1] == "absmax":
+            assert q.scale == 1.0
+        assert float(A.decode_buffer(q, cb).abs().max()) == 0.0
+    cb = A.build_codebook(A.DataTypeSpec("mantissa"))
+    x = torch.randn(3, 4, 5, device=cuda)
+    q = A.encode_buffer(x, cb)
+    assert q.shape == (3, 4, 5) and tuple(A.decode_buffer(q, cb).shape) == (3, 4, 5)
+
+
+@pytest.mark.parametrize("spec", [ALL_SPECS[1], ALL_SPECS[2], ALL_SPECS[5]], ids=tag)
+@pytest.mark.parametrize("pos", [0, 3, 4096 + 17, 3 * 4096 + 2])
+@pytest.mark.parametrize("bad", [float("nan"), float("inf"), float("-inf")])
+def test_non_finite_raises_input_error(spec, pos, bad, cuda):
+    x = torch.randn(3 * 4096 + 5, device=cuda)
+    x[pos] = bad
+    cb = A.build_codebook(S(spec))
+    with pytest.raises(A.InputError):
+        A.encode_buffer(x, cb)
+    # the next call on the same workspace is clean again
+    q = A.encode_buffer(torch.ones(8, device=cuda), cb)
+    assert q.scale > 0
+
+
+def test_spec_mismatch_raises_usage_error(cuda):
+    cb_lin = A.build_codebook(A.DataTypeSpec("linear"))
+    cb_dyn = A.build_codebook(A.DataTypeSpec("dynamic-tree"))
+    q = A.encode_buffer(torch.tensor([0.5], device=cuda), cb_lin)
+    with pytest.raises(A.UsageError):
+        A.decode_buffer(q, cb_dyn)
+
+
+def test_tie_breaks_toward_smaller_and_table_identity(cuda):
+    cb = A.build_codebook(A.DataTypeSpec("linear"))
+    mid = float(cb.sorted_values[1]) / 2.0
+    q = A.encode_buffer(torch.tensor([mid, -mid], device=cuda), cb)
+    assert q.codes.tolist() == [0, 0]
+    for kind in ("dynamic-tree", "static-tree", "linear", "mantissa"):
+        spec = A.DataTypeSpec(kind)
+        v = torch.from_numpy(A.build_codebook(spec).decode_table.copy()).to(cuda)
+        assert torch.equal(A.roundtrip(v, spec), v), kind
+
+
+@pytest.mark.parametrize("spec", ALL_SPECS, ids=tag)
+def test_properties_on_random_buffers(spec, cuda):
+    """test_properties.py:50-102 invariants on many random buffers."""
+    rng = np.random.default_rng(hash(tag(spec)) % 2**32)
+    cb = A.build_codebook(S(spec))
+    for n in (1, 7, 24, 333, 5000):
+        x = (rng.normal(size=n) * 10.0 ** rng.integers(-8, 3, size=n)).astype(np.float32)
+        t = torch.from_numpy(x).to(cuda)
+        pos = A.encode_buffer(t, cb).codes
+        neg = A.encode_buffer(-t, cb).codes
+        zero = pos == 0
+        assert torch.equal(neg[zero], pos[zero]) and torch.equal(neg[~zero], pos[~zero] ^ 0x80)
+        assert torch.equal(A.encode_buffer(t.clone(), cb).codes, pos)  # purity
+        srt = torch.sort(t).values
+        d = A.roundtrip(srt, cb.spec)
+        assert bool((d[1:] >= d[:-1]).all())  # order preservation
+        if spec[1] != "absmax":
+            once = A.roundtrip(t, cb.spec)
+            assert torch.equal(A.roundtrip(once, cb.spec), once)  # idempotence
+        else:
+            for f in (0.25, 2.0, 1024.0):
+                assert torch.equal(A.encode_buffer(t * f, cb).codes, pos)
+
+
+@pytest.mark.parametrize("spec", [ALL_SPECS[1], ALL_SPECS[3], ALL_SPECS[5], ALL_SPECS[7]], ids=tag)
+def test_large_seeded_buffer_matches_oracle(spec, cuda):
+    """2^24 + 5 elements (multi-wave persistent grid) vs the oracle."""
+    x = O.sample_normal(2**24 + 5, 7, 0.0, 0.01)
+    codes, s, q, cb = enc(x, spec, cuda)
+    ref, rs = O.encode(x, *spec)
+    assert s == rs
+    assert np.array_equal(codes, ref)
+
+
+def test_roundtrip_numpy_in_numpy_out(cuda):
+    x = O.sample_normal(10000, 1)
+    y = A.roundtrip(x, A.DataTypeSpec("dynamic-tree", "absmax"))
+    assert isinstance(y, np.ndarray) and y.dtype == np.float32
+    assert y.tobytes() == O.roundtrip(x, "dynamic-tree", "absmax").tobytes()
+
+
+def test_error_suite_cells_on_gpu(cuda):
+    """Error bench cells (errorbench.py:79-99) from GPU round trips equal the
+    reference's published-protocol numbers exactly."""
+    _, meta = golden()
+    cells = {(c["seed"]): c for c in meta["suite"]}
+    for seed, kind, spec in [(0, "dynamic-tree", ("dynamic-tree", "absmax", 0)),
+                             (1, "linear", ("linear", "absmax", 0)),
+                             (6, "mantissa", ("mantissa", "decade", 1)),
+                             (11, "static-tree", ("static-tree", "decade", 2))]:
+        c = cells[seed]
+        assert c["spec"] == tag(spec)
+        d_idx = seed // 4
+        sigma = [None, 1.0, 10.0, 0.2][d_idx]
+        x = O.sample_uniform01(1_000_000, seed) if d_idx == 0 else O.sample_normal(1_000_000, seed, 0.0, sigma)
+        y = A.roundtrip(x, S(spec)).astype(np.float64)
+        x64 = x.astype(np.float64)
+        err = np.abs(x64 - y)
+        nz = x64 != 0
+        assert float(err.mean()) == c["mean_abs_error"]
+        assert float(np.mean(err[nz] / np.abs(x64[nz])) * 100.0) == c["mean_rel_error_pct"]

@@ -1,0 +1,132 @@
+"""GPU parity of the compressed exchange (allgather / two_round, avg / sum).
+
+One GPU: N ranks are simulated as N threads (``ThreadComm``) that each drive
+the real CUDA codec on the same device; the collectives are buffer copies.
+The result must equal the composed oracle (oracle.exchange_*) -- bit-exact in
+practice; the contract tolerance is 1e-6 relative in float32, written below.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from helpers import O, run_virtual_ranks
+
+import paper_1511_04561_b200 as A
+
+pytestmark = pytest.mark.gpu
+
+ALEXNET = [(64, 3, 11, 11), (64,), (192, 64, 5, 5), (192,), (384, 192, 3, 3), (384,),
+           (256, 384, 3, 3), (256,), (256, 256, 3, 3), (256,), (4096, 9216), (4096,),
+           (4096, 4096), (4096,), (1000, 4096), (1000,)]
+SMALL = [(40, 30), (1,), (17,), (0,), (300,), (4, 4, 4), (5000,), (70000,)]
+RTOL = 1e-6  # north-star tolerance for averaged outputs (float32)
+
+
+def grads(rank, sizes, seed=0, sigma=1e-2):
+    rng = np.random.default_rng(seed * 1000 + rank)
+    return [rng.normal(0.0, sigma, size=s).astype(np.float32) for s in sizes]
+
+
+def close(a, b):
+    a64, b64 = a.astype(np.float64), b.astype(np.float64)
+    return bool(np.all(np.abs(a64 - b64) <= RTOL * np.abs(b64) + 1e-45))
+
+
+def run(nranks, sizes, spec, mode, op, cuda, seed=0):
+    def body(rank, comm):
+        ex = A.GradientExchange(spec, mode=mode, op=op, check="sync", comm=comm)
+        ts = [torch.from_numpy(g).to(cuda) for g in grads(rank, sizes, seed)]
+        ex(ts)
+        torch.cuda.synchronize()
+        return [t.cpu().numpy() for t in ts]
+
+    res = run_virtual_ranks(nranks, body)
+    g = [grads(r, sizes, seed) for r in range(nranks)]
+    fn = O.exchange_allgather if mode == "allgather" else O.exchange_two_round
+    want = fn(g, spec.kind.value, spec.normalization.value, spec.decades, op)
+    return res, want
+
+
+def test_world_size_one_is_roundtrip(cuda):
+    spec = A.DataTypeSpec("dynamic-tree", "absmax")
+    ex = A.GradientExchange(spec, check="sync")
+    gs = grads(0, SMALL + ALEXNET[:4])
+    ts = [torch.from_numpy(g).to(cuda) for g in gs]
+    ex(ts)
+    for t, g in zip(ts, gs):
+        assert t.cpu().numpy().tobytes() == O.roundtrip(g, "dynamic-tree", "absmax").tobytes()
+
+
+@pytest.mark.parametrize("nranks", [2, 4, 8])
+@pytest.mark.parametrize("mode", ["allgather", "two_round"])
+@pytest.mark.parametrize("op", ["avg", "sum"])
+def test_virtual_ranks_match_oracle(nranks, mode, op, cuda):
+    spec = A.DataTypeSpec("dynamic-tree", "absmax")
+    res, want = run(nranks, SMALL, spec, mode, op, cuda)
+    for r in range(nranks):
+        for a, b in zip(res[r], want):
+            assert a.shape == b.shape
+            assert close(a, b), (r, mode, op)
+            assert a.tobytes() == b.tobytes(), (r, mode, op)  # bit-exact in practice
+
+
+@pytest.mark.parametrize("spec", [A.DataTypeSpec("linear", "absmax"), A.DataTypeSpec("mantissa", "none"),
+                                  A.DataTypeSpec("static-tree", "decade", -2)], ids=lambda s: s.label())
+def test_other_specs_three_ranks(spec, cuda):
+    for mode in ("allgather", "two_round"):
+        res, want = run(3, SMALL, spec, mode, "avg", cuda, seed=4)
+        for r in range(3):
+            for a, b in zip(res[r], want):
+                assert a.tobytes() == b.tobytes(), (spec.label(), mode, r)
+
+
+def test_alexnet_shapes_two_ranks(cuda):
+    spec = A.DataTypeSpec("dynamic-tree", "absmax")
+    for mode in ("allgather", "two_round"):
+        res, want = run(2, ALEXNET, spec, mode, "avg", cuda, seed=9)
+        for r in range(2):
+            for a, b in zip(res[r], want):
+                assert a.tobytes() == b.tobytes(), (mode, r)
+
+
+@pytest.mark.parametrize("mode", ["allgather", "two_round"])
+def test_non_finite_raises_on_every_rank(mode, cuda):
+    spec = A.DataTypeSpec("dynamic-tree", "absmax")
+
+    def body(rank, comm):
+        ex = A.GradientExchange(spec, mode=mode, check="sync", comm=comm)
+        ts = [torch.from_numpy(g).to(cuda) for g in grads(rank, SMALL)]
+        if rank == 2:
+            ts[6][123] = float("inf")
+        try:
+            ex(ts)
+        except A.InputError:
+            return "raised"
+        return "ok"
+
+    assert run_virtual_ranks(4, body) == ["raised"] * 4
+
+
+def test_many_segments_use_device_plan(cuda):
+    """> 48 tensors: descriptors go through the workspace instead of the launch."""
+    spec = A.DataTypeSpec("dynamic-tree", "absmax")
+    sizes = [(int(n),) for n in np.random.default_rng(2).integers(1, 3000, size=130)]
+    res, want = run(2, sizes, spec, "allgather", "avg", cuda, seed=5)
+    for r in range(2):
+        for a, b in zip(res[r], want):
+            assert a.tobytes() == b.tobytes()
+
+
+def test_model_parallel_quantizer_seam(cuda):
+    """mlp.py:167-175 seam on the GPU: quantize(x) == roundtrip, stats recorded."""
+    spec = A.default_hook_spec("dynamic-tree", "model-parallel")
+    stats = A.HookStats()
+    qz = A.make_quantizer(spec, stats, "forward")
+    x = torch.relu(torch.randn(128, 512, device=cuda))
+    y = qz(x, 1)
+    assert torch.equal(y, A.roundtrip(x, spec))
+    s = stats.summary()["forward"][0]
+    assert s[0] > 0 and 0 < s[1] < 5
