@@ -1,6 +1,6 @@
 // approx8 B200 kernels (sm_100a) and their C-ABI launchers.
 //
-//   a8_encode  -- K1+K2+K3 fused into one persistent kernel:
+//   a8_encode  -- K1+K2+K3 fused into one persistent, warp-specialised kernel:
 //                 segmented max-abs (+ non-finite detection), per-scale
 //                 decision thresholds and bucket table, then the encode.
 //                 Replaces encode_buffer (approx8/codecs.py:244-269).
@@ -14,26 +14,39 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <deque>
 #include <mutex>
 #include <string>
 #include <vector>
 
 #include "a8_core.cuh"
+#include "a8_ptx.cuh"
 #include "approx8_b200.h"
 
 namespace a8 {
 int fail(int code, const char* msg);
 extern thread_local std::string g_last_error;
 
-constexpr int kEncThreads = 256;
+// ---- encode geometry ---------------------------------------------------------
+constexpr int kConsumerWarps = 8;
+constexpr int kConsumers = kConsumerWarps * 32;  // threads doing reduce / encode
+constexpr int kEncThreads = kConsumers + 32;     // + one producer warp
+constexpr int kStages = 5;                       // bulk-copy ring depth per CTA
+constexpr int kChunk = 4096;                     // elements per stage (16 KB)
+constexpr int kBarC = 1;                         // named barrier of the consumer warps
+constexpr int64_t kBigSeg = 2 << 20;             // segments >= this run A then E back to back
+constexpr int kLag = 2;                          // small segments: E(s) after A(s + kLag)
+constexpr size_t kEncDynSmem = (size_t)kStages * kChunk * sizeof(float);
+
+// ---- decode geometry ---------------------------------------------------------
 constexpr int kDecThreads = 256;
-constexpr int kGroups = 4;                          // float4 groups per thread per chunk
-constexpr int kChunk = kEncThreads * kGroups * 4;   // 4096 elements
+constexpr int kGroups = 4;
 constexpr int kDecChunk = kDecThreads * kGroups * 4;
-constexpr int kInlineSegs = 48;
-constexpr int kLag = 2;        // E(s) is scheduled after A(s + kLag)
-constexpr int kDecRep = 4;     // replicated decode tables (bank-conflict relief)
+constexpr int kDecRep = 4;  // replicated decode tables (bank-conflict relief)
 constexpr int kMaxRanks = 16;
+
+constexpr int kInlineSegs = 48;
+constexpr int kInlineBlks = 2 * kInlineSegs + 1;
 
 // ---------------------------------------------------------------------------
 // device-side plan / workspace
@@ -45,7 +58,14 @@ struct EncSegD {
     int32_t scale_idx;
     int32_t nA;       // absmax chunks (0 for fixed scales)
     int32_t nE;       // encode chunks
-    int32_t aligned;  // x is 16-byte aligned
+    int32_t aligned;  // x is 16-byte aligned (bulk copies allowed)
+};
+
+// A contiguous run of tickets: all A-chunks or all E-chunks of one segment.
+struct EncBlk {
+    int64_t tstart;
+    int32_t seg;
+    int32_t kind;  // 0 = A (max-abs), 1 = E (encode, chunks in reverse order)
 };
 
 struct DecSegD {
@@ -81,14 +101,14 @@ struct EncParams {
     const unsigned int* status_in;
     unsigned int* status_out;
     const EncSegD* segs_dev;
-    const int64_t* bstart_dev;
+    const EncBlk* blks_dev;
     int nseg;
     int nblk;
-    int lag;
     int absmax;
+    int pad;
     int64_t total;
     EncSegD segs[kInlineSegs];
-    int64_t bstart[kInlineSegs + kLag + 1];
+    EncBlk blks[kInlineBlks];
 };
 
 struct DecParams {
@@ -111,66 +131,37 @@ static size_t ctl_off() { return sizeof(WsHead); }
 static size_t lut_off(int nseg) { return align_up(ctl_off() + sizeof(SegCtl) * (size_t)nseg, 256); }
 static size_t plan_off(int nseg) { return align_up(lut_off(nseg) + sizeof(a8_lut_t) * (size_t)nseg, 256); }
 static size_t plan_bytes(int nseg) {
-    const size_t enc = sizeof(EncSegD) * (size_t)nseg + sizeof(int64_t) * (size_t)(nseg + kLag + 1);
+    const size_t enc = sizeof(EncSegD) * (size_t)nseg + sizeof(EncBlk) * (size_t)(2 * nseg + 1);
     const size_t dec = sizeof(DecSegD) * (size_t)nseg;
     return align_up(std::max(enc, dec), 256);
 }
 
 // ---------------------------------------------------------------------------
-// memory helpers
+// K2: thresholds + bucket table for one scale, built by the consumer warps
+// into global memory (`dst`), staged through shared memory.
 
-__device__ __forceinline__ float4 ld_stream(const float* p) {
-    float4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                 : "l"(p));
-    return v;
-}
-
-__device__ __forceinline__ unsigned int ld_stream_u32(const uint8_t* p) {
-    unsigned int v;
-    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
-    return v;
-}
-
-__device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
-    unsigned int v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-__device__ __forceinline__ void st_release(unsigned int* p, unsigned int v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-// ---------------------------------------------------------------------------
-// K2: thresholds + bucket table for one scale, built by one whole CTA into
-// global memory (`dst`), staged through shared memory.
-
-__device__ void build_lut_cta(const a8_book_t* book, float scale, a8_lut_t* dst, uint32_t* sT,
-                              uint8_t* sCanon) {
-    const int tid = threadIdx.x;
+__device__ void build_lut(const a8_book_t* book, float scale, a8_lut_t* dst, uint32_t* sT, uint8_t* sCanon,
+                          int ctid) {
     const int D = book->ndistinct;
-    if (tid < 128) {
-        sCanon[tid] = book->codes[tid];
+    if (ctid < 128) {
+        sCanon[ctid] = book->codes[ctid];
         uint32_t t = kInfBits;
-        if (scale_ok(scale) && tid + 1 < D)
-            t = threshold((double)scale, book->values[tid], book->values[tid + 1]);
-        sT[tid] = t;
+        if (scale_ok(scale) && ctid + 1 < D) t = threshold((double)scale, book->values[ctid], book->values[ctid + 1]);
+        sT[ctid] = t;
     }
-    const int F = __syncthreads_count(tid < 127 && sT[tid < 128 ? tid : 0] < kInfBits);
+    const int F = nbar_popc(kBarC, kConsumers, ctid < 127 && sT[ctid < 128 ? ctid : 0] < kInfBits);
     int32_t kbase;
     uint32_t len;
     lut_geometry(sT, (uint32_t)F, &kbase, &len);
     bool ok = true;
     if (len <= (uint32_t)kLutMax) {
-        const uint32_t per = (len + blockDim.x - 1) / blockDim.x;
-        const uint32_t j0 = min(len, per * tid), j1 = min(len, j0 + per);
+        const uint32_t per = (len + kConsumers - 1) / kConsumers;
+        const uint32_t j0 = min(len, per * ctid), j1 = min(len, j0 + per);
         ok = lut_fill(sT, (uint32_t)F, sCanon, kbase, j0, j1, dst->e + j0);
     }
-    const int valid = __syncthreads_and(ok) && len <= (uint32_t)kLutMax;
-    if (tid < 128) dst->T[tid] = sT[tid];
-    if (tid == 0) {
+    const int valid = nbar_and(kBarC, kConsumers, ok) && len <= (uint32_t)kLutMax;
+    if (ctid < 128) dst->T[ctid] = sT[ctid];
+    if (ctid == 0) {
         dst->len = len;
         dst->kbase = kbase;
         dst->valid = valid;
@@ -179,216 +170,259 @@ __device__ void build_lut_cta(const a8_book_t* book, float scale, a8_lut_t* dst,
     }
 }
 
-// Copy a table into shared memory (readers bypass L1: the table may have
-// been written by another CTA of this launch).
+// Copy a table into shared memory.  Readers bypass L1: the table may have
+// been written by another CTA of this launch.
 __device__ void load_lut_smem(const a8_lut_t* src, uint32_t* sE, uint32_t* sT, uint8_t* sCanon,
-                              const a8_book_t* book, int* sHdr) {
-    const int tid = threadIdx.x;
+                              const a8_book_t* book, int* sHdr, int ctid, int nthreads) {
     const uint32_t len = __ldcg(&src->len);
     const uint32_t valid = __ldcg(&src->valid);
     if (valid) {
-        for (uint32_t j = tid; j < len; j += blockDim.x) sE[j] = __ldcg(&src->e[j]);
-    } else if (tid < 128) {
-        sT[tid] = __ldcg(&src->T[tid]);
-        sCanon[tid] = book->codes[tid];
+        for (uint32_t j = ctid; j < len; j += nthreads) sE[j] = __ldcg(&src->e[j]);
+    } else if (ctid < 128) {
+        sT[ctid] = __ldcg(&src->T[ctid]);
+        sCanon[ctid] = book->codes[ctid];
     }
-    if (tid == 0) {
+    if (ctid == 0) {
         sHdr[0] = (int)valid;
         sHdr[1] = __ldcg(&src->kbase);
         sHdr[2] = (int)len - 1;
     }
 }
 
-// ---------------------------------------------------------------------------
-// K1+K2+K3: persistent encode.  Work items ("tickets") are handed out in a
-// fixed order by an atomic counter:  block b = [A-chunks of segment b]
-// followed by [E-chunks of segment b - lag].  A-chunks reduce max|x| into the
-// segment; the CTA finishing the last A-chunk builds that segment's table and
-// publishes it; E-chunks wait for the table (it is always produced by a
-// lower ticket, so the wait cannot deadlock) and encode.  E-chunks of a
-// segment run in reverse order so the most recently read data (still in L2)
-// is re-read first.
+struct StageMeta {
+    int64_t base;  // first element of the chunk inside its segment
+    int32_t cnt;   // elements in the chunk
+    int32_t bulk;  // leading elements delivered to shared memory by the bulk copy
+    int32_t seg;
+    int32_t kind;  // 0 A, 1 E, 2 end
+};
 
-__global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_constant__ EncParams p) {
+// ---------------------------------------------------------------------------
+// K1+K2+K3: persistent encode.
+//
+// Work items ("tickets", one 4096-element chunk each) are taken in a fixed
+// global order by an atomic counter.  The host builds the order as blocks of
+// A-chunks (max-abs) and E-chunks (encode) per segment.  Warp 0 (producer)
+// takes tickets and streams each chunk global->shared with a bulk async copy
+// into a kStages-deep ring guarded by mbarriers; warps 1..8 (consumers)
+// reduce or encode from shared memory.  The CTA finishing a segment's last
+// A-chunk builds that segment's threshold table and publishes it; E-chunks
+// wait for the table.  Every wait is on a strictly lower ticket, so the
+// schedule cannot deadlock; the producer keeps prefetching while consumers
+// wait, so HBM stays busy.  E-chunks run in reverse order so the data most
+// recently read by the A pass (still in L2) is re-read first.
+
+__global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_constant__ EncParams p) {
+    extern __shared__ __align__(128) float sStage[];  // [kStages][kChunk]
     __shared__ uint32_t sE[kLutMax];
     __shared__ uint32_t sT[128];
     __shared__ uint8_t sCanon[128];
+    __shared__ __align__(8) uint64_t sFull[kStages];
+    __shared__ __align__(8) uint64_t sEmpty[kStages];
+    __shared__ StageMeta sMeta[kStages];
     __shared__ int sHdr[4];
-    __shared__ int64_t sTicket;
-    __shared__ unsigned int sRed[kEncThreads / 32];
+    __shared__ unsigned int sRed[kConsumerWarps];
     __shared__ int sLast;
+    __shared__ int sFinal;
 
     const int tid = threadIdx.x;
+    const int warp = tid >> 5;
     const int lane = tid & 31;
     const EncSegD* segs = p.segs_dev ? p.segs_dev : p.segs;
-    const int64_t* bstart = p.bstart_dev ? p.bstart_dev : p.bstart;
-    int cur = -1;  // segment whose table is in shared memory
+    const EncBlk* blks = p.blks_dev ? p.blks_dev : p.blks;
 
-    const uint8_t* codes_base = p.lay.codes;
-    const int64_t L = p.lay.block_len;
-    const int64_t gap = p.lay.block_stride - p.lay.block_len;
-
-    if (!p.absmax) {  // fixed scale: one table for every segment
-        load_lut_smem(p.static_lut, sE, sT, sCanon, p.book, sHdr);
-        __syncthreads();
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&sFull[s], 1);
+            mbar_init(&sEmpty[s], kConsumerWarps);
+        }
+        mbar_fence_init();
     }
+    if (!p.absmax && tid >= 32)  // fixed scale: one table for every segment
+        load_lut_smem(p.static_lut, sE, sT, sCanon, p.book, sHdr, tid - 32, kConsumers);
+    __syncthreads();
 
-    for (;;) {
-        if (tid == 0) sTicket = (int64_t)atomicAdd(&p.head->ticket, 1u);
-        __syncthreads();
-        const int64_t t = sTicket;
-        __syncthreads();
-        if (t >= p.total) break;
-
-        // locate the block holding ticket t (uniform across the CTA)
-        int lo = 0, hi = p.nblk;  // bstart[lo] <= t < bstart[hi]
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (bstart[mid] <= t)
-                lo = mid;
-            else
-                hi = mid;
-        }
-        const int b = lo;
-        int64_t k = t - bstart[b];
-        const int nA_b = b < p.nseg ? segs[b].nA : 0;
-
-        if (k < nA_b) {
-            // ---------------- A: max-abs over one chunk --------------------
-            const EncSegD sg = segs[b];
-            const int64_t base = k * kChunk;
-            const int64_t cnt = min((int64_t)kChunk, sg.n - base);
-            unsigned int m = 0;
-            if (cnt == kChunk && sg.aligned) {
-                float4 v[kGroups];
-#pragma unroll
-                for (int q = 0; q < kGroups; ++q)
-                    v[q] = ld_stream(sg.x + base + q * (kEncThreads * 4) + tid * 4);
-#pragma unroll
-                for (int q = 0; q < kGroups; ++q) {
-                    m = max(m, __float_as_uint(v[q].x) & 0x7fffffffu);
-                    m = max(m, __float_as_uint(v[q].y) & 0x7fffffffu);
-                    m = max(m, __float_as_uint(v[q].z) & 0x7fffffffu);
-                    m = max(m, __float_as_uint(v[q].w) & 0x7fffffffu);
+    if (warp == 0) {
+        // ===================== producer =====================
+        if (lane == 0) {
+            const uint64_t keep = policy_evict_last();   // A reads: keep for the E re-read
+            const uint64_t drop = policy_evict_first();  // E reads: last use
+            for (int it = 0;; ++it) {
+                const int st = it % kStages;
+                mbar_wait(&sEmpty[st], ((it / kStages) & 1) ^ 1);
+                const int64_t t = (int64_t)atomicAdd(&p.head->ticket, 1u);
+                StageMeta m;
+                if (t >= p.total) {
+                    m.kind = 2;
+                    sMeta[st] = m;
+                    mbar_arrive(&sFull[st]);
+                    break;
                 }
-            } else {
-                for (int64_t i = tid; i < cnt; i += kEncThreads)
-                    m = max(m, __float_as_uint(sg.x[base + i]) & 0x7fffffffu);
-            }
-            m = __reduce_max_sync(0xffffffffu, m);
-            if (lane == 0) sRed[tid >> 5] = m;
-            __syncthreads();
-            if (tid == 0) {
-                unsigned int mm = 0;
-#pragma unroll
-                for (int w = 0; w < kEncThreads / 32; ++w) mm = max(mm, sRed[w]);
-                SegCtl* c = p.ctl + b;
-                if (mm) atomicMax(&c->amax, mm);
-                __threadfence();
-                const unsigned int done = atomicAdd(&c->a_done, 1u);
-                sLast = (done == (unsigned int)sg.nA - 1u);
-                if (sLast) {
-                    __threadfence();
-                    sHdr[3] = (int)atomicAdd(&c->amax, 0u);
+                int lo = 0, hi = p.nblk;  // blks[lo].tstart <= t < blks[hi].tstart
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (blks[mid].tstart <= t)
+                        lo = mid;
+                    else
+                        hi = mid;
+                }
+                const EncBlk bk = blks[lo];
+                const EncSegD& sg = segs[bk.seg];
+                const int64_t k = t - bk.tstart;
+                const int64_t chunk = bk.kind == 0 ? k : (int64_t)sg.nE - 1 - k;
+                m.base = chunk * kChunk;
+                m.cnt = (int32_t)min((int64_t)kChunk, sg.n - m.base);
+                m.bulk = sg.aligned ? (m.cnt & ~3) : 0;
+                m.seg = bk.seg;
+                m.kind = bk.kind;
+                sMeta[st] = m;
+                if (m.bulk > 0) {
+                    mbar_arrive_expect_tx(&sFull[st], (uint32_t)m.bulk * 4u);
+                    bulk_g2s(sStage + (size_t)st * kChunk, sg.x + m.base, (uint32_t)m.bulk * 4u, &sFull[st],
+                             bk.kind == 0 ? keep : drop);
+                } else {
+                    mbar_arrive(&sFull[st]);
                 }
             }
-            __syncthreads();
-            if (sLast) {
-                // K2 for this segment: scale, thresholds, bucket table
-                const unsigned int amax = (unsigned int)sHdr[3];
-                const float scale = amax == 0u ? 1.0f : __uint_as_float(amax);
-                if (amax >= kInfBits && tid == 0) atomicOr(&p.head->status, A8_STATUS_NONFINITE);
-                build_lut_cta(p.book, scale, p.luts + b, sT, sCanon);
-                if (tid < p.lay.scale_reps)
-                    p.lay.scales[tid * p.lay.scale_block_stride + sg.scale_idx] = scale;
-                __threadfence();
-                __syncthreads();
-                if (tid == 0) st_release(&p.ctl[b].ready, 1u);
-                cur = -1;  // sT/sCanon were used as scratch
-            }
-            continue;
         }
+    } else {
+        // ===================== consumers =====================
+        const int ctid = tid - 32;
+        const int cw = warp - 1;
+        int cur = p.absmax ? -1 : -2;  // segment whose table is in shared memory (-2: static)
+        uint8_t* const codes_base = p.lay.codes;
+        const int64_t L = p.lay.block_len;
+        const int64_t gap = p.lay.block_stride - p.lay.block_len;
 
-        // ---------------- E: encode one chunk ------------------------------
-        const int s = b - p.lag;
-        k -= nA_b;
-        const EncSegD sg = segs[s];
-        const int64_t chunk = (int64_t)sg.nE - 1 - k;
-        if (p.absmax) {
-            if (cur != s) {
-                if (tid == 0) {
-                    unsigned int ns = 32;
-                    while (ld_acquire(&p.ctl[s].ready) == 0u) {
-                        __nanosleep(ns);
-                        ns = min(ns * 2u, 1024u);
+        for (int it = 0;; ++it) {
+            const int st = it % kStages;
+            mbar_wait(&sFull[st], (it / kStages) & 1);
+            const StageMeta m = sMeta[st];
+            if (m.kind == 2) break;
+            const EncSegD& sg = segs[m.seg];
+            const float* stage = sStage + (size_t)st * kChunk;
+
+            if (m.kind == 0) {
+                // ---------------- A: max |x| over the chunk ----------------
+                unsigned int mx = 0;
+#pragma unroll
+                for (int q = 0; q < kChunk / (kConsumers * 4); ++q) {
+                    const int i = q * (kConsumers * 4) + ctid * 4;
+                    if (i + 4 <= m.bulk) {
+                        const uint4 v = *reinterpret_cast<const uint4*>(stage + i);
+                        mx = max(mx, max(max(v.x & 0x7fffffffu, v.y & 0x7fffffffu),
+                                         max(v.z & 0x7fffffffu, v.w & 0x7fffffffu)));
                     }
                 }
-                __syncthreads();
-                load_lut_smem(p.luts + s, sE, sT, sCanon, p.book, sHdr);
-                __syncthreads();
-                cur = s;
-            }
-        } else if (chunk == 0 && tid < p.lay.scale_reps) {
-            p.lay.scales[tid * p.lay.scale_block_stride + sg.scale_idx] = p.static_lut->scale;
-        }
-        const int valid = sHdr[0];
-        const int32_t kbase = sHdr[1];
-        const int32_t lenm1 = sHdr[2];
-        const int64_t base = chunk * kChunk;
-        const int64_t cnt = min((int64_t)kChunk, sg.n - base);
-        unsigned int bad = 0;  // max |x| bits seen (fixed-scale specs detect NaN/Inf here)
-
-        // flat position of this chunk and its block
-        const int64_t f0 = sg.flat_off + base;
-        int64_t j = f0 / L;
-        int64_t bnd = (j + 1) * L;
-
-        if (cnt == kChunk && sg.aligned) {
-            float4 v[kGroups];
-#pragma unroll
-            for (int q = 0; q < kGroups; ++q) v[q] = ld_stream(sg.x + base + q * (kEncThreads * 4) + tid * 4);
-#pragma unroll
-            for (int q = 0; q < kGroups; ++q) {
-                const uint32_t b0 = __float_as_uint(v[q].x), b1 = __float_as_uint(v[q].y);
-                const uint32_t b2 = __float_as_uint(v[q].z), b3 = __float_as_uint(v[q].w);
-                uint32_t c0, c1, c2, c3;
-                if (valid) {
-                    c0 = encode_lut(b0, sE, kbase, lenm1);
-                    c1 = encode_lut(b1, sE, kbase, lenm1);
-                    c2 = encode_lut(b2, sE, kbase, lenm1);
-                    c3 = encode_lut(b3, sE, kbase, lenm1);
-                } else {
-                    c0 = encode_search(b0, sT, sCanon);
-                    c1 = encode_search(b1, sT, sCanon);
-                    c2 = encode_search(b2, sT, sCanon);
-                    c3 = encode_search(b3, sT, sCanon);
+                for (int i = m.bulk + ctid; i < m.cnt; i += kConsumers)
+                    mx = max(mx, __float_as_uint(sg.x[m.base + i]) & 0x7fffffffu);
+                mx = __reduce_max_sync(0xffffffffu, mx);
+                __syncwarp();
+                if (lane == 0) {
+                    sRed[cw] = mx;
+                    mbar_arrive(&sEmpty[st]);  // stage consumed
                 }
-                bad = max(bad, max(max(b0 & 0x7fffffffu, b1 & 0x7fffffffu), max(b2 & 0x7fffffffu, b3 & 0x7fffffffu)));
-                const int64_t f = f0 + q * (kEncThreads * 4) + tid * 4;
+                nbar_sync(kBarC, kConsumers);
+                if (ctid == 0) {
+                    unsigned int mm = 0;
+#pragma unroll
+                    for (int w = 0; w < kConsumerWarps; ++w) mm = max(mm, sRed[w]);
+                    SegCtl* c = p.ctl + m.seg;
+                    if (mm) atomicMax(&c->amax, mm);
+                    __threadfence();
+                    const unsigned int done = atomicAdd(&c->a_done, 1u);
+                    sLast = (done == (unsigned int)sg.nA - 1u);
+                    if (sLast) {
+                        __threadfence();
+                        sHdr[3] = (int)atomicAdd(&c->amax, 0u);
+                    }
+                }
+                nbar_sync(kBarC, kConsumers);
+                if (sLast) {
+                    // K2 for this segment: scale, thresholds, bucket table
+                    const unsigned int amax = (unsigned int)sHdr[3];
+                    const float scale = amax == 0u ? 1.0f : __uint_as_float(amax);
+                    if (amax >= kInfBits && ctid == 0) atomicOr(&p.head->status, A8_STATUS_NONFINITE);
+                    build_lut(p.book, scale, p.luts + m.seg, sT, sCanon, ctid);
+                    if (ctid < p.lay.scale_reps) p.lay.scales[ctid * p.lay.scale_block_stride + sg.scale_idx] = scale;
+                    __threadfence();
+                    nbar_sync(kBarC, kConsumers);
+                    if (ctid == 0) st_release(&p.ctl[m.seg].ready, 1u);
+                    cur = -1;  // sT / sCanon / sHdr were used as scratch
+                }
+                continue;
+            }
+
+            // ---------------- E: encode the chunk ----------------------------
+            if (cur != m.seg && cur != -2) {
+                nbar_sync(kBarC, kConsumers);  // everyone is done with the old table
+                if (ctid == 0) {
+                    unsigned int ns = 32;
+                    while (ld_acquire(&p.ctl[m.seg].ready) == 0u) {
+                        __nanosleep(ns);
+                        ns = min(ns * 2u, 512u);
+                    }
+                }
+                nbar_sync(kBarC, kConsumers);
+                load_lut_smem(p.luts + m.seg, sE, sT, sCanon, p.book, sHdr, ctid, kConsumers);
+                nbar_sync(kBarC, kConsumers);
+                cur = m.seg;
+            }
+            if (cur == -2 && m.base == 0 && ctid < p.lay.scale_reps)
+                p.lay.scales[ctid * p.lay.scale_block_stride + sg.scale_idx] = p.static_lut->scale;
+            const int valid = sHdr[0];
+            const int32_t kbase = sHdr[1];
+            const int32_t lenm1 = sHdr[2];
+            unsigned int big = 0;  // max |x| bits (fixed-scale specs detect NaN/Inf here)
+            const int64_t f0 = sg.flat_off + m.base;
+            int64_t j = f0 / L;
+            int64_t bnd = (j + 1) * L;
+#pragma unroll
+            for (int q = 0; q < kChunk / (kConsumers * 4); ++q) {
+                const int i = q * (kConsumers * 4) + ctid * 4;
+                if (i >= m.cnt) break;
+                const int64_t f = f0 + i;
                 while (f >= bnd) {
                     ++j;
                     bnd += L;
                 }
-                *reinterpret_cast<uint32_t*>(const_cast<uint8_t*>(codes_base) + f + j * gap) =
-                    c0 | (c1 << 8) | (c2 << 16) | (c3 << 24);
+                if (i + 4 <= m.bulk) {
+                    const uint4 v = *reinterpret_cast<const uint4*>(stage + i);
+                    uint32_t c0, c1, c2, c3;
+                    if (valid) {
+                        c0 = encode_lut(v.x, sE, kbase, lenm1);
+                        c1 = encode_lut(v.y, sE, kbase, lenm1);
+                        c2 = encode_lut(v.z, sE, kbase, lenm1);
+                        c3 = encode_lut(v.w, sE, kbase, lenm1);
+                    } else {
+                        c0 = encode_search(v.x, sT, sCanon);
+                        c1 = encode_search(v.y, sT, sCanon);
+                        c2 = encode_search(v.z, sT, sCanon);
+                        c3 = encode_search(v.w, sT, sCanon);
+                    }
+                    big = max(big, max(max(v.x & 0x7fffffffu, v.y & 0x7fffffffu), max(v.z & 0x7fffffffu, v.w & 0x7fffffffu)));
+                    *reinterpret_cast<uint32_t*>(codes_base + f + j * gap) = c0 | (c1 << 8) | (c2 << 16) | (c3 << 24);
+                } else {
+                    const int e_end = min(i + 4, m.cnt);
+                    for (int e = i; e < e_end; ++e) {
+                        const uint32_t b = e < m.bulk ? __float_as_uint(stage[e]) : __float_as_uint(sg.x[m.base + e]);
+                        const uint32_t c = valid ? encode_lut(b, sE, kbase, lenm1) : encode_search(b, sT, sCanon);
+                        big = max(big, b & 0x7fffffffu);
+                        const int64_t fe = f0 + e;
+                        const int64_t je = fe / L;
+                        codes_base[fe + je * gap] = (uint8_t)c;
+                    }
+                }
             }
-        } else {
-            for (int64_t i = tid; i < cnt; i += kEncThreads) {
-                const uint32_t bb = __float_as_uint(sg.x[base + i]);
-                const uint32_t c = valid ? encode_lut(bb, sE, kbase, lenm1) : encode_search(bb, sT, sCanon);
-                bad = max(bad, bb & 0x7fffffffu);
-                const int64_t f = f0 + i;
-                const int64_t jj = f / L;
-                const_cast<uint8_t*>(codes_base)[f + jj * gap] = (uint8_t)c;
-            }
-        }
-        if (!p.absmax) {
-            if (__syncthreads_or(bad >= kInfBits) && tid == 0) atomicOr(&p.head->status, A8_STATUS_NONFINITE);
+            if (!p.absmax && __any_sync(0xffffffffu, big >= kInfBits) && lane == 0)
+                atomicOr(&p.head->status, A8_STATUS_NONFINITE);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sEmpty[st]);
         }
     }
 
-    // last CTA out leaves the workspace zeroed for the next call
-    __shared__ int sFinal;
+    // last CTA out publishes the status and leaves the workspace zeroed
+    __syncthreads();
     if (tid == 0) {
         __threadfence();
         sFinal = atomicAdd(&p.head->ctas_done, 1u) == gridDim.x - 1;
@@ -402,8 +436,8 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
             p.ctl[i].ready = 0u;
         }
         if (tid < p.lay.scale_reps) {
-            const unsigned int st = atomicAdd(&p.head->status, 0u) | (p.status_in ? *p.status_in : 0u);
-            p.status_out[(int64_t)tid * p.lay.scale_block_stride] = st;
+            const unsigned int stt = atomicAdd(&p.head->status, 0u) | (p.status_in ? *p.status_in : 0u);
+            p.status_out[(int64_t)tid * p.lay.scale_block_stride] = stt;
         }
         __syncthreads();
         if (tid == 0) {
@@ -426,7 +460,7 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(const __grid_consta
     const int R = p.nranks;
     const int64_t L = p.lay.block_len;
     const int64_t gap = p.lay.block_stride - p.lay.block_len;
-    const float invN = 1.0f / (float)R;                  // exact when R is a power of two
+    const float invN = 1.0f / (float)R;  // exact when R is a power of two
     const bool pow2 = (R & (R - 1)) == 0;
     int cur = -1;
     int64_t cbase = 0;
@@ -439,8 +473,8 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(const __grid_consta
         for (int i = tid; i < R * p.status_blocks; i += kDecThreads) {
             const int r = i / p.status_blocks, j = i % p.status_blocks;
             const unsigned int* w = reinterpret_cast<const unsigned int*>(
-                reinterpret_cast<const uint8_t*>(p.lay.scales) + (int64_t)r * p.lay.rank_stride) +
-                (int64_t)j * p.lay.scale_block_stride + p.status_idx;
+                                        reinterpret_cast<const uint8_t*>(p.lay.scales) + (int64_t)r * p.lay.rank_stride) +
+                                    (int64_t)j * p.lay.scale_block_stride + p.status_idx;
             atomicOr(&sSt, __ldcg(w));
         }
         __syncthreads();
@@ -462,10 +496,10 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(const __grid_consta
             const int64_t j = sg.flat_off / L;
             for (int i = tid; i < R * 256; i += kDecThreads) {
                 const int r = i >> 8, code = i & 255;
-                const float* sc = reinterpret_cast<const float*>(
-                                      reinterpret_cast<const uint8_t*>(p.lay.scales) + (int64_t)r * p.lay.rank_stride) +
+                const float* sc = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.lay.scales) +
+                                                                 (int64_t)r * p.lay.rank_stride) +
                                   j * p.lay.scale_block_stride + sg.scale_idx;
-                const float v = __fmul_rn(p.book->table[code], __ldg(sc));  // codecs.py:281
+                const float v = __fmul_rn(p.book->table[code], __ldcg(sc));  // codecs.py:281
 #pragma unroll
                 for (int q = 0; q < kDecRep; ++q) sTab[(i << 2) + q] = v;
             }
@@ -500,12 +534,16 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(const __grid_consta
                 }
                 if (p.op == 1 && R > 1) {
                     if (pow2) {
-                        a0 = __fmul_rn(a0, invN); a1 = __fmul_rn(a1, invN);
-                        a2 = __fmul_rn(a2, invN); a3 = __fmul_rn(a3, invN);
+                        a0 = __fmul_rn(a0, invN);
+                        a1 = __fmul_rn(a1, invN);
+                        a2 = __fmul_rn(a2, invN);
+                        a3 = __fmul_rn(a3, invN);
                     } else {
                         const float fn = (float)R;
-                        a0 = __fdiv_rn(a0, fn); a1 = __fdiv_rn(a1, fn);
-                        a2 = __fdiv_rn(a2, fn); a3 = __fdiv_rn(a3, fn);
+                        a0 = __fdiv_rn(a0, fn);
+                        a1 = __fdiv_rn(a1, fn);
+                        a2 = __fdiv_rn(a2, fn);
+                        a3 = __fdiv_rn(a3, fn);
                     }
                 }
                 __stcs(reinterpret_cast<float4*>(sg.out + base + e), make_float4(a0, a1, a2, a3));
@@ -541,7 +579,12 @@ static int dev_info(int device, DevInfo* out) {
     if (d.sms == 0) {
         cudaError_t e = cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, device);
         if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.enc_occ, encode_kernel, kEncThreads, 0);
+        e = cudaFuncSetAttribute(encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEncDynSmem);
+        if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
+        e = cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kMaxRanks * 256 * kDecRep * (int)sizeof(float));
+        if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.enc_occ, encode_kernel, kEncThreads, kEncDynSmem);
         if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
         const size_t dsm = (size_t)8 * 256 * kDecRep * sizeof(float);
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.dec_occ, decode_kernel, kDecThreads, dsm);
@@ -555,12 +598,13 @@ static int dev_info(int device, DevInfo* out) {
 
 static int check_layout(const a8_layout_t& lay) {
     if (!lay.codes || !lay.scales) return fail(A8_ERR_USAGE, "layout: null codes or scales");
-    if (lay.block_len <= 0 || lay.block_len % 16) return fail(A8_ERR_USAGE, "layout: block_len must be a positive multiple of 16");
+    if (lay.block_len <= 0 || lay.block_len % 16)
+        return fail(A8_ERR_USAGE, "layout: block_len must be a positive multiple of 16");
     if (lay.block_stride < lay.block_len || lay.block_stride % 16)
         return fail(A8_ERR_USAGE, "layout: block_stride must be >= block_len and a multiple of 16");
     if (reinterpret_cast<uintptr_t>(lay.codes) % 16) return fail(A8_ERR_USAGE, "layout: codes must be 16-byte aligned");
     if (lay.rank_stride % 16) return fail(A8_ERR_USAGE, "layout: rank_stride must be a multiple of 16");
-    if (lay.rank_stride % 4 || lay.scale_block_stride < 0) return fail(A8_ERR_USAGE, "layout: bad scale strides");
+    if (lay.scale_block_stride < 0) return fail(A8_ERR_USAGE, "layout: bad scale strides");
     return A8_OK;
 }
 
@@ -571,6 +615,46 @@ static int cuda_check(const char* what) {
         return A8_ERR_CUDA;
     }
     return A8_OK;
+}
+
+// Ticket order: ascending segment size; a segment of kBigSeg+ elements runs
+// its A-chunks and then its E-chunks (reverse order, L2 reuse); smaller ones
+// are pipelined with a lag so their table builds overlap other work.
+static void schedule(const std::vector<EncSegD>& d, bool absmax, std::vector<EncBlk>* blks) {
+    int64_t t = 0;
+    auto push = [&](int s, int kind) {
+        const int64_t cnt = kind == 0 ? d[s].nA : d[s].nE;
+        if (cnt == 0) return;
+        blks->push_back(EncBlk{t, s, kind});
+        t += cnt;
+    };
+    const int nseg = (int)d.size();
+    if (!absmax) {
+        for (int s = 0; s < nseg; ++s) push(s, 1);
+    } else {
+        std::deque<int> pending;
+        for (int s = 0; s < nseg; ++s) {
+            push(s, 0);
+            if (d[s].n >= kBigSeg) {
+                while (!pending.empty()) {
+                    push(pending.front(), 1);
+                    pending.pop_front();
+                }
+                push(s, 1);
+            } else {
+                pending.push_back(s);
+                if ((int)pending.size() > kLag) {
+                    push(pending.front(), 1);
+                    pending.pop_front();
+                }
+            }
+        }
+        while (!pending.empty()) {
+            push(pending.front(), 1);
+            pending.pop_front();
+        }
+    }
+    blks->push_back(EncBlk{t, -1, 2});  // sentinel: total tickets
 }
 
 }  // namespace a8
@@ -597,27 +681,26 @@ extern "C" int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_de
                          const uint32_t* status_in, uint32_t* status_out, void* stream) {
     if (nseg <= 0) return fail(A8_ERR_USAGE, "a8_encode: need at least one segment");
     if (!segs || !book_dev || !workspace || !status_out) return fail(A8_ERR_USAGE, "a8_encode: null argument");
-    if (norm != A8_NORM_ABSMAX && !static_lut_dev) return fail(A8_ERR_USAGE, "a8_encode: fixed-scale spec needs a static table");
+    if (norm != A8_NORM_ABSMAX && !static_lut_dev)
+        return fail(A8_ERR_USAGE, "a8_encode: fixed-scale spec needs a static table");
     if (int rc = check_layout(layout)) return rc;
-    if (layout.scale_reps < 1 || layout.scale_reps > kEncThreads) return fail(A8_ERR_USAGE, "a8_encode: scale_reps out of range");
+    if (layout.scale_reps < 1 || layout.scale_reps > kConsumers)
+        return fail(A8_ERR_USAGE, "a8_encode: scale_reps out of range");
     int device = 0;
     cudaGetDevice(&device);
     DevInfo di;
     if (int rc = dev_info(device, &di)) return rc;
 
     const bool absmax = norm == A8_NORM_ABSMAX;
-    // scheduling order: ascending size, so that the E-chunks of the big
-    // segments trail at the end and cover the last table builds
     std::vector<int> order(nseg);
     for (int i = 0; i < nseg; ++i) order[i] = i;
-    if (absmax)
-        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return segs[a].n < segs[b].n; });
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return segs[a].n < segs[b].n; });
 
     std::vector<EncSegD> d(nseg);
     for (int i = 0; i < nseg; ++i) {
         const a8_enc_seg_t& s = segs[order[i]];
         if (s.n < 0 || (s.n > 0 && !s.x)) return fail(A8_ERR_USAGE, "a8_encode: bad segment");
-        if (s.flat_off % 16) return fail(A8_ERR_USAGE, "a8_encode: flat_off must be a multiple of 16");
+        if (s.flat_off % 16 || s.flat_off < 0) return fail(A8_ERR_USAGE, "a8_encode: flat_off must be a multiple of 16");
         const int64_t nch = (s.n + kChunk - 1) / kChunk;
         if (nch > INT32_MAX / 2) return fail(A8_ERR_USAGE, "a8_encode: segment too large");
         d[i].x = s.x;
@@ -628,12 +711,9 @@ extern "C" int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_de
         d[i].nE = absmax ? (int32_t)nch : (int32_t)std::max<int64_t>(1, nch);
         d[i].aligned = (reinterpret_cast<uintptr_t>(s.x) % 16) == 0;
     }
-    const int lag = absmax ? std::min(kLag, nseg) : 0;
-    const int nblk = nseg + lag;
-    std::vector<int64_t> bstart(nblk + 1);
-    bstart[0] = 0;
-    for (int b = 0; b < nblk; ++b)
-        bstart[b + 1] = bstart[b] + (b < nseg ? d[b].nA : 0) + (b >= lag ? d[b - lag].nE : 0);
+    std::vector<EncBlk> blks;
+    schedule(d, absmax, &blks);
+    const int nblk = (int)blks.size() - 1;
 
     uint8_t* ws = static_cast<uint8_t*>(workspace);
     EncParams p;
@@ -648,23 +728,22 @@ extern "C" int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_de
     p.status_out = status_out;
     p.nseg = nseg;
     p.nblk = nblk;
-    p.lag = lag;
     p.absmax = absmax ? 1 : 0;
-    p.total = bstart[nblk];
+    p.total = blks[nblk].tstart;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (nseg <= kInlineSegs) {
         std::copy(d.begin(), d.end(), p.segs);
-        std::copy(bstart.begin(), bstart.end(), p.bstart);
+        std::copy(blks.begin(), blks.end(), p.blks);
     } else {
         uint8_t* plan = ws + plan_off(nseg);
         const size_t sb = sizeof(EncSegD) * nseg;
         cudaMemcpyAsync(plan, d.data(), sb, cudaMemcpyHostToDevice, st);
-        cudaMemcpyAsync(plan + sb, bstart.data(), sizeof(int64_t) * (nblk + 1), cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(plan + sb, blks.data(), sizeof(EncBlk) * blks.size(), cudaMemcpyHostToDevice, st);
         p.segs_dev = reinterpret_cast<const EncSegD*>(plan);
-        p.bstart_dev = reinterpret_cast<const int64_t*>(plan + sb);
+        p.blks_dev = reinterpret_cast<const EncBlk*>(plan + sb);
     }
     const int64_t grid = std::min<int64_t>((int64_t)di.sms * di.enc_occ, std::max<int64_t>(1, p.total));
-    encode_kernel<<<(unsigned)grid, kEncThreads, 0, st>>>(p);
+    encode_kernel<<<(unsigned)grid, kEncThreads, kEncDynSmem, st>>>(p);
     return cuda_check("a8_encode");
 }
 
@@ -683,12 +762,12 @@ extern "C" int a8_decode(const a8_dec_seg_t* segs, int nseg, const void* book_de
     DevInfo di;
     if (int rc = dev_info(device, &di)) return rc;
 
-    std::vector<DecSegD> d(nseg);
+    std::vector<DecSegD> d(std::max(nseg, 1));
     int64_t chunks = 0;
     for (int i = 0; i < nseg; ++i) {
         const a8_dec_seg_t& s = segs[i];
         if (s.n < 0 || (s.n > 0 && !s.out)) return fail(A8_ERR_USAGE, "a8_decode: bad segment");
-        if (s.flat_off % 16) return fail(A8_ERR_USAGE, "a8_decode: flat_off must be a multiple of 16");
+        if (s.flat_off % 16 || s.flat_off < 0) return fail(A8_ERR_USAGE, "a8_decode: flat_off must be a multiple of 16");
         if (s.n > 0 && (s.flat_off / layout.block_len) != ((s.flat_off + s.n - 1) / layout.block_len))
             return fail(A8_ERR_USAGE, "a8_decode: a segment may not straddle blocks");
         d[i].out = s.out;
@@ -713,20 +792,13 @@ extern "C" int a8_decode(const a8_dec_seg_t* segs, int nseg, const void* book_de
     p.total = chunks;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (nseg <= kInlineSegs) {
-        std::copy(d.begin(), d.end(), p.segs);
+        std::copy(d.begin(), d.begin() + nseg, p.segs);
     } else {
         uint8_t* plan = static_cast<uint8_t*>(workspace) + plan_off(nseg);
         cudaMemcpyAsync(plan, d.data(), sizeof(DecSegD) * nseg, cudaMemcpyHostToDevice, st);
         p.segs_dev = reinterpret_cast<const DecSegD*>(plan);
     }
     const size_t smem = (size_t)nranks * 256 * kDecRep * sizeof(float);
-    if (smem > 48 * 1024) {
-        static thread_local bool attr_set[64] = {false};
-        if (!attr_set[device]) {
-            cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-            attr_set[device] = true;
-        }
-    }
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)di.sms * di.dec_occ, chunks));
     decode_kernel<<<(unsigned)grid, kDecThreads, smem, st>>>(p);
     return cuda_check("a8_decode");

@@ -1,0 +1,91 @@
+"""Codec micro-benchmark / profiling driver (one GPU).
+
+    python tools/prof_codec.py --case alexnet|single|static|sweep [--iters N]
+
+Times a8_encode / a8_decode launches with CUDA events and prints GB/s at
+algorithmic bytes (encode 5 B/elem, decode 5 B/elem).  Used under ncu to
+capture the kernels (short --iters).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+import paper_1511_04561_b200 as A  # noqa: E402
+from paper_1511_04561_b200.exchange import CudaSegmentCodec, make_plan  # noqa: E402
+
+ALEXNET = [(64, 3, 11, 11), (64,), (192, 64, 5, 5), (192,), (384, 192, 3, 3), (384,),
+           (256, 384, 3, 3), (256,), (256, 256, 3, 3), (256,), (4096, 9216), (4096,),
+           (4096, 4096), (4096,), (1000, 4096), (1000,)]
+
+
+def run(sizes, spec, iters, dev):
+    gen = torch.Generator(device=dev).manual_seed(0)
+    xs = [torch.randn(int(np.prod(s)), device=dev, generator=gen) * 1e-3 for s in sizes]
+    outs = [torch.empty_like(x) for x in xs]
+    plan = make_plan([x.numel() for x in xs], 1)
+    cb = A.build_codebook(spec)
+    codec = CudaSegmentCodec()
+    B = plan.allgather_block()
+    buf = torch.zeros(B, dtype=torch.uint8, device=dev)
+    st = torch.zeros(1, dtype=torch.int32, device=dev)
+    idx = list(range(len(xs)))
+    n = sum(x.numel() for x in xs)
+
+    def enc():
+        codec.encode(xs, plan.offs, idx, cb, buf, 0, plan.flat, plan.flat, plan.flat, 0, 1,
+                     plan.flat + 4 * plan.status_slot)
+
+    def dec():
+        codec.decode(outs, plan.offs, idx, cb, buf, 0, plan.flat, plan.flat, plan.flat, 0, B, 1, 1,
+                     plan.status_slot, 1, st)
+
+    for _ in range(3):
+        enc()
+        dec()
+    torch.cuda.synchronize()
+    res = {}
+    for name, fn in (("encode", enc), ("decode", dec)):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
+        for e0, e1 in evs:
+            e0.record()
+            fn()
+            e1.record()
+        torch.cuda.synchronize()
+        ms = float(np.median([e0.elapsed_time(e1) for e0, e1 in evs]))
+        res[name] = {"ms": ms, "GBps": 5.0 * n / (ms * 1e-3) / 1e9}
+    return n, res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--case", default="alexnet")
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--spec", default="dynamic-tree/absmax")
+    a = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    spec = A.parse_spec(a.spec)
+    if a.case == "alexnet":
+        cases = [("alexnet", ALEXNET)]
+    elif a.case == "single":
+        cases = [("single_2^26", [(1 << 26,)])]
+    elif a.case == "sweep":
+        cases = [(f"2^{k}", [(1 << k,)]) for k in range(10, 31, 2)]
+    else:
+        raise SystemExit(f"unknown case {a.case}")
+    for name, sizes in cases:
+        n, res = run(sizes, spec, a.iters, dev)
+        print(json.dumps({"case": name, "spec": a.spec, "n": n, **res}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
