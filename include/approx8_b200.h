@@ -84,7 +84,8 @@ typedef struct a8_lut {
     float scale;      /* the scale the table encodes    */
     uint32_t pad[3];
     uint32_t T[128];  /* thresholds, padded with 0x7f800000 */
-    uint32_t e[A8_LUT_MAX];
+    uint32_t e[A8_LUT_MAX]; /* t_low << 16 | code_hi << 8 | code_lo; an element of
+                             * the bucket takes code_hi iff lo16(bits) >= t_low */
 } a8_lut_t;
 
 /* Encode segment: a float32 tensor (contiguous). */
@@ -130,8 +131,11 @@ int a8_fixed_scale(int norm, int decades, float* scale_out);
  * none/decade specs and by the CPU tests of the table logic). */
 int a8_build_lut_host(const a8_book_t* book, float scale, a8_lut_t* out);
 
-/* Device scratch needed by a8_encode / a8_decode for `nseg` segments.
- * Must be zero-filled once after allocation; the kernels leave it zeroed. */
+/* Device scratch needed by a8_encode / a8_decode for up to `nseg` segments.
+ * Must be zero-filled once after allocation; the kernels leave it zeroed.
+ * Calls pass the workspace's byte size: its layout is a function of that
+ * capacity only, so calls with different segment counts can share it (in
+ * stream order). */
 size_t a8_workspace_bytes(int nseg);
 
 /* encode_buffer (codecs.py:244-269) for nseg tensors in one launch.
@@ -147,7 +151,8 @@ size_t a8_workspace_bytes(int nseg);
  *               status_out[k * scale_block_stride] for k < scale_reps      */
 int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_dev, int norm,
               const void* static_lut_dev, a8_layout_t layout, void* workspace,
-              const uint32_t* status_in, uint32_t* status_out, void* stream);
+              size_t workspace_bytes, const uint32_t* status_in, uint32_t* status_out,
+              void* stream);
 
 /* decode_buffer (codecs.py:272-282) fused with the cross-rank reduction:
  *   out = sum_{r<nranks} table[c_r] * s_r, accumulated in rank order in
@@ -159,7 +164,14 @@ int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_dev, int norm
  *   r < nranks, j < status_blocks (the encoders' replicated status words). */
 int a8_decode(const a8_dec_seg_t* segs, int nseg, const void* book_dev, a8_layout_t layout,
               int nranks, int op, int status_idx, int status_blocks, uint32_t* status_out,
-              void* workspace, void* stream);
+              void* workspace, size_t workspace_bytes, void* stream);
+
+/* Diagnostics: globaltimer trace of the last a8_encode on `workspace`
+ * (synchronous device->host copy).  out[0..3] = kernel start ns, end ns,
+ * total CTA time spent waiting for segment tables (ns), number of waits;
+ * out[4 + 2k], out[5 + 2k] = table build start/end of the k-th segment in
+ * scheduling order (ascending size).  Needs 4 + 2*nseg entries.            */
+int a8_encode_trace(const void* workspace, int nseg, uint64_t* out);
 
 /* Number of SMs and the persistent grid sizes the kernels use on `device`. */
 int a8_device_info(int device, int* num_sms, int* enc_ctas_per_sm, int* dec_ctas_per_sm);

@@ -2,7 +2,7 @@
 
 The library is the product: there is no Python/NumPy/torch fallback for any
 compute path.  If ``_lib/libapprox8_b200.so`` is missing this module raises
-at import (build it with ``python -m paper_1511_04561_b200.build``).
+at import (build it with ``python paper_1511_04561_b200/build.py``).
 """
 
 from __future__ import annotations
@@ -90,13 +90,14 @@ SIGNATURES = {
     "a8_encode": (
         C.c_int,
         [C.POINTER(EncSeg), C.c_int, C.c_void_p, C.c_int, C.c_void_p, Layout, C.c_void_p,
-         C.c_void_p, C.c_void_p, C.c_void_p],
+         C.c_size_t, C.c_void_p, C.c_void_p, C.c_void_p],
     ),
     "a8_decode": (
         C.c_int,
         [C.POINTER(DecSeg), C.c_int, C.c_void_p, Layout, C.c_int, C.c_int, C.c_int, C.c_int,
-         C.c_void_p, C.c_void_p, C.c_void_p],
+         C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p],
     ),
+    "a8_encode_trace": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_uint64)]),
     "a8_device_info": (
         C.c_int,
         [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)],
@@ -108,7 +109,7 @@ def _load() -> C.CDLL:
     if not _LIB_PATH.exists():
         raise ImportError(
             f"approx8 B200 library not built: {_LIB_PATH} is missing. "
-            "Run `python -m paper_1511_04561_b200.build` (needs nvcc); there is no CPU fallback."
+            "Run `python paper_1511_04561_b200/build.py` (needs nvcc); there is no CPU fallback."
         )
     lib = C.CDLL(str(_LIB_PATH), mode=os.RTLD_NOW | getattr(os, "RTLD_LOCAL", 0))
     for name, (res, args) in SIGNATURES.items():

@@ -1,6 +1,8 @@
 """Build the sm_100a C-ABI library in-tree with nvcc (no JIT, no torch build).
 
-    python -m paper_1511_04561_b200.build          # -> paper_1511_04561_b200/_lib/libapprox8_b200.so
+    python paper_1511_04561_b200/build.py [--force] [-v]   # -> paper_1511_04561_b200/_lib/libapprox8_b200.so
+
+(Run it as a script: importing the package loads the library it builds.)
 
 The .so is git-ignored but travels to the GPU box with the gpurun snapshot.
 """

@@ -360,7 +360,7 @@ def encode_buffer(x, codebook: Codebook, *, device=None, sync: bool = True) -> Q
         ws = workspace(dev, stream, 1)
         N.check(N.lib.a8_encode(C.byref(seg), 1, book.data_ptr(), spec.norm_code,
                                 None if lut is None else lut.data_ptr(), lay, ws.data_ptr(),
-                                None, meta.data_ptr(), stream))
+                                ws.numel(), None, meta.data_ptr(), stream))
     q = QuantizedTensor(codes, shape, spec, scale_tensor=meta[1:].view(torch.float32), meta=meta)
     q._keepalive = t  # input must outlive the asynchronous kernel
     if sync:
@@ -398,7 +398,7 @@ def decode_buffer(q: QuantizedTensor, codebook: Codebook, *, device=None, out=No
         lay = N.Layout(codes.data_ptr(), scale_t.data_ptr(), round16(n), round16(n), 0, 0, 1, 0)
         ws = workspace(dev, stream, 1)
         N.check(N.lib.a8_decode(C.byref(seg), 1, book.data_ptr(), lay, 1, 0, -1, 0, None,
-                                ws.data_ptr(), stream))
+                                ws.data_ptr(), ws.numel(), stream))
     return out
 
 

@@ -83,12 +83,30 @@ A8_HD uint32_t threshold(double s, double v_lo, double v_hi) {
     } else {
         g = f32_bits((float)m);
     }
-    uint32_t lo = g > 16u ? g - 16u : 0u;
-    uint32_t hi = g + 16u < kInfBits ? g + 16u : kInfBits;
-    if ((lo != 0u && picks_upper(lo, s, v_lo, v_hi)) ||
-        (hi != kInfBits && !picks_upper(hi, s, v_lo, v_hi))) {
-        lo = 0u;
-        hi = kInfBits;
+    // the rounded midpoint is almost always within a step or two of the
+    // threshold: walk from it (2-3 predicate evaluations), and fall back to
+    // a full bisection if the walk does not settle quickly
+    uint32_t lo = 0u, hi = kInfBits;
+    if (g > 0u && g < kInfBits) {
+        if (picks_upper(g, s, v_lo, v_hi)) {
+            uint32_t a = g;
+            int steps = 0;
+            while (a > 0u && steps < 4 && picks_upper(a - 1u, s, v_lo, v_hi)) {
+                --a;
+                ++steps;
+            }
+            if (a == 0u || steps < 4) return a;  // pred(a) true, pred(a-1) false
+            hi = a;
+        } else {
+            uint32_t a = g + 1u;
+            int steps = 0;
+            while (a < kInfBits && steps < 4 && !picks_upper(a, s, v_lo, v_hi)) {
+                ++a;
+                ++steps;
+            }
+            if (a == kInfBits || steps < 4) return a;  // pred(a-1) false, pred(a) true
+            lo = a - 1u;                                // pred(a-1) false is known
+        }
     }
     while (hi - lo > 1u) {
         const uint32_t mid = lo + ((hi - lo) >> 1);
@@ -106,7 +124,12 @@ A8_HD bool scale_ok(float s) {
 }
 
 // Entries [j0, j1) of the bucket table.  T[0..F) are the finite thresholds
-// (non-decreasing).  Returns false if a bucket holds two distinct thresholds.
+// (non-decreasing).  Entry = t_low << 16 | code_hi << 8 | code_lo where t_low
+// is the low half of the bucket's threshold: an element of the bucket takes
+// code_hi iff lo16(bits) >= t_low, which is exactly
+// ((bits << 16) | 0xffff) >= entry because codes never exceed 0x7f7f.
+// A bucket without a threshold stores t_low = 0 and code_hi = code_lo.
+// Returns false if a bucket holds two distinct thresholds.
 A8_HD bool lut_fill(const uint32_t* T, uint32_t F, const uint8_t* canon, int32_t kbase, uint32_t j0,
                     uint32_t j1, uint32_t* e) {
     if (j0 >= j1) return true;
@@ -155,18 +178,50 @@ A8_HD void lut_geometry(const uint32_t* T, uint32_t F, int32_t* kbase, uint32_t*
     *len = (uint32_t)(kmax - kmin + 3);
 }
 
-// One element: |x| bits -> code via the bucket table (codecs.py:262-268).
+// One element: bits(x) -> code via the bucket table (codecs.py:262-268).
 A8_HD uint32_t encode_lut(uint32_t b, const uint32_t* e, int32_t kbase, int32_t lenm1) {
-    const uint32_t a = b & 0x7fffffffu;
-    int32_t j = (int32_t)(a >> kKeyShift) - kbase;
+    int32_t j = (int32_t)((b & 0x7fffffffu) >> kKeyShift) - kbase;
     j = j < 0 ? 0 : (j > lenm1 ? lenm1 : j);
     const uint32_t v = e[j];
-    uint32_t c = ((a & 0xffffu) >= (v >> 16)) ? (v >> 8) : v;
+    uint32_t c = (((b << 16) | 0xffffu) >= v) ? (v >> 8) : v;
     c &= 0xffu;
     // sign bit only for non-zero values (codecs.py:267-268); code 0 is the
     // only zero code, and c + 127 carries into bit 7 iff c != 0
     return c | ((c + 0x7fu) & (b >> 24) & 0x80u);
 }
+
+#if defined(__CUDACC__)
+// Canonical code (no sign) in the low byte of the result, garbage above.
+// `eb` is the table base pre-offset by -kbase entries, so the clamped key
+// indexes it directly.  Key and operand arithmetic use IMAD (FMA pipe); the
+// ALU pipe does the clamp, compare and select.
+__device__ __forceinline__ uint32_t lut_code_lo(uint32_t b, const uint32_t* eb, int32_t kmin, int32_t kmax) {
+    const int32_t key = (int32_t)__umulhi(b * 2u, 1u << (31 - kKeyShift));  // (b & 0x7fffffff) >> 16
+    const int32_t k = min(max(key, kmin), kmax);
+    const uint32_t v = eb[k];
+    return (b * 65536u + 0xffffu >= v) ? (v >> 8) : v;
+}
+
+// Sign attachment for 4 packed canonical codes (each <= 127): bit 7 of a
+// byte is set iff the input is negative and the code is non-zero
+// (codecs.py:267-268).  c + 0x7f carries into bit 7 iff c != 0; no byte
+// overflows into its neighbour.
+__device__ __forceinline__ uint32_t attach_signs4(uint32_t packed, uint32_t b0, uint32_t b1, uint32_t b2,
+                                                  uint32_t b3) {
+    const uint32_t s = __byte_perm(__byte_perm(b0, b1, 0x0073), __byte_perm(b2, b3, 0x0073), 0x5410);
+    return packed | ((packed + 0x7f7f7f7fu) & s & 0x80808080u);
+}
+
+// Four elements -> four codes packed little-endian (bucket table).
+__device__ __forceinline__ uint32_t encode4_lut(uint4 v, const uint32_t* eb, int32_t kmin, int32_t kmax) {
+    const uint32_t c0 = lut_code_lo(v.x, eb, kmin, kmax);
+    const uint32_t c1 = lut_code_lo(v.y, eb, kmin, kmax);
+    const uint32_t c2 = lut_code_lo(v.z, eb, kmin, kmax);
+    const uint32_t c3 = lut_code_lo(v.w, eb, kmin, kmax);
+    const uint32_t packed = __byte_perm(__byte_perm(c0, c1, 0x0040), __byte_perm(c2, c3, 0x0040), 0x5410);
+    return attach_signs4(packed, v.x, v.y, v.z, v.w);
+}
+#endif
 
 // One element by binary search over the padded thresholds (paper's method).
 A8_HD uint32_t encode_search(uint32_t b, const uint32_t* T128, const uint8_t* canon128) {

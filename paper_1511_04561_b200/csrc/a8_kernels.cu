@@ -31,11 +31,9 @@ extern thread_local std::string g_last_error;
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = kConsumerWarps * 32;  // threads doing reduce / encode
 constexpr int kEncThreads = kConsumers + 32;     // + one producer warp
-constexpr int kStages = 5;                       // bulk-copy ring depth per CTA
+constexpr int kStages = 4;                       // bulk-copy ring depth per CTA
 constexpr int kChunk = 4096;                     // elements per stage (16 KB)
 constexpr int kBarC = 1;                         // named barrier of the consumer warps
-constexpr int64_t kBigSeg = 2 << 20;             // segments >= this run A then E back to back
-constexpr int kLag = 2;                          // small segments: E(s) after A(s + kLag)
 constexpr size_t kEncDynSmem = (size_t)kStages * kChunk * sizeof(float);
 
 // ---- decode geometry ---------------------------------------------------------
@@ -45,8 +43,10 @@ constexpr int kDecChunk = kDecThreads * kGroups * 4;
 constexpr int kDecRep = 4;  // replicated decode tables (bank-conflict relief)
 constexpr int kMaxRanks = 16;
 
-constexpr int kInlineSegs = 48;
-constexpr int kInlineBlks = 2 * kInlineSegs + 1;
+constexpr int kInlineSegs = 32;
+constexpr int kInlineBlks = 3 * kInlineSegs + 2;
+constexpr int64_t kGroupMin = 2 << 20;  // schedule segments in groups of at least this many elements
+constexpr int64_t kFill = 768;          // E-chunks of the previous group that cover a table build
 
 // ---------------------------------------------------------------------------
 // device-side plan / workspace
@@ -61,11 +61,12 @@ struct EncSegD {
     int32_t aligned;  // x is 16-byte aligned (bulk copies allowed)
 };
 
-// A contiguous run of tickets: all A-chunks or all E-chunks of one segment.
+// A contiguous run of tickets over one segment: c0 >= 0 -> A-chunks (max-abs)
+// c0, c0+1, ...; c0 < 0 -> E-chunks (encode) -c0-1, -c0-2, ... (descending).
 struct EncBlk {
     int64_t tstart;
     int32_t seg;
-    int32_t kind;  // 0 = A (max-abs), 1 = E (encode, chunks in reverse order)
+    int32_t c0;
 };
 
 struct DecSegD {
@@ -81,15 +82,29 @@ struct WsHead {
     unsigned int ticket;
     unsigned int ctas_done;
     unsigned int status;
-    unsigned int pad[13];
+    unsigned int waits;  // table waits (trace)
+    unsigned long long t_start_inv;  // ~min(CTA start time), trace
+    unsigned long long wait_ns;      // total CTA time spent waiting for tables, trace
+    // copies of the last call's trace (kept across the reset)
+    unsigned long long tr_start, tr_end, tr_wait_ns;
+    unsigned int tr_waits;
+    unsigned int pad;
 };
+static_assert(sizeof(WsHead) == 64, "workspace head");
 
 struct SegCtl {
     unsigned int amax;
     unsigned int a_done;
     unsigned int ready;
     unsigned int pad;
+    unsigned long long t_b0, t_b1;  // table build start / end (globaltimer ns), trace
 };
+
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 struct EncParams {
     a8_layout_t lay;
@@ -127,11 +142,16 @@ struct DecParams {
 
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+// Workspace layout for a capacity of `cap` segments:
+//   [head][ctl x cap][tables x cap][plan for cap segments]
+// The layout depends only on the capacity (derived from the workspace size),
+// never on a call's segment count, so the control slots that kernels leave
+// zeroed are never overlapped by another call's tables or plan.
 static size_t ctl_off() { return sizeof(WsHead); }
-static size_t lut_off(int nseg) { return align_up(ctl_off() + sizeof(SegCtl) * (size_t)nseg, 256); }
-static size_t plan_off(int nseg) { return align_up(lut_off(nseg) + sizeof(a8_lut_t) * (size_t)nseg, 256); }
+static size_t lut_off(int cap) { return align_up(ctl_off() + sizeof(SegCtl) * (size_t)cap, 256); }
+static size_t plan_off(int cap) { return align_up(lut_off(cap) + sizeof(a8_lut_t) * (size_t)cap, 256); }
 static size_t plan_bytes(int nseg) {
-    const size_t enc = sizeof(EncSegD) * (size_t)nseg + sizeof(EncBlk) * (size_t)(2 * nseg + 1);
+    const size_t enc = sizeof(EncSegD) * (size_t)nseg + sizeof(EncBlk) * (size_t)(3 * nseg + 2);
     const size_t dec = sizeof(DecSegD) * (size_t)nseg;
     return align_up(std::max(enc, dec), 256);
 }
@@ -176,8 +196,12 @@ __device__ void load_lut_smem(const a8_lut_t* src, uint32_t* sE, uint32_t* sT, u
                               const a8_book_t* book, int* sHdr, int ctid, int nthreads) {
     const uint32_t len = __ldcg(&src->len);
     const uint32_t valid = __ldcg(&src->valid);
-    if (valid) {
-        for (uint32_t j = ctid; j < len; j += nthreads) sE[j] = __ldcg(&src->e[j]);
+    if (valid) {  // 16-byte loads, several in flight per thread (e[] is 4096 entries)
+        const uint4* s4 = reinterpret_cast<const uint4*>(src->e);
+        uint4* d4 = reinterpret_cast<uint4*>(sE);
+        const uint32_t n4 = (len + 3) >> 2;
+#pragma unroll 4
+        for (uint32_t j = ctid; j < n4; j += nthreads) d4[j] = __ldcg(&s4[j]);
     } else if (ctid < 128) {
         sT[ctid] = __ldcg(&src->T[ctid]);
         sCanon[ctid] = book->codes[ctid];
@@ -190,12 +214,17 @@ __device__ void load_lut_smem(const a8_lut_t* src, uint32_t* sE, uint32_t* sT, u
 }
 
 struct StageMeta {
-    int64_t base;  // first element of the chunk inside its segment
-    int32_t cnt;   // elements in the chunk
-    int32_t bulk;  // leading elements delivered to shared memory by the bulk copy
+    int64_t base;      // first element of the chunk inside its segment
+    int64_t code_off;  // byte offset of the chunk's first code (valid if simple)
+    int32_t cnt;       // elements in the chunk
+    int32_t bulk;      // leading elements delivered to shared memory by the bulk copy
     int32_t seg;
-    int32_t kind;  // 0 A, 1 E, 2 end
+    int32_t kind;      // 0 A, 1 E, 2 end
+    int32_t simple;    // full chunk inside one block of the code layout
+    int32_t pad;
 };
+
+constexpr unsigned int kTicketBatch = 4;  // tickets per atomic (one batch prefetched)
 
 // ---------------------------------------------------------------------------
 // K1+K2+K3: persistent encode.
@@ -214,7 +243,7 @@ struct StageMeta {
 
 __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_constant__ EncParams p) {
     extern __shared__ __align__(128) float sStage[];  // [kStages][kChunk]
-    __shared__ uint32_t sE[kLutMax];
+    __shared__ __align__(16) uint32_t sE[kLutMax];
     __shared__ uint32_t sT[128];
     __shared__ uint8_t sCanon[128];
     __shared__ __align__(8) uint64_t sFull[kStages];
@@ -238,6 +267,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
         }
         mbar_fence_init();
     }
+    if (tid == 0) atomicMax(&p.head->t_start_inv, ~gtime());
     if (!p.absmax && tid >= 32)  // fixed scale: one table for every segment
         load_lut_smem(p.static_lut, sE, sT, sCanon, p.book, sHdr, tid - 32, kConsumers);
     __syncthreads();
@@ -247,10 +277,22 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
         if (lane == 0) {
             const uint64_t keep = policy_evict_last();   // A reads: keep for the E re-read
             const uint64_t drop = policy_evict_first();  // E reads: last use
+            const int64_t L = p.lay.block_len;
+            const int64_t gap = p.lay.block_stride - p.lay.block_len;
+            // tickets come in batches; the next batch is requested one batch
+            // ahead so the atomic's round trip never stalls the ring
+            int64_t tb = (int64_t)atomicAdd(&p.head->ticket, kTicketBatch);
+            int64_t tnext = 0;
+            unsigned int g = 0;
             for (int it = 0;; ++it) {
                 const int st = it % kStages;
+                if (g == 0) tnext = (int64_t)atomicAdd(&p.head->ticket, kTicketBatch);
+                const int64_t t = tb + g;
+                if (++g == kTicketBatch) {
+                    g = 0;
+                    tb = tnext;
+                }
                 mbar_wait(&sEmpty[st], ((it / kStages) & 1) ^ 1);
-                const int64_t t = (int64_t)atomicAdd(&p.head->ticket, 1u);
                 StageMeta m;
                 if (t >= p.total) {
                     m.kind = 2;
@@ -269,17 +311,24 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                 const EncBlk bk = blks[lo];
                 const EncSegD& sg = segs[bk.seg];
                 const int64_t k = t - bk.tstart;
-                const int64_t chunk = bk.kind == 0 ? k : (int64_t)sg.nE - 1 - k;
+                const int kind = bk.c0 >= 0 ? 0 : 1;
+                const int64_t chunk = kind == 0 ? bk.c0 + k : (int64_t)(-bk.c0 - 1) - k;
                 m.base = chunk * kChunk;
                 m.cnt = (int32_t)min((int64_t)kChunk, sg.n - m.base);
                 m.bulk = sg.aligned ? (m.cnt & ~3) : 0;
                 m.seg = bk.seg;
-                m.kind = bk.kind;
+                m.kind = kind;
+                {
+                    const int64_t f0 = sg.flat_off + m.base;
+                    const int64_t j = f0 / L;
+                    m.code_off = f0 + j * gap;
+                    m.simple = m.bulk == kChunk && f0 + kChunk <= (j + 1) * L;
+                }
                 sMeta[st] = m;
                 if (m.bulk > 0) {
                     mbar_arrive_expect_tx(&sFull[st], (uint32_t)m.bulk * 4u);
                     bulk_g2s(sStage + (size_t)st * kChunk, sg.x + m.base, (uint32_t)m.bulk * 4u, &sFull[st],
-                             bk.kind == 0 ? keep : drop);
+                             kind == 0 ? keep : drop);
                 } else {
                     mbar_arrive(&sFull[st]);
                 }
@@ -294,74 +343,101 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
         const int64_t L = p.lay.block_len;
         const int64_t gap = p.lay.block_stride - p.lay.block_len;
 
+        // A-chunks of one segment are reduced in registers; the CTA publishes
+        // its partial max and chunk count once per run (when the next stage
+        // is not an A-chunk of the same segment), so the global atomics and
+        // barriers are off the per-chunk path.  The CTA whose count completes
+        // the segment builds its table.  Flushing happens before any wait.
+        int aseg = -1;          // segment of the pending A run
+        unsigned int amx = 0;   // per-thread max of bits(|x|) * 2
+        unsigned int acnt = 0;  // A-chunks in the pending run
+
+        auto flush = [&]() {
+            const unsigned int wmx = __reduce_max_sync(0xffffffffu, amx) >> 1;
+            if (lane == 0) sRed[cw] = wmx;
+            nbar_sync(kBarC, kConsumers);
+            if (ctid == 0) {
+                unsigned int mm = 0;
+#pragma unroll
+                for (int w = 0; w < kConsumerWarps; ++w) mm = max(mm, sRed[w]);
+                SegCtl* c = p.ctl + aseg;
+                if (mm) atomicMax(&c->amax, mm);
+                // acq_rel: publishes our max before the count, and (for the
+                // last contributor) makes every other CTA's max visible
+                const unsigned int done = atom_add_acq_rel(&c->a_done, acnt) + acnt;
+                sLast = (done == (unsigned int)segs[aseg].nA);
+                if (sLast) sHdr[3] = (int)ld_acquire(&c->amax);
+            }
+            nbar_sync(kBarC, kConsumers);
+            if (sLast) {
+                // K2 for this segment: scale, thresholds, bucket table
+                const EncSegD& sa = segs[aseg];
+                const unsigned int amax = (unsigned int)sHdr[3];
+                const float scale = amax == 0u ? 1.0f : __uint_as_float(amax);
+                if (ctid == 0) p.ctl[aseg].t_b0 = gtime();
+                if (amax >= kInfBits && ctid == 0) atomicOr(&p.head->status, A8_STATUS_NONFINITE);
+                build_lut(p.book, scale, p.luts + aseg, sT, sCanon, ctid);
+                if (ctid < p.lay.scale_reps) p.lay.scales[ctid * p.lay.scale_block_stride + sa.scale_idx] = scale;
+                __threadfence();  // each thread's table writes are gpu-visible ...
+                nbar_sync(kBarC, kConsumers);
+                if (ctid == 0) {  // ... before the flag is released
+                    p.ctl[aseg].t_b1 = gtime();
+                    st_release(&p.ctl[aseg].ready, 1u);
+                }
+                cur = -1;  // sT / sCanon / sHdr were used as scratch
+            }
+            aseg = -1;
+            amx = 0;
+            acnt = 0;
+        };
+
         for (int it = 0;; ++it) {
             const int st = it % kStages;
             mbar_wait(&sFull[st], (it / kStages) & 1);
             const StageMeta m = sMeta[st];
+            if (aseg >= 0 && (m.kind != 0 || m.seg != aseg)) flush();
             if (m.kind == 2) break;
             const EncSegD& sg = segs[m.seg];
             const float* stage = sStage + (size_t)st * kChunk;
 
             if (m.kind == 0) {
                 // ---------------- A: max |x| over the chunk ----------------
-                unsigned int mx = 0;
+                if (m.bulk == kChunk) {
+                    const uint4* in = reinterpret_cast<const uint4*>(stage) + ctid;
 #pragma unroll
-                for (int q = 0; q < kChunk / (kConsumers * 4); ++q) {
-                    const int i = q * (kConsumers * 4) + ctid * 4;
-                    if (i + 4 <= m.bulk) {
+                    for (int q = 0; q < kChunk / (kConsumers * 4); ++q) {
+                        const uint4 v = in[q * kConsumers];  // bits*2 drops the sign (IMAD), 3-way max
+                        amx = __vimax3_u32(amx, v.x * 2u, v.y * 2u);
+                        amx = __vimax3_u32(amx, v.z * 2u, v.w * 2u);
+                    }
+                } else {
+                    for (int i = ctid * 4; i + 4 <= m.bulk; i += kConsumers * 4) {
                         const uint4 v = *reinterpret_cast<const uint4*>(stage + i);
-                        mx = max(mx, max(max(v.x & 0x7fffffffu, v.y & 0x7fffffffu),
-                                         max(v.z & 0x7fffffffu, v.w & 0x7fffffffu)));
+                        amx = __vimax3_u32(amx, v.x * 2u, v.y * 2u);
+                        amx = __vimax3_u32(amx, v.z * 2u, v.w * 2u);
                     }
+                    for (int i = m.bulk + ctid; i < m.cnt; i += kConsumers)
+                        amx = max(amx, __float_as_uint(sg.x[m.base + i]) * 2u);
                 }
-                for (int i = m.bulk + ctid; i < m.cnt; i += kConsumers)
-                    mx = max(mx, __float_as_uint(sg.x[m.base + i]) & 0x7fffffffu);
-                mx = __reduce_max_sync(0xffffffffu, mx);
                 __syncwarp();
-                if (lane == 0) {
-                    sRed[cw] = mx;
-                    mbar_arrive(&sEmpty[st]);  // stage consumed
-                }
-                nbar_sync(kBarC, kConsumers);
-                if (ctid == 0) {
-                    unsigned int mm = 0;
-#pragma unroll
-                    for (int w = 0; w < kConsumerWarps; ++w) mm = max(mm, sRed[w]);
-                    SegCtl* c = p.ctl + m.seg;
-                    if (mm) atomicMax(&c->amax, mm);
-                    __threadfence();
-                    const unsigned int done = atomicAdd(&c->a_done, 1u);
-                    sLast = (done == (unsigned int)sg.nA - 1u);
-                    if (sLast) {
-                        __threadfence();
-                        sHdr[3] = (int)atomicAdd(&c->amax, 0u);
-                    }
-                }
-                nbar_sync(kBarC, kConsumers);
-                if (sLast) {
-                    // K2 for this segment: scale, thresholds, bucket table
-                    const unsigned int amax = (unsigned int)sHdr[3];
-                    const float scale = amax == 0u ? 1.0f : __uint_as_float(amax);
-                    if (amax >= kInfBits && ctid == 0) atomicOr(&p.head->status, A8_STATUS_NONFINITE);
-                    build_lut(p.book, scale, p.luts + m.seg, sT, sCanon, ctid);
-                    if (ctid < p.lay.scale_reps) p.lay.scales[ctid * p.lay.scale_block_stride + sg.scale_idx] = scale;
-                    __threadfence();
-                    nbar_sync(kBarC, kConsumers);
-                    if (ctid == 0) st_release(&p.ctl[m.seg].ready, 1u);
-                    cur = -1;  // sT / sCanon / sHdr were used as scratch
-                }
+                if (lane == 0) mbar_arrive(&sEmpty[st]);  // stage consumed
+                aseg = m.seg;
+                ++acnt;
                 continue;
             }
 
             // ---------------- E: encode the chunk ----------------------------
             if (cur != m.seg && cur != -2) {
                 nbar_sync(kBarC, kConsumers);  // everyone is done with the old table
-                if (ctid == 0) {
+                if (ctid == 0 && ld_acquire(&p.ctl[m.seg].ready) == 0u) {
+                    const unsigned long long w0 = gtime();
                     unsigned int ns = 32;
                     while (ld_acquire(&p.ctl[m.seg].ready) == 0u) {
                         __nanosleep(ns);
-                        ns = min(ns * 2u, 512u);
+                        ns = min(ns * 2u, 256u);
                     }
+                    atomicAdd(&p.head->wait_ns, gtime() - w0);
+                    atomicAdd(&p.head->waits, 1u);
                 }
                 nbar_sync(kBarC, kConsumers);
                 load_lut_smem(p.luts + m.seg, sE, sT, sCanon, p.book, sHdr, ctid, kConsumers);
@@ -374,10 +450,30 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
             const int32_t kbase = sHdr[1];
             const int32_t lenm1 = sHdr[2];
             unsigned int big = 0;  // max |x| bits (fixed-scale specs detect NaN/Inf here)
+            if (m.simple && valid) {
+                // fast path: a full chunk inside one block, bucket table
+                uint32_t* out = reinterpret_cast<uint32_t*>(codes_base + m.code_off) + ctid;
+                const uint4* in = reinterpret_cast<const uint4*>(stage) + ctid;
+                const uint32_t* eb = sE - kbase;  // indexed by the clamped key
+                const int32_t kmax = kbase + lenm1;
+                if (p.absmax) {
+#pragma unroll
+                    for (int q = 0; q < kChunk / (kConsumers * 4); ++q)
+                        out[q * kConsumers] = encode4_lut(in[q * kConsumers], eb, kbase, kmax);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < kChunk / (kConsumers * 4); ++q) {
+                        const uint4 v = in[q * kConsumers];
+                        out[q * kConsumers] = encode4_lut(v, eb, kbase, kmax);
+                        big = max(big, max(max(v.x & 0x7fffffffu, v.y & 0x7fffffffu),
+                                           max(v.z & 0x7fffffffu, v.w & 0x7fffffffu)));
+                    }
+                }
+            } else {
             const int64_t f0 = sg.flat_off + m.base;
             int64_t j = f0 / L;
             int64_t bnd = (j + 1) * L;
-#pragma unroll
+#pragma unroll 1
             for (int q = 0; q < kChunk / (kConsumers * 4); ++q) {
                 const int i = q * (kConsumers * 4) + ctid * 4;
                 if (i >= m.cnt) break;
@@ -414,6 +510,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                     }
                 }
             }
+            }
             if (!p.absmax && __any_sync(0xffffffffu, big >= kInfBits) && lane == 0)
                 atomicOr(&p.head->status, A8_STATUS_NONFINITE);
             __syncwarp();
@@ -441,9 +538,17 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
         }
         __syncthreads();
         if (tid == 0) {
-            p.head->ticket = 0u;
-            p.head->ctas_done = 0u;
-            p.head->status = 0u;
+            WsHead* h = p.head;
+            h->tr_start = ~h->t_start_inv;
+            h->tr_end = gtime();
+            h->tr_wait_ns = h->wait_ns;
+            h->tr_waits = h->waits;
+            h->ticket = 0u;
+            h->ctas_done = 0u;
+            h->status = 0u;
+            h->waits = 0u;
+            h->t_start_inv = 0ull;
+            h->wait_ns = 0ull;
         }
         __threadfence();
     }
@@ -513,25 +618,39 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(const __grid_consta
         const int64_t f0 = sg.flat_off + base;
 
         if (cnt == kDecChunk && sg.aligned) {
+            // all code words of the chunk are loaded before any store (the
+            // output may alias nothing we read, but the compiler cannot know)
+            float acc[kGroups][4];
+            {
+                uint32_t w[kGroups];
+#pragma unroll
+                for (int q = 0; q < kGroups; ++q) w[q] = ld_stream_u32(src + f0 + q * (kDecThreads * 4) + tid * 4);
+#pragma unroll
+                for (int q = 0; q < kGroups; ++q) {
+                    acc[q][0] = sTab[((w[q] & 255u) << 2) + rep];
+                    acc[q][1] = sTab[(((w[q] >> 8) & 255u) << 2) + rep];
+                    acc[q][2] = sTab[(((w[q] >> 16) & 255u) << 2) + rep];
+                    acc[q][3] = sTab[((w[q] >> 24) << 2) + rep];
+                }
+            }
+            for (int r = 1; r < R; ++r) {
+                const uint8_t* sr = src + (int64_t)r * p.lay.rank_stride + f0 + tid * 4;
+                const float* T = sTab + r * 1024;
+                uint32_t w[kGroups];
+#pragma unroll
+                for (int q = 0; q < kGroups; ++q) w[q] = ld_stream_u32(sr + q * (kDecThreads * 4));
+#pragma unroll
+                for (int q = 0; q < kGroups; ++q) {
+                    acc[q][0] = __fadd_rn(acc[q][0], T[((w[q] & 255u) << 2) + rep]);
+                    acc[q][1] = __fadd_rn(acc[q][1], T[(((w[q] >> 8) & 255u) << 2) + rep]);
+                    acc[q][2] = __fadd_rn(acc[q][2], T[(((w[q] >> 16) & 255u) << 2) + rep]);
+                    acc[q][3] = __fadd_rn(acc[q][3], T[((w[q] >> 24) << 2) + rep]);
+                }
+            }
 #pragma unroll
             for (int q = 0; q < kGroups; ++q) {
                 const int64_t e = q * (kDecThreads * 4) + tid * 4;
-                float a0, a1, a2, a3;
-                {
-                    const uint32_t w = ld_stream_u32(src + f0 + e);
-                    a0 = sTab[((w & 255u) << 2) + rep];
-                    a1 = sTab[(((w >> 8) & 255u) << 2) + rep];
-                    a2 = sTab[(((w >> 16) & 255u) << 2) + rep];
-                    a3 = sTab[((w >> 24) << 2) + rep];
-                }
-                for (int r = 1; r < R; ++r) {
-                    const uint32_t w = ld_stream_u32(src + (int64_t)r * p.lay.rank_stride + f0 + e);
-                    const float* T = sTab + r * 1024;
-                    a0 = __fadd_rn(a0, T[((w & 255u) << 2) + rep]);
-                    a1 = __fadd_rn(a1, T[(((w >> 8) & 255u) << 2) + rep]);
-                    a2 = __fadd_rn(a2, T[(((w >> 16) & 255u) << 2) + rep]);
-                    a3 = __fadd_rn(a3, T[((w >> 24) << 2) + rep]);
-                }
+                float a0 = acc[q][0], a1 = acc[q][1], a2 = acc[q][2], a3 = acc[q][3];
                 if (p.op == 1 && R > 1) {
                     if (pow2) {
                         a0 = __fmul_rn(a0, invN);
@@ -617,53 +736,102 @@ static int cuda_check(const char* what) {
     return A8_OK;
 }
 
-// Ticket order: ascending segment size; a segment of kBigSeg+ elements runs
-// its A-chunks and then its E-chunks (reverse order, L2 reuse); smaller ones
-// are pipelined with a lag so their table builds overlap other work.
+// Ticket order (host).  Segments in ascending size are cut into groups of
+// >= kGroupMin elements.  Per group: all A-chunks, then the held-back tail of
+// the previous group's E pass (its table is long built; this covers the new
+// group's table builds), then the group's E pass in reverse order (the data
+// read last by the A pass -- still in L2 -- first) minus its own last kFill
+// chunks, which are held back as the next group's filler.
 static void schedule(const std::vector<EncSegD>& d, bool absmax, std::vector<EncBlk>* blks) {
     int64_t t = 0;
-    auto push = [&](int s, int kind) {
-        const int64_t cnt = kind == 0 ? d[s].nA : d[s].nE;
-        if (cnt == 0) return;
-        blks->push_back(EncBlk{t, s, kind});
+    auto push = [&](int s, int32_t c0, int64_t cnt) {
+        if (cnt <= 0) return;
+        blks->push_back(EncBlk{t, s, c0});
         t += cnt;
     };
     const int nseg = (int)d.size();
     if (!absmax) {
-        for (int s = 0; s < nseg; ++s) push(s, 1);
-    } else {
-        std::deque<int> pending;
-        for (int s = 0; s < nseg; ++s) {
-            push(s, 0);
-            if (d[s].n >= kBigSeg) {
-                while (!pending.empty()) {
-                    push(pending.front(), 1);
-                    pending.pop_front();
-                }
-                push(s, 1);
-            } else {
-                pending.push_back(s);
-                if ((int)pending.size() > kLag) {
-                    push(pending.front(), 1);
-                    pending.pop_front();
-                }
-            }
-        }
-        while (!pending.empty()) {
-            push(pending.front(), 1);
-            pending.pop_front();
-        }
+        for (int s = 0; s < nseg; ++s) push(s, -d[s].nE, d[s].nE);
+        blks->push_back(EncBlk{t, -1, 0});  // sentinel: total tickets
+        return;
     }
-    blks->push_back(EncBlk{t, -1, 2});  // sentinel: total tickets
+    struct Run {
+        int s;
+        int32_t top;  // first (highest) chunk
+        int64_t cnt;
+    };
+    std::vector<Run> tail;
+    int g0 = 0;
+    while (g0 < nseg) {
+        int g1 = g0;
+        int64_t sum = 0;
+        while (g1 < nseg && (sum < kGroupMin || g1 == g0)) sum += d[g1++].n;
+        for (int s = g0; s < g1; ++s) push(s, 0, d[s].nA);
+        for (const Run& r : tail) push(r.s, -r.top - 1, r.cnt);
+        tail.clear();
+        int64_t total = 0;
+        for (int s = g0; s < g1; ++s) total += d[s].nE;
+        int64_t head = total - std::min<int64_t>(kFill, total / 2);
+        for (int s = g1 - 1; s >= g0; --s) {  // last-read segment first
+            int32_t top = d[s].nE - 1;
+            int64_t cnt = d[s].nE;
+            const int64_t now = std::min(cnt, head);
+            if (now > 0) push(s, -top - 1, now);
+            head -= now;
+            if (cnt > now) tail.push_back(Run{s, (int32_t)(top - now), cnt - now});
+        }
+        g0 = g1;
+    }
+    for (const Run& r : tail) push(r.s, -r.top - 1, r.cnt);
+    blks->push_back(EncBlk{t, -1, 0});  // sentinel: total tickets
 }
 
 }  // namespace a8
 
 using namespace a8;
 
+static size_t ws_bytes_for(int cap) { return plan_off(cap) + plan_bytes(cap); }
+
+// Largest capacity whose layout fits in `bytes` (0 if none).
+static int ws_capacity(size_t bytes) {
+    int lo = 0, hi = 1;
+    while (ws_bytes_for(hi) <= bytes) {
+        lo = hi;
+        hi *= 2;
+        if (hi > (1 << 24)) break;
+    }
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) / 2;
+        if (ws_bytes_for(mid) <= bytes)
+            lo = mid;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+extern "C" int a8_encode_trace(const void* workspace, int nseg, uint64_t* out) {
+    if (!workspace || !out || nseg < 1) return fail(A8_ERR_USAGE, "a8_encode_trace: bad argument");
+    WsHead h;
+    std::vector<SegCtl> c(nseg);
+    const uint8_t* ws = static_cast<const uint8_t*>(workspace);
+    cudaError_t e = cudaMemcpy(&h, ws, sizeof(h), cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(c.data(), ws + ctl_off(), sizeof(SegCtl) * nseg, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
+    out[0] = h.tr_start;
+    out[1] = h.tr_end;
+    out[2] = h.tr_wait_ns;
+    out[3] = h.tr_waits;
+    for (int i = 0; i < nseg; ++i) {
+        out[4 + 2 * i] = c[i].t_b0;
+        out[5 + 2 * i] = c[i].t_b1;
+    }
+    return A8_OK;
+}
+
 extern "C" size_t a8_workspace_bytes(int nseg) {
     if (nseg < 1) nseg = 1;
-    return plan_off(nseg) + plan_bytes(nseg);
+    return ws_bytes_for(nseg);
 }
 
 extern "C" int a8_device_info(int device, int* num_sms, int* enc_ctas_per_sm, int* dec_ctas_per_sm) {
@@ -678,7 +846,8 @@ extern "C" int a8_device_info(int device, int* num_sms, int* enc_ctas_per_sm, in
 
 extern "C" int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_dev, int norm,
                          const void* static_lut_dev, a8_layout_t layout, void* workspace,
-                         const uint32_t* status_in, uint32_t* status_out, void* stream) {
+                         size_t workspace_bytes, const uint32_t* status_in, uint32_t* status_out,
+                         void* stream) {
     if (nseg <= 0) return fail(A8_ERR_USAGE, "a8_encode: need at least one segment");
     if (!segs || !book_dev || !workspace || !status_out) return fail(A8_ERR_USAGE, "a8_encode: null argument");
     if (norm != A8_NORM_ABSMAX && !static_lut_dev)
@@ -722,8 +891,10 @@ extern "C" int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_de
     p.book = static_cast<const a8_book_t*>(book_dev);
     p.static_lut = static_cast<const a8_lut_t*>(static_lut_dev);
     p.head = reinterpret_cast<WsHead*>(ws);
+    const int cap = ws_capacity(workspace_bytes);
+    if (cap < nseg) return fail(A8_ERR_USAGE, "a8_encode: workspace too small for the segment count");
     p.ctl = reinterpret_cast<SegCtl*>(ws + ctl_off());
-    p.luts = reinterpret_cast<a8_lut_t*>(ws + lut_off(nseg));
+    p.luts = reinterpret_cast<a8_lut_t*>(ws + lut_off(cap));
     p.status_in = status_in;
     p.status_out = status_out;
     p.nseg = nseg;
@@ -735,7 +906,7 @@ extern "C" int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_de
         std::copy(d.begin(), d.end(), p.segs);
         std::copy(blks.begin(), blks.end(), p.blks);
     } else {
-        uint8_t* plan = ws + plan_off(nseg);
+        uint8_t* plan = ws + plan_off(cap);
         const size_t sb = sizeof(EncSegD) * nseg;
         cudaMemcpyAsync(plan, d.data(), sb, cudaMemcpyHostToDevice, st);
         cudaMemcpyAsync(plan + sb, blks.data(), sizeof(EncBlk) * blks.size(), cudaMemcpyHostToDevice, st);
@@ -749,7 +920,7 @@ extern "C" int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_de
 
 extern "C" int a8_decode(const a8_dec_seg_t* segs, int nseg, const void* book_dev, a8_layout_t layout,
                          int nranks, int op, int status_idx, int status_blocks, uint32_t* status_out,
-                         void* workspace, void* stream) {
+                         void* workspace, size_t workspace_bytes, void* stream) {
     if (nseg <= 0 && !status_out) return A8_OK;
     if (nseg < 0) return fail(A8_ERR_USAGE, "a8_decode: negative segment count");
     if (status_out && (status_idx < 0 || status_blocks < 1)) return fail(A8_ERR_USAGE, "a8_decode: bad status request");
@@ -794,7 +965,9 @@ extern "C" int a8_decode(const a8_dec_seg_t* segs, int nseg, const void* book_de
     if (nseg <= kInlineSegs) {
         std::copy(d.begin(), d.begin() + nseg, p.segs);
     } else {
-        uint8_t* plan = static_cast<uint8_t*>(workspace) + plan_off(nseg);
+        const int cap = ws_capacity(workspace_bytes);
+        if (cap < nseg) return fail(A8_ERR_USAGE, "a8_decode: workspace too small for the segment count");
+        uint8_t* plan = static_cast<uint8_t*>(workspace) + plan_off(cap);
         cudaMemcpyAsync(plan, d.data(), sizeof(DecSegD) * nseg, cudaMemcpyHostToDevice, st);
         p.segs_dev = reinterpret_cast<const DecSegD*>(plan);
     }

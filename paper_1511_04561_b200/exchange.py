@@ -84,7 +84,7 @@ class CudaSegmentCodec(SegmentCodec):
         stream = torch.cuda.current_stream(dev).cuda_stream
         ws = workspace(dev, stream, n)
         N.check(N.lib.a8_encode(segs, n, book.data_ptr(), cb.spec.norm_code,
-                                None if lut is None else lut.data_ptr(), lay, ws.data_ptr(),
+                                None if lut is None else lut.data_ptr(), lay, ws.data_ptr(), ws.numel(),
                                 None if status_in is None else status_in.data_ptr(),
                                 base + status_off, stream))
 
@@ -104,7 +104,7 @@ class CudaSegmentCodec(SegmentCodec):
         ws = workspace(dev, stream, max(n, 1))
         N.check(N.lib.a8_decode(segs, n, book.data_ptr(), lay, nranks, op, status_idx,
                                 status_blocks, None if status_out is None else status_out.data_ptr(),
-                                ws.data_ptr(), stream))
+                                ws.data_ptr(), ws.numel(), stream))
 
 
 # ---------------------------------------------------------------------------

@@ -96,7 +96,7 @@ def _lut_encode(x, lut, book):
         e = np.frombuffer(bytes(lut.e), np.uint32)
         j = np.clip((a >> 16).astype(np.int64) - lut.kbase, 0, lut.len - 1)
         v = e[j]
-        c = np.where((a & 0xFFFF) >= (v >> 16), v >> 8, v) & 0xFF
+        c = np.where(((a << 16) | 0xFFFF) >= v, v >> 8, v) & 0xFF
     else:
         T = np.frombuffer(bytes(lut.T), np.uint32)[:127]
         c = np.frombuffer(bytes(book.codes), np.uint8)[np.searchsorted(T, a, side="right")].astype(np.uint32)
@@ -127,10 +127,10 @@ def test_error_codes_map_to_reference_exceptions():
         N.check(N.lib.a8_fixed_scale(1, 0, C.byref(s)))
     lay = N.Layout()
     with pytest.raises(A.UsageError):  # no segment: rejected before any launch
-        N.check(N.lib.a8_encode(None, 0, None, 1, None, lay, None, None, None, None))
+        N.check(N.lib.a8_encode(None, 0, None, 1, None, lay, None, 0, None, None, None))
     with pytest.raises(A.UsageError):
         N.check(N.lib.a8_decode((N.DecSeg * 1)(), 1, C.c_void_p(16), lay, 0, 0, -1, 0, None,
-                                C.c_void_p(16), None))
+                                C.c_void_p(16), 0, None))
 
 
 def test_compute_has_no_cpu_fallback():
@@ -185,3 +185,20 @@ def test_hook_config_mirrors_reference():
     assert A.default_hook_spec("dynamic-tree", "model-parallel") == A.DataTypeSpec("dynamic-tree", "absmax")
     assert A.default_hook_spec("mantissa", "model-parallel") == A.DataTypeSpec("mantissa", "decade", 2)
     assert A.default_hook_spec("static-tree", "data-parallel") == A.DataTypeSpec("static-tree")
+
+
+@pytest.mark.parametrize("kind", ["dynamic-tree", "static-tree", "linear", "mantissa"])
+def test_thresholds_at_random_scales_match_bisection(kind):
+    """The library's guess-and-walk threshold search equals the oracle's full
+    bisection of the reference decision at random and extreme scales."""
+    rng = np.random.default_rng({"dynamic-tree": 1, "static-tree": 2, "linear": 3, "mantissa": 4}[kind])
+    scales = list((10.0 ** rng.uniform(-44, 38, size=12)).astype(np.float32))
+    scales += [np.float32(x) for x in (1e-45, 2.5e-42, 1.1754942e-38, 1.0, 3.4028235e38, 4.998160362243652)]
+    cb = A.build_codebook(A.DataTypeSpec(kind))
+    for s in scales:
+        if not np.isfinite(s) or s <= 0:
+            continue
+        lut = N.Lut()
+        N.check(N.lib.a8_build_lut_host(C.byref(cb._book), float(s), C.byref(lut)))
+        T = np.frombuffer(bytes(lut.T), np.uint32)[:127]
+        assert np.array_equal(T, O.thresholds(kind, float(s))), (kind, s)

@@ -63,7 +63,29 @@ def run(sizes, spec, iters, dev):
         torch.cuda.synchronize()
         ms = float(np.median([e0.elapsed_time(e1) for e0, e1 in evs]))
         res[name] = {"ms": ms, "GBps": 5.0 * n / (ms * 1e-3) / 1e9}
+    if TRACE:
+        import ctypes as C
+
+        from paper_1511_04561_b200 import _native as N
+        from paper_1511_04561_b200.codecs import workspace
+
+        enc()
+        torch.cuda.synchronize()
+        ws = workspace(dev, torch.cuda.current_stream(dev).cuda_stream, len(xs))
+        out = (C.c_uint64 * (4 + 2 * len(xs)))()
+        N.check(N.lib.a8_encode_trace(ws.data_ptr(), len(xs), out))
+        t0 = out[0]
+        order = sorted(range(len(xs)), key=lambda i: xs[i].numel())
+        res["trace"] = {
+            "kernel_us": (out[1] - t0) / 1e3, "wait_cta_us": out[2] / 1e3, "waits": out[3],
+            "builds": [{"n": xs[order[k]].numel(), "start_us": round((out[4 + 2 * k] - t0) / 1e3, 2),
+                        "build_us": round((out[5 + 2 * k] - out[4 + 2 * k]) / 1e3, 2)}
+                       for k in range(len(xs)) if out[4 + 2 * k] >= t0],
+        }
     return n, res
+
+
+TRACE = "--trace" in sys.argv
 
 
 def main():
@@ -71,6 +93,7 @@ def main():
     ap.add_argument("--case", default="alexnet")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--spec", default="dynamic-tree/absmax")
+    ap.add_argument("--trace", action="store_true")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     spec = A.parse_spec(a.spec)
@@ -78,6 +101,25 @@ def main():
         cases = [("alexnet", ALEXNET)]
     elif a.case == "single":
         cases = [("single_2^26", [(1 << 26,)])]
+    elif a.case == "bw":
+        # torch reference kernels on 2^28 floats: read-only / write-only / copy
+        x = torch.randn(1 << 28, device=dev)
+        y = torch.empty_like(x)
+        for name, fn, nbytes in (("read(sum)", lambda: x.sum(), 4 << 28),
+                                 ("write(fill)", lambda: y.fill_(1.0), 4 << 28),
+                                 ("copy", lambda: y.copy_(x), 8 << 28)):
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(a.iters):
+                fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / a.iters
+            print(json.dumps({"case": name, "ms": ms, "GBps": nbytes / (ms * 1e-3) / 1e9}), flush=True)
+        return
     elif a.case == "sweep":
         cases = [(f"2^{k}", [(1 << k,)]) for k in range(10, 31, 2)]
     else:
