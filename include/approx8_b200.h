@@ -169,8 +169,9 @@ int a8_decode(const a8_dec_seg_t* segs, int nseg, const void* book_dev, a8_layou
 /* Diagnostics: globaltimer trace of the last a8_encode on `workspace`
  * (synchronous device->host copy).  out[0..3] = kernel start ns, end ns,
  * total CTA time spent waiting for segment tables (ns), number of waits;
- * out[4 + 2k], out[5 + 2k] = table build start/end of the k-th segment in
- * scheduling order (ascending size).  Needs 4 + 2*nseg entries.            */
+ * out[4 + 4k .. 7 + 4k] = table build start, thresholds done, table filled,
+ * table published, for the k-th segment in scheduling order (ascending
+ * size).  Needs 4 + 4*nseg entries.                                        */
 int a8_encode_trace(const void* workspace, int nseg, uint64_t* out);
 
 /* Number of SMs and the persistent grid sizes the kernels use on `device`. */

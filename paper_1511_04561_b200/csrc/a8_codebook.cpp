@@ -129,7 +129,10 @@ extern "C" int a8_build_lut_host(const a8_book_t* book, float scale, a8_lut_t* o
     out->kbase = kbase;
     out->len = len;
     out->valid = 0;
-    if (len <= (uint32_t)a8::kLutMax)
-        out->valid = a8::lut_fill(out->T, F, book->codes, kbase, 0, len, out->e) ? 1u : 0u;
+    if (len <= (uint32_t)a8::kLutMax) {
+        bool ok = true;
+        for (uint32_t j = 0; j < len; ++j) ok &= a8::lut_entry(out->T, F, book->codes, kbase, j, &out->e[j]);
+        out->valid = ok ? 1u : 0u;
+    }
     return A8_OK;
 }

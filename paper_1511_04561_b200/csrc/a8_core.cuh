@@ -123,46 +123,39 @@ A8_HD bool scale_ok(float s) {
     return b != 0u && b < kInfBits;  // positive, finite, non-zero
 }
 
-// Entries [j0, j1) of the bucket table.  T[0..F) are the finite thresholds
-// (non-decreasing).  Entry = t_low << 16 | code_hi << 8 | code_lo where t_low
-// is the low half of the bucket's threshold: an element of the bucket takes
-// code_hi iff lo16(bits) >= t_low, which is exactly
+// Bucket table entry encoding: t_low << 16 | code_hi << 8 | code_lo, where
+// t_low is the low half of the bucket's threshold: an element of the bucket
+// takes code_hi iff lo16(bits) >= t_low, which is exactly
 // ((bits << 16) | 0xffff) >= entry because codes never exceed 0x7f7f.
 // A bucket without a threshold stores t_low = 0 and code_hi = code_lo.
-// Returns false if a bucket holds two distinct thresholds.
-A8_HD bool lut_fill(const uint32_t* T, uint32_t F, const uint8_t* canon, int32_t kbase, uint32_t j0,
-                    uint32_t j1, uint32_t* e) {
-    if (j0 >= j1) return true;
-    // lo = #{T < start of bucket j0}
-    const int64_t k0 = (int64_t)kbase + j0;
-    const uint32_t start0 = k0 <= 0 ? 0u : (uint32_t)(k0 << kKeyShift);
-    uint32_t lo = 0, n = F;
-    while (n > 0) {  // lower_bound
-        const uint32_t half = n >> 1;
-        if (T[lo + half] < start0) {
-            lo += half + 1;
-            n -= half + 1;
-        } else {
-            n = half;
-        }
+
+// #{i < F : T[i] < key}, branch-free over a 128-entry array (F <= 127).
+A8_HD uint32_t count_below(const uint32_t* T, uint32_t F, uint32_t key) {
+    uint32_t p = 0;
+#if defined(__CUDA_ARCH__)
+#pragma unroll
+#endif
+    for (uint32_t step = 64; step; step >>= 1)
+        if (p + step <= F && T[p + step - 1] < key) p += step;
+    return p;
+}
+
+// One entry of the bucket table (same encoding as lut_fill), computed
+// independently of its neighbours.  Returns false if the bucket holds two
+// distinct thresholds.
+A8_HD bool lut_entry(const uint32_t* T, uint32_t F, const uint8_t* canon, int32_t kbase, uint32_t j,
+                     uint32_t* out) {
+    const int64_t k = (int64_t)kbase + j;
+    const uint32_t start = k <= 0 ? 0u : (uint32_t)(k << kKeyShift);
+    const uint32_t end = (uint32_t)((k + 1) << kKeyShift);  // k+1 <= 0x7f81
+    const uint32_t lo = count_below(T, F, start);
+    const uint32_t hi = count_below(T, F, end);
+    if (hi == lo) {
+        *out = (uint32_t)canon[lo] | ((uint32_t)canon[lo] << 8);
+        return true;
     }
-    bool ok = true;
-    for (uint32_t j = j0; j < j1; ++j) {
-        const int64_t k = (int64_t)kbase + j;
-        const uint32_t end = (uint32_t)((k + 1) << kKeyShift);  // k+1 <= 0x7f81
-        uint32_t hi = lo;
-        while (hi < F && T[hi] < end) ++hi;
-        uint32_t v;
-        if (hi == lo) {
-            v = (uint32_t)canon[lo] | ((uint32_t)canon[lo] << 8);
-        } else {
-            if (T[lo] != T[hi - 1]) ok = false;
-            v = (uint32_t)canon[lo] | ((uint32_t)canon[hi] << 8) | ((T[lo] & 0xffffu) << 16);
-        }
-        e[j - j0] = v;
-        lo = hi;
-    }
-    return ok;
+    *out = (uint32_t)canon[lo] | ((uint32_t)canon[hi] << 8) | ((T[lo] & 0xffffu) << 16);
+    return T[lo] == T[hi - 1];
 }
 
 // Table geometry from the thresholds: keys [kmin-1, kmax+1].

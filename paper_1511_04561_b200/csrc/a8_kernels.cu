@@ -45,6 +45,7 @@ constexpr int kMaxRanks = 16;
 
 constexpr int kInlineSegs = 32;
 constexpr int kInlineBlks = 3 * kInlineSegs + 2;
+static int max_blocks(int nseg) { return 6 * nseg + 8; }
 constexpr int64_t kGroupMin = 2 << 20;  // schedule segments in groups of at least this many elements
 constexpr int64_t kFill = 768;          // E-chunks of the previous group that cover a table build
 
@@ -61,12 +62,17 @@ struct EncSegD {
     int32_t aligned;  // x is 16-byte aligned (bulk copies allowed)
 };
 
-// A contiguous run of tickets over one segment: c0 >= 0 -> A-chunks (max-abs)
-// c0, c0+1, ...; c0 < 0 -> E-chunks (encode) -c0-1, -c0-2, ... (descending).
+// Ticket kinds.  A: max-abs of a chunk; E: encode a chunk with the segment's
+// table; F: a whole single-chunk segment (max, thresholds and encode in one
+// CTA, no cross-CTA dependency); END: no more work.
+constexpr int kA = 0, kE = 1, kEnd = 2, kF = 3;
+
+// A contiguous run of tickets over one segment: chunks c0, c0+1, ... (A, F)
+// or c0, c0-1, ... (E).  c0k = c0 << 2 | kind.
 struct EncBlk {
     int64_t tstart;
     int32_t seg;
-    int32_t c0;
+    int32_t c0k;
 };
 
 struct DecSegD {
@@ -98,6 +104,7 @@ struct SegCtl {
     unsigned int ready;
     unsigned int pad;
     unsigned long long t_b0, t_b1;  // table build start / end (globaltimer ns), trace
+    unsigned long long t_thr, t_fill;  // thresholds done / table filled, trace
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -151,7 +158,7 @@ static size_t ctl_off() { return sizeof(WsHead); }
 static size_t lut_off(int cap) { return align_up(ctl_off() + sizeof(SegCtl) * (size_t)cap, 256); }
 static size_t plan_off(int cap) { return align_up(lut_off(cap) + sizeof(a8_lut_t) * (size_t)cap, 256); }
 static size_t plan_bytes(int nseg) {
-    const size_t enc = sizeof(EncSegD) * (size_t)nseg + sizeof(EncBlk) * (size_t)(3 * nseg + 2);
+    const size_t enc = sizeof(EncSegD) * (size_t)nseg + sizeof(EncBlk) * (size_t)max_blocks(nseg);
     const size_t dec = sizeof(DecSegD) * (size_t)nseg;
     return align_up(std::max(enc, dec), 256);
 }
@@ -160,26 +167,33 @@ static size_t plan_bytes(int nseg) {
 // K2: thresholds + bucket table for one scale, built by the consumer warps
 // into global memory (`dst`), staged through shared memory.
 
-__device__ void build_lut(const a8_book_t* book, float scale, a8_lut_t* dst, uint32_t* sT, uint8_t* sCanon,
-                          int ctid) {
-    const int D = book->ndistinct;
+__device__ __forceinline__ unsigned long long gtime();
+
+// sV / sCanon: the codebook's distinct values and canonical codes, staged
+// in shared memory at kernel start; D = number of distinct values.
+__device__ void build_lut(const double* sV, const uint8_t* sCanon, int D, float scale, a8_lut_t* dst,
+                          uint32_t* sT, int ctid, unsigned long long* tr) {
     if (ctid < 128) {
-        sCanon[ctid] = book->codes[ctid];
         uint32_t t = kInfBits;
-        if (scale_ok(scale) && ctid + 1 < D) t = threshold((double)scale, book->values[ctid], book->values[ctid + 1]);
+        if (scale_ok(scale) && ctid + 1 < D) t = threshold((double)scale, sV[ctid], sV[ctid + 1]);
         sT[ctid] = t;
     }
     const int F = nbar_popc(kBarC, kConsumers, ctid < 127 && sT[ctid < 128 ? ctid : 0] < kInfBits);
+    if (tr && ctid == 0) tr[0] = gtime();
     int32_t kbase;
     uint32_t len;
     lut_geometry(sT, (uint32_t)F, &kbase, &len);
     bool ok = true;
-    if (len <= (uint32_t)kLutMax) {
-        const uint32_t per = (len + kConsumers - 1) / kConsumers;
-        const uint32_t j0 = min(len, per * ctid), j1 = min(len, j0 + per);
-        ok = lut_fill(sT, (uint32_t)F, sCanon, kbase, j0, j1, dst->e + j0);
+    if (len <= (uint32_t)kLutMax) {  // independent entries, strided: ILP + coalesced stores
+#pragma unroll 4
+        for (uint32_t j = ctid; j < len; j += kConsumers) {
+            uint32_t v;
+            ok &= lut_entry(sT, (uint32_t)F, sCanon, kbase, j, &v);
+            dst->e[j] = v;
+        }
     }
     const int valid = nbar_and(kBarC, kConsumers, ok) && len <= (uint32_t)kLutMax;
+    if (tr && ctid == 0) tr[1] = gtime();
     if (ctid < 128) dst->T[ctid] = sT[ctid];
     if (ctid == 0) {
         dst->len = len;
@@ -246,6 +260,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
     __shared__ __align__(16) uint32_t sE[kLutMax];
     __shared__ uint32_t sT[128];
     __shared__ uint8_t sCanon[128];
+    __shared__ double sV[128];
     __shared__ __align__(8) uint64_t sFull[kStages];
     __shared__ __align__(8) uint64_t sEmpty[kStages];
     __shared__ StageMeta sMeta[kStages];
@@ -268,6 +283,10 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
         mbar_fence_init();
     }
     if (tid == 0) atomicMax(&p.head->t_start_inv, ~gtime());
+    if (tid >= 32 && tid < 32 + 128) {  // codebook in shared memory (table builds)
+        sV[tid - 32] = p.book->values[tid - 32];
+        sCanon[tid - 32] = p.book->codes[tid - 32];
+    }
     if (!p.absmax && tid >= 32)  // fixed scale: one table for every segment
         load_lut_smem(p.static_lut, sE, sT, sCanon, p.book, sHdr, tid - 32, kConsumers);
     __syncthreads();
@@ -295,7 +314,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                 mbar_wait(&sEmpty[st], ((it / kStages) & 1) ^ 1);
                 StageMeta m;
                 if (t >= p.total) {
-                    m.kind = 2;
+                    m.kind = kEnd;
                     sMeta[st] = m;
                     mbar_arrive(&sFull[st]);
                     break;
@@ -311,8 +330,9 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                 const EncBlk bk = blks[lo];
                 const EncSegD& sg = segs[bk.seg];
                 const int64_t k = t - bk.tstart;
-                const int kind = bk.c0 >= 0 ? 0 : 1;
-                const int64_t chunk = kind == 0 ? bk.c0 + k : (int64_t)(-bk.c0 - 1) - k;
+                const int kind = bk.c0k & 3;
+                const int64_t c0 = bk.c0k >> 2;
+                const int64_t chunk = kind == kE ? c0 - k : c0 + k;
                 m.base = chunk * kChunk;
                 m.cnt = (int32_t)min((int64_t)kChunk, sg.n - m.base);
                 m.bulk = sg.aligned ? (m.cnt & ~3) : 0;
@@ -328,7 +348,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                 if (m.bulk > 0) {
                     mbar_arrive_expect_tx(&sFull[st], (uint32_t)m.bulk * 4u);
                     bulk_g2s(sStage + (size_t)st * kChunk, sg.x + m.base, (uint32_t)m.bulk * 4u, &sFull[st],
-                             kind == 0 ? keep : drop);
+                             kind == kA ? keep : drop);
                 } else {
                     mbar_arrive(&sFull[st]);
                 }
@@ -376,7 +396,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                 const float scale = amax == 0u ? 1.0f : __uint_as_float(amax);
                 if (ctid == 0) p.ctl[aseg].t_b0 = gtime();
                 if (amax >= kInfBits && ctid == 0) atomicOr(&p.head->status, A8_STATUS_NONFINITE);
-                build_lut(p.book, scale, p.luts + aseg, sT, sCanon, ctid);
+                build_lut(sV, sCanon, p.book->ndistinct, scale, p.luts + aseg, sT, ctid, &p.ctl[aseg].t_thr);
                 if (ctid < p.lay.scale_reps) p.lay.scales[ctid * p.lay.scale_block_stride + sa.scale_idx] = scale;
                 __threadfence();  // each thread's table writes are gpu-visible ...
                 nbar_sync(kBarC, kConsumers);
@@ -395,30 +415,38 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
             const int st = it % kStages;
             mbar_wait(&sFull[st], (it / kStages) & 1);
             const StageMeta m = sMeta[st];
-            if (aseg >= 0 && (m.kind != 0 || m.seg != aseg)) flush();
-            if (m.kind == 2) break;
+            if (aseg >= 0 && (m.kind != kA || m.seg != aseg)) flush();
+            if (m.kind == kEnd) break;
             const EncSegD& sg = segs[m.seg];
             const float* stage = sStage + (size_t)st * kChunk;
 
-            if (m.kind == 0) {
-                // ---------------- A: max |x| over the chunk ----------------
+            // per-thread max of bits(x) * 2 over the chunk (the doubling drops
+            // the sign on the FMA pipe; 3-way integer max)
+            auto part_max = [&]() -> unsigned int {
+                unsigned int mx = 0;
                 if (m.bulk == kChunk) {
                     const uint4* in = reinterpret_cast<const uint4*>(stage) + ctid;
 #pragma unroll
                     for (int q = 0; q < kChunk / (kConsumers * 4); ++q) {
-                        const uint4 v = in[q * kConsumers];  // bits*2 drops the sign (IMAD), 3-way max
-                        amx = __vimax3_u32(amx, v.x * 2u, v.y * 2u);
-                        amx = __vimax3_u32(amx, v.z * 2u, v.w * 2u);
+                        const uint4 v = in[q * kConsumers];
+                        mx = __vimax3_u32(mx, v.x * 2u, v.y * 2u);
+                        mx = __vimax3_u32(mx, v.z * 2u, v.w * 2u);
                     }
                 } else {
                     for (int i = ctid * 4; i + 4 <= m.bulk; i += kConsumers * 4) {
                         const uint4 v = *reinterpret_cast<const uint4*>(stage + i);
-                        amx = __vimax3_u32(amx, v.x * 2u, v.y * 2u);
-                        amx = __vimax3_u32(amx, v.z * 2u, v.w * 2u);
+                        mx = __vimax3_u32(mx, v.x * 2u, v.y * 2u);
+                        mx = __vimax3_u32(mx, v.z * 2u, v.w * 2u);
                     }
                     for (int i = m.bulk + ctid; i < m.cnt; i += kConsumers)
-                        amx = max(amx, __float_as_uint(sg.x[m.base + i]) * 2u);
+                        mx = max(mx, __float_as_uint(sg.x[m.base + i]) * 2u);
                 }
+                return mx;
+            };
+
+            if (m.kind == kA) {
+                // ---------------- A: max |x| over the chunk ----------------
+                amx = max(amx, part_max());
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&sEmpty[st]);  // stage consumed
                 aseg = m.seg;
@@ -426,6 +454,31 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                 continue;
             }
 
+            int valid;
+            int32_t kbase, lenm1;
+            if (m.kind == kF) {
+                // -------- F: a single-chunk segment, entirely in this CTA ------
+                const unsigned int wmx = __reduce_max_sync(0xffffffffu, part_max()) >> 1;
+                if (lane == 0) sRed[cw] = wmx;
+                nbar_sync(kBarC, kConsumers);
+                unsigned int amax = 0;
+#pragma unroll
+                for (int w = 0; w < kConsumerWarps; ++w) amax = max(amax, sRed[w]);
+                const float scale = amax == 0u ? 1.0f : __uint_as_float(amax);
+                if (ctid < 128) {
+                    uint32_t t = kInfBits;
+                    if (scale_ok(scale) && ctid + 1 < p.book->ndistinct)
+                        t = threshold((double)scale, sV[ctid], sV[ctid + 1]);
+                    sT[ctid] = t;
+                }
+                if (amax >= kInfBits && ctid == 0) atomicOr(&p.head->status, A8_STATUS_NONFINITE);
+                if (ctid < p.lay.scale_reps) p.lay.scales[ctid * p.lay.scale_block_stride + sg.scale_idx] = scale;
+                nbar_sync(kBarC, kConsumers);  // thresholds ready; sRed fully read
+                valid = 0;  // encode by branch-free search over sT
+                kbase = 0;
+                lenm1 = 0;
+                cur = -1;  // sT now holds this segment's thresholds
+            } else {
             // ---------------- E: encode the chunk ----------------------------
             if (cur != m.seg && cur != -2) {
                 nbar_sync(kBarC, kConsumers);  // everyone is done with the old table
@@ -446,9 +499,10 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
             }
             if (cur == -2 && m.base == 0 && ctid < p.lay.scale_reps)
                 p.lay.scales[ctid * p.lay.scale_block_stride + sg.scale_idx] = p.static_lut->scale;
-            const int valid = sHdr[0];
-            const int32_t kbase = sHdr[1];
-            const int32_t lenm1 = sHdr[2];
+            valid = sHdr[0];
+            kbase = sHdr[1];
+            lenm1 = sHdr[2];
+            }
             unsigned int big = 0;  // max |x| bits (fixed-scale specs detect NaN/Inf here)
             if (m.simple && valid) {
                 // fast path: a full chunk inside one block, bucket table
@@ -736,53 +790,94 @@ static int cuda_check(const char* what) {
     return A8_OK;
 }
 
-// Ticket order (host).  Segments in ascending size are cut into groups of
-// >= kGroupMin elements.  Per group: all A-chunks, then the held-back tail of
-// the previous group's E pass (its table is long built; this covers the new
-// group's table builds), then the group's E pass in reverse order (the data
-// read last by the A pass -- still in L2 -- first) minus its own last kFill
-// chunks, which are held back as the next group's filler.
+// Ticket order (host).
+//  * Fixed-scale specs: E-chunks only.
+//  * absmax: single-chunk segments become one F ticket each (no dependency),
+//    issued first.  The other segments, in descending size, form groups of
+//    >= kGroupMin elements.  Group i's E pass (reverse chunk order, so the
+//    data the A pass read last -- still in L2 -- comes first) can start only
+//    once its tables are built; the kFill tickets before it are independent
+//    work that covers the build: the first A-chunks of group i+1, topped up
+//    with held-back tail E-chunks of earlier groups (the L2-cold part of
+//    their E pass, whose tables are long done).
 static void schedule(const std::vector<EncSegD>& d, bool absmax, std::vector<EncBlk>* blks) {
+    struct Run {
+        int s;
+        int kind;
+        int64_t c0;  // first chunk
+        int64_t cnt;
+    };
     int64_t t = 0;
-    auto push = [&](int s, int32_t c0, int64_t cnt) {
-        if (cnt <= 0) return;
-        blks->push_back(EncBlk{t, s, c0});
-        t += cnt;
+    auto emit = [&](const Run& r) {
+        if (r.cnt <= 0) return;
+        blks->push_back(EncBlk{t, r.s, (int32_t)((r.c0 << 2) | r.kind)});
+        t += r.cnt;
+    };
+    auto emit_all = [&](std::deque<Run>& q) {
+        for (const Run& r : q) emit(r);
+        q.clear();
+    };
+    auto total = [](const std::deque<Run>& q) {
+        int64_t n = 0;
+        for (const Run& r : q) n += r.cnt;
+        return n;
+    };
+    // move the first `want` chunks of q into out (splitting a run if needed)
+    auto take = [](std::deque<Run>& q, int64_t want, std::deque<Run>& out) {
+        while (want > 0 && !q.empty()) {
+            Run& r = q.front();
+            const int64_t now = std::min(want, r.cnt);
+            out.push_back(Run{r.s, r.kind, r.c0, now});
+            r.c0 += r.kind == kE ? -now : now;
+            r.cnt -= now;
+            want -= now;
+            if (r.cnt == 0) q.pop_front();
+        }
     };
     const int nseg = (int)d.size();
     if (!absmax) {
-        for (int s = 0; s < nseg; ++s) push(s, -d[s].nE, d[s].nE);
+        for (int s = 0; s < nseg; ++s) emit(Run{s, kE, d[s].nE - 1, d[s].nE});
         blks->push_back(EncBlk{t, -1, 0});  // sentinel: total tickets
         return;
     }
-    struct Run {
-        int s;
-        int32_t top;  // first (highest) chunk
-        int64_t cnt;
-    };
-    std::vector<Run> tail;
-    int g0 = 0;
-    while (g0 < nseg) {
-        int g1 = g0;
-        int64_t sum = 0;
-        while (g1 < nseg && (sum < kGroupMin || g1 == g0)) sum += d[g1++].n;
-        for (int s = g0; s < g1; ++s) push(s, 0, d[s].nA);
-        for (const Run& r : tail) push(r.s, -r.top - 1, r.cnt);
-        tail.clear();
-        int64_t total = 0;
-        for (int s = g0; s < g1; ++s) total += d[s].nE;
-        int64_t head = total - std::min<int64_t>(kFill, total / 2);
-        for (int s = g1 - 1; s >= g0; --s) {  // last-read segment first
-            int32_t top = d[s].nE - 1;
-            int64_t cnt = d[s].nE;
-            const int64_t now = std::min(cnt, head);
-            if (now > 0) push(s, -top - 1, now);
-            head -= now;
-            if (cnt > now) tail.push_back(Run{s, (int32_t)(top - now), cnt - now});
+    for (int s = 0; s < nseg; ++s)
+        if (d[s].n <= kChunk) emit(Run{s, kF, 0, 1});
+    // groups over the multi-chunk segments, largest first (d is ascending)
+    std::vector<std::deque<Run>> gA, gE;
+    {
+        int s = nseg - 1;
+        while (s >= 0 && d[s].n > kChunk) {
+            std::deque<Run> a, e;
+            int64_t sum = 0;
+            int first = s;
+            while (s >= 0 && d[s].n > kChunk && (sum < kGroupMin || s == first)) {
+                a.push_back(Run{s, kA, 0, d[s].nA});
+                sum += d[s].n;
+                --s;
+            }
+            for (auto it = a.rbegin(); it != a.rend(); ++it)  // last-read segment first
+                e.push_back(Run{it->s, kE, d[it->s].nE - 1, d[it->s].nE});
+            gA.push_back(std::move(a));
+            gE.push_back(std::move(e));
         }
-        g0 = g1;
     }
-    for (const Run& r : tail) push(r.s, -r.top - 1, r.cnt);
+    const int ng = (int)gA.size();
+    std::deque<Run> held;  // L2-cold E tails, available as filler
+    if (ng > 0) emit_all(gA[0]);
+    for (int i = 0; i < ng; ++i) {
+        std::deque<Run> fill;
+        if (i + 1 < ng) take(gA[i + 1], kFill, fill);
+        take(held, kFill - total(fill), fill);
+        emit_all(fill);
+        std::deque<Run> head;
+        const int64_t te = total(gE[i]);
+        take(gE[i], i + 1 < ng ? te - std::min<int64_t>(kFill, te / 2) : te, head);
+        emit_all(head);
+        for (const Run& r : gE[i]) held.push_back(r);  // this group's tail
+        gE[i].clear();
+        if (i + 1 < ng) emit_all(gA[i + 1]);
+    }
+    emit_all(held);
     blks->push_back(EncBlk{t, -1, 0});  // sentinel: total tickets
 }
 
@@ -823,8 +918,10 @@ extern "C" int a8_encode_trace(const void* workspace, int nseg, uint64_t* out) {
     out[2] = h.tr_wait_ns;
     out[3] = h.tr_waits;
     for (int i = 0; i < nseg; ++i) {
-        out[4 + 2 * i] = c[i].t_b0;
-        out[5 + 2 * i] = c[i].t_b1;
+        out[4 + 4 * i] = c[i].t_b0;
+        out[5 + 4 * i] = c[i].t_thr;
+        out[6 + 4 * i] = c[i].t_fill;
+        out[7 + 4 * i] = c[i].t_b1;
     }
     return A8_OK;
 }
@@ -876,8 +973,11 @@ extern "C" int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_de
         d[i].n = s.n;
         d[i].flat_off = s.flat_off;
         d[i].scale_idx = s.scale_idx;
-        d[i].nA = absmax ? (int32_t)std::max<int64_t>(1, nch) : 0;
-        d[i].nE = absmax ? (int32_t)nch : (int32_t)std::max<int64_t>(1, nch);
+        // absmax: multi-chunk segments take A- and E-chunks; single-chunk
+        // (and empty) segments are one F ticket.  Fixed scale: E-chunks.
+        const bool fused = absmax && s.n <= kChunk;
+        d[i].nA = absmax && !fused ? (int32_t)nch : 0;
+        d[i].nE = fused ? 0 : absmax ? (int32_t)nch : (int32_t)std::max<int64_t>(1, nch);
         d[i].aligned = (reinterpret_cast<uintptr_t>(s.x) % 16) == 0;
     }
     std::vector<EncBlk> blks;
@@ -902,7 +1002,8 @@ extern "C" int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_de
     p.absmax = absmax ? 1 : 0;
     p.total = blks[nblk].tstart;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (nseg <= kInlineSegs) {
+    if ((int)blks.size() > max_blocks(nseg)) return fail(A8_ERR_USAGE, "a8_encode: schedule overflow");
+    if (nseg <= kInlineSegs && (int)blks.size() <= kInlineBlks) {
         std::copy(d.begin(), d.end(), p.segs);
         std::copy(blks.begin(), blks.end(), p.blks);
     } else {

@@ -72,15 +72,17 @@ def run(sizes, spec, iters, dev):
         enc()
         torch.cuda.synchronize()
         ws = workspace(dev, torch.cuda.current_stream(dev).cuda_stream, len(xs))
-        out = (C.c_uint64 * (4 + 2 * len(xs)))()
+        out = (C.c_uint64 * (4 + 4 * len(xs)))()
         N.check(N.lib.a8_encode_trace(ws.data_ptr(), len(xs), out))
         t0 = out[0]
         order = sorted(range(len(xs)), key=lambda i: xs[i].numel())
         res["trace"] = {
             "kernel_us": (out[1] - t0) / 1e3, "wait_cta_us": out[2] / 1e3, "waits": out[3],
-            "builds": [{"n": xs[order[k]].numel(), "start_us": round((out[4 + 2 * k] - t0) / 1e3, 2),
-                        "build_us": round((out[5 + 2 * k] - out[4 + 2 * k]) / 1e3, 2)}
-                       for k in range(len(xs)) if out[4 + 2 * k] >= t0],
+            "builds": [{"n": xs[order[k]].numel(), "start_us": round((out[4 + 4 * k] - t0) / 1e3, 2),
+                        "thr_us": round((out[5 + 4 * k] - out[4 + 4 * k]) / 1e3, 2),
+                        "fill_us": round((out[6 + 4 * k] - out[5 + 4 * k]) / 1e3, 2),
+                        "pub_us": round((out[7 + 4 * k] - out[6 + 4 * k]) / 1e3, 2)}
+                       for k in range(len(xs)) if out[4 + 4 * k] >= t0],
         }
     return n, res
 
