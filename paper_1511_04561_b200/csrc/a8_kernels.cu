@@ -38,9 +38,6 @@ constexpr size_t kEncDynSmem = (size_t)kStages * kChunk * sizeof(float);
 
 // ---- decode geometry ---------------------------------------------------------
 constexpr int kDecThreads = 256;
-constexpr int kGroups = 4;
-constexpr int kDecChunk = kDecThreads * kGroups * 4;
-constexpr int kDecRep = 4;  // replicated decode tables (bank-conflict relief)
 constexpr int kMaxRanks = 16;
 
 constexpr int kInlineSegs = 32;
@@ -610,11 +607,24 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
 
 // ---------------------------------------------------------------------------
 // K4/K5: decode (+ rank-ordered sum, + 1/N average).
+//
+// Per segment, each CTA keeps pre-scaled tables fl(table[c] * s_r) for every
+// rank in shared memory, replicated 4 times.  Each thread decodes 4 groups
+// of 4 elements of a chunk with all code words loaded before any store.
+
+constexpr int kDecGroups = 4;
+constexpr int kDecChunkD = kDecThreads * kDecGroups * 4;  // 4096 elements
+
+// 4 copies: 1-4 copies measured equal; 8 and 32 (lane-private) were slower
+// (the larger shared-memory carveout costs more than the conflicts save).
+__host__ __device__ __forceinline__ int dec_rep_shift(int) { return 2; }
 
 __global__ void __launch_bounds__(kDecThreads) decode_kernel(const __grid_constant__ DecParams p) {
-    extern __shared__ float sTab[];  // [nranks][256][kDecRep]
+    extern __shared__ float sTab[];  // [nranks][256][rep]
     const int tid = threadIdx.x;
-    const int rep = tid & (kDecRep - 1);
+    const int rsh = dec_rep_shift(p.nranks);
+    const int rep = tid & ((1 << rsh) - 1);
+    const int tstride = 256 << rsh;  // floats per rank table
     const DecSegD* segs = p.segs_dev ? p.segs_dev : p.segs;
     const int R = p.nranks;
     const int64_t L = p.lay.block_len;
@@ -659,50 +669,48 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(const __grid_consta
                                                                  (int64_t)r * p.lay.rank_stride) +
                                   j * p.lay.scale_block_stride + sg.scale_idx;
                 const float v = __fmul_rn(p.book->table[code], __ldcg(sc));  // codecs.py:281
-#pragma unroll
-                for (int q = 0; q < kDecRep; ++q) sTab[(i << 2) + q] = v;
+                float* d = sTab + r * tstride + (code << rsh);
+                for (int q = 0; q < (1 << rsh); ++q) d[q] = v;
             }
             __syncthreads();
             cur = lo;
             cbase = sg.cstart;
             src = p.lay.codes + j * gap;
         }
-        const int64_t base = (c - cbase) * kDecChunk;
-        const int64_t cnt = min((int64_t)kDecChunk, sg.n - base);
+        const int64_t base = (c - cbase) * kDecChunkD;
+        const int64_t cnt = min((int64_t)kDecChunkD, sg.n - base);
         const int64_t f0 = sg.flat_off + base;
 
-        if (cnt == kDecChunk && sg.aligned) {
-            // all code words of the chunk are loaded before any store (the
-            // output may alias nothing we read, but the compiler cannot know)
-            float acc[kGroups][4];
+        if (cnt == kDecChunkD && sg.aligned) {
+            float acc[kDecGroups][4];
             {
-                uint32_t w[kGroups];
+                uint32_t w[kDecGroups];
 #pragma unroll
-                for (int q = 0; q < kGroups; ++q) w[q] = ld_stream_u32(src + f0 + q * (kDecThreads * 4) + tid * 4);
+                for (int q = 0; q < kDecGroups; ++q) w[q] = ld_stream_u32(src + f0 + q * (kDecThreads * 4) + tid * 4);
 #pragma unroll
-                for (int q = 0; q < kGroups; ++q) {
-                    acc[q][0] = sTab[((w[q] & 255u) << 2) + rep];
-                    acc[q][1] = sTab[(((w[q] >> 8) & 255u) << 2) + rep];
-                    acc[q][2] = sTab[(((w[q] >> 16) & 255u) << 2) + rep];
-                    acc[q][3] = sTab[((w[q] >> 24) << 2) + rep];
+                for (int q = 0; q < kDecGroups; ++q) {
+                    acc[q][0] = sTab[((w[q] & 255u) << rsh) + rep];
+                    acc[q][1] = sTab[(((w[q] >> 8) & 255u) << rsh) + rep];
+                    acc[q][2] = sTab[(((w[q] >> 16) & 255u) << rsh) + rep];
+                    acc[q][3] = sTab[((w[q] >> 24) << rsh) + rep];
                 }
             }
             for (int r = 1; r < R; ++r) {
                 const uint8_t* sr = src + (int64_t)r * p.lay.rank_stride + f0 + tid * 4;
-                const float* T = sTab + r * 1024;
-                uint32_t w[kGroups];
+                const float* T = sTab + r * tstride;
+                uint32_t w[kDecGroups];
 #pragma unroll
-                for (int q = 0; q < kGroups; ++q) w[q] = ld_stream_u32(sr + q * (kDecThreads * 4));
+                for (int q = 0; q < kDecGroups; ++q) w[q] = ld_stream_u32(sr + q * (kDecThreads * 4));
 #pragma unroll
-                for (int q = 0; q < kGroups; ++q) {
-                    acc[q][0] = __fadd_rn(acc[q][0], T[((w[q] & 255u) << 2) + rep]);
-                    acc[q][1] = __fadd_rn(acc[q][1], T[(((w[q] >> 8) & 255u) << 2) + rep]);
-                    acc[q][2] = __fadd_rn(acc[q][2], T[(((w[q] >> 16) & 255u) << 2) + rep]);
-                    acc[q][3] = __fadd_rn(acc[q][3], T[((w[q] >> 24) << 2) + rep]);
+                for (int q = 0; q < kDecGroups; ++q) {
+                    acc[q][0] = __fadd_rn(acc[q][0], T[((w[q] & 255u) << rsh) + rep]);
+                    acc[q][1] = __fadd_rn(acc[q][1], T[(((w[q] >> 8) & 255u) << rsh) + rep]);
+                    acc[q][2] = __fadd_rn(acc[q][2], T[(((w[q] >> 16) & 255u) << rsh) + rep]);
+                    acc[q][3] = __fadd_rn(acc[q][3], T[((w[q] >> 24) << rsh) + rep]);
                 }
             }
 #pragma unroll
-            for (int q = 0; q < kGroups; ++q) {
+            for (int q = 0; q < kDecGroups; ++q) {
                 const int64_t e = q * (kDecThreads * 4) + tid * 4;
                 float a0 = acc[q][0], a1 = acc[q][1], a2 = acc[q][2], a3 = acc[q][3];
                 if (p.op == 1 && R > 1) {
@@ -723,15 +731,17 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(const __grid_consta
             }
         } else {
             for (int64_t i = tid; i < cnt; i += kDecThreads) {
-                float a = sTab[((uint32_t)src[f0 + i] << 2) + rep];
+                float a = sTab[((uint32_t)src[f0 + i] << rsh) + rep];
                 for (int r = 1; r < R; ++r)
-                    a = __fadd_rn(a, sTab[r * 1024 + ((uint32_t)src[(int64_t)r * p.lay.rank_stride + f0 + i] << 2) + rep]);
+                    a = __fadd_rn(a, sTab[r * tstride + ((uint32_t)src[(int64_t)r * p.lay.rank_stride + f0 + i] << rsh) + rep]);
                 if (p.op == 1 && R > 1) a = pow2 ? __fmul_rn(a, invN) : __fdiv_rn(a, (float)R);
                 sg.out[base + i] = a;
             }
         }
     }
 }
+
+static size_t dec_smem(int nranks) { return (size_t)nranks * (256u << dec_rep_shift(nranks)) * sizeof(float); }
 
 // ---------------------------------------------------------------------------
 // host launchers
@@ -755,11 +765,11 @@ static int dev_info(int device, DevInfo* out) {
         e = cudaFuncSetAttribute(encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEncDynSmem);
         if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
         e = cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kMaxRanks * 256 * kDecRep * (int)sizeof(float));
+                                 (int)dec_smem(kMaxRanks));
         if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.enc_occ, encode_kernel, kEncThreads, kEncDynSmem);
         if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
-        const size_t dsm = (size_t)8 * 256 * kDecRep * sizeof(float);
+        const size_t dsm = dec_smem(1);
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.dec_occ, decode_kernel, kDecThreads, dsm);
         if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
         d.enc_occ = std::max(1, d.enc_occ);
@@ -958,6 +968,7 @@ extern "C" int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_de
     if (int rc = dev_info(device, &di)) return rc;
 
     const bool absmax = norm == A8_NORM_ABSMAX;
+
     std::vector<int> order(nseg);
     for (int i = 0; i < nseg; ++i) order[i] = i;
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return segs[a].n < segs[b].n; });
@@ -1048,7 +1059,7 @@ extern "C" int a8_decode(const a8_dec_seg_t* segs, int nseg, const void* book_de
         d[i].scale_idx = s.scale_idx;
         d[i].aligned = (reinterpret_cast<uintptr_t>(s.out) % 16) == 0;
         d[i].cstart = chunks;
-        chunks += (s.n + kDecChunk - 1) / kDecChunk;
+        chunks += (s.n + kDecChunkD - 1) / kDecChunkD;
     }
     if (chunks == 0 && !status_out) return A8_OK;
     DecParams p;
@@ -1072,7 +1083,7 @@ extern "C" int a8_decode(const a8_dec_seg_t* segs, int nseg, const void* book_de
         cudaMemcpyAsync(plan, d.data(), sizeof(DecSegD) * nseg, cudaMemcpyHostToDevice, st);
         p.segs_dev = reinterpret_cast<const DecSegD*>(plan);
     }
-    const size_t smem = (size_t)nranks * 256 * kDecRep * sizeof(float);
+    const size_t smem = dec_smem(nranks);
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)di.sms * di.dec_occ, chunks));
     decode_kernel<<<(unsigned)grid, kDecThreads, smem, st>>>(p);
     return cuda_check("a8_decode");
