@@ -101,6 +101,8 @@ def main():
     spec = A.parse_spec(a.spec)
     if a.case == "alexnet":
         cases = [("alexnet", ALEXNET)]
+    elif a.case == "mlpcodec":
+        cases = [("mlp", [(784, 1200), (1200,), (1200, 1200), (1200,), (1200, 10), (10,)])]
     elif a.case == "single":
         cases = [("single_2^26", [(1 << 26,)])]
     elif a.case == "bw":
@@ -121,6 +123,34 @@ def main():
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / a.iters
             print(json.dumps({"case": name, "ms": ms, "GBps": nbytes / (ms * 1e-3) / 1e9}), flush=True)
+        return
+    elif a.case == "mlp":
+        # BASELINE config 2 gradients (784-1200-1200-10): exchange step latency
+        import time
+
+        sizes = [(784, 1200), (1200,), (1200, 1200), (1200,), (1200, 10), (10,)]
+        gs = [torch.randn(s, device=dev) * 1e-3 for s in sizes]
+        outs = [torch.empty_like(g) for g in gs]
+        for graph in (False, True):
+            kw = {"graph": True} if graph else {}
+            try:
+                ex = A.GradientExchange(spec, check="deferred", **kw)
+            except TypeError:
+                continue
+            for _ in range(5):
+                ex(gs, out=outs)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
+            e0.record()
+            for _ in range(a.iters):
+                ex(gs, out=outs)
+            e1.record()
+            torch.cuda.synchronize()
+            wall = (time.perf_counter() - t0) / a.iters * 1e6
+            print(json.dumps({"case": "mlp_exchange", "graph": graph, "n": sum(g.numel() for g in gs),
+                              "gpu_us_per_step": e0.elapsed_time(e1) / a.iters * 1e3,
+                              "wall_us_per_step": wall}), flush=True)
         return
     elif a.case == "sweep":
         cases = [(f"2^{k}", [(1 << k,)]) for k in range(10, 31, 2)]
