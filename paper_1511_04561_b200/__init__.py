@@ -22,8 +22,22 @@ from .codecs import (
     roundtrip,
 )
 from .errors import ApproxError, ConfigError, InputError, TrainingError, UsageError
-from .exchange import DDPHookState, GradientExchange, a8_comm_hook, exchange
-from .hooks import HookMode, HookStats, QuantHookConfig, default_hook_spec, make_quantizer
+from .exchange import (
+    CompressedAllGather,
+    DDPHookState,
+    GradientExchange,
+    LocalExchange,
+    a8_comm_hook,
+    exchange,
+)
+from .hooks import (
+    HookMode,
+    HookStats,
+    ModelParallelFC,
+    QuantHookConfig,
+    default_hook_spec,
+    make_quantizer,
+)
 
 __all__ = [
     "CODE_COUNT",
@@ -31,6 +45,7 @@ __all__ = [
     "SIGN_MASK",
     "ApproxError",
     "Codebook",
+    "CompressedAllGather",
     "ConfigError",
     "DDPHookState",
     "DataTypeKind",
@@ -39,6 +54,8 @@ __all__ = [
     "HookMode",
     "HookStats",
     "InputError",
+    "LocalExchange",
+    "ModelParallelFC",
     "NormKind",
     "QuantHookConfig",
     "QuantizedTensor",

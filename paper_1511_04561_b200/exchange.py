@@ -365,6 +365,99 @@ def exchange(tensors, spec: DataTypeSpec, group=None, mode: str = "allgather", o
     return GradientExchange(spec, group, mode, op, check="sync")(tensors)
 
 
+class CompressedAllGather:
+    """8-bit all-gather (concatenation, no reduction) of one float32 tensor
+    per rank: the model-parallel activation seam (mlp.py:208-215, "the
+    activation shipped to the next device").  Each rank encodes its shard
+    with its own absmax scale into its slab, the slabs are all-gathered, and
+    one decode launch writes every rank's decoded shard into ``out[r]``."""
+
+    def __init__(self, spec: DataTypeSpec, group=None, codec: Optional[SegmentCodec] = None, comm=None):
+        self.spec = spec
+        self.cb = build_codebook(spec)
+        self.codec = codec or CudaSegmentCodec()
+        self.comm = comm or TorchDistComm(group)
+        self._bufs: dict = {}
+
+    def __call__(self, shard: torch.Tensor, out: Optional[Sequence[torch.Tensor]] = None):
+        if shard.dtype != torch.float32 or not shard.is_contiguous():
+            raise UsageError("all-gather needs a contiguous float32 tensor")
+        nranks, rank = self.comm.world()
+        dev = shard.device
+        n = shard.numel()
+        plan = make_plan((n,), 1)
+        B = plan.allgather_block()
+        key = (n, nranks, dev)
+        if key not in self._bufs:
+            self._bufs[key] = (torch.zeros(nranks * B, dtype=torch.uint8, device=dev),
+                               torch.zeros(1, dtype=torch.int32, device=dev))
+        slab, status = self._bufs[key]
+        self.codec.encode([shard], [0], [0], self.cb, slab, rank * B, rank * B + plan.flat, plan.flat,
+                          plan.flat, 0, 1, rank * B + plan.flat + 4 * plan.status_slot)
+        if nranks > 1:
+            self.comm.all_gather(slab, slab[rank * B:(rank + 1) * B])
+        outs = list(out) if out is not None else [torch.empty_like(shard) for _ in range(nranks)]
+        # rank j's shard is segment j of a layout whose blocks are the slabs
+        flat_offs = [j * plan.flat for j in range(nranks)]
+        self.codec.decode(outs, flat_offs, [0] * nranks, self.cb, slab, 0, plan.flat, plan.flat, B, B // 4,
+                          0, 1, 0, plan.status_slot, nranks, status)
+        if int(status.cpu()[0]) & N.A8_STATUS_NONFINITE:
+            raise InputError("cannot encode non-finite values (NaN or Inf present)")
+        return outs
+
+
+class LocalExchange:
+    """The allgather exchange among N replicas that live in ONE process on
+    one device (e.g. several model replicas per GPU): every replica's tensors
+    are encoded into its slab of one buffer -- the slabs are then already
+    "gathered" -- and one decode-sum(-average) launch writes the result for
+    all replicas.  Same kernels, slab layout and numerics as
+    ``GradientExchange(mode="allgather")`` with N ranks."""
+
+    def __init__(self, spec: DataTypeSpec, op: str = "avg", codec: Optional[SegmentCodec] = None):
+        if op not in OPS:
+            raise UsageError(f"op must be one of {OPS}, got {op!r}")
+        self.spec = spec
+        self.cb = build_codebook(spec)
+        self.op = op
+        self.codec = codec or CudaSegmentCodec()
+        self._bufs: dict = {}
+
+    def __call__(self, per_replica: Sequence[Sequence[torch.Tensor]], out: Optional[Sequence[torch.Tensor]] = None):
+        """per_replica[r] = replica r's tensors (same shapes for every r).
+        Returns (or fills ``out`` with) one averaged/summed list."""
+        nranks = len(per_replica)
+        if nranks < 1:
+            raise UsageError("need at least one replica")
+        first = list(per_replica[0])
+        sizes = tuple(t.numel() for t in first)
+        for rep in per_replica:
+            if tuple(t.numel() for t in rep) != sizes:
+                raise UsageError("every replica must hold tensors of the same sizes")
+            for t in rep:
+                if t.dtype != torch.float32 or not t.is_contiguous() or t.device != first[0].device:
+                    raise UsageError("exchange needs contiguous float32 tensors on one device")
+        dev = first[0].device
+        plan = make_plan(sizes, 1)
+        B = plan.allgather_block()
+        key = (sizes, nranks, dev)
+        buf = self._bufs.get(key)
+        if buf is None:
+            buf = self._bufs[key] = (torch.zeros(nranks * B, dtype=torch.uint8, device=dev),
+                                     torch.zeros(1, dtype=torch.int32, device=dev))
+        slab, status = buf
+        idx = list(range(plan.nseg))
+        for r, rep in enumerate(per_replica):
+            self.codec.encode(list(rep), plan.offs, idx, self.cb, slab, r * B, r * B + plan.flat,
+                              plan.flat, plan.flat, 0, 1, r * B + plan.flat + 4 * plan.status_slot)
+        outs = list(out) if out is not None else [torch.empty_like(t) for t in first]
+        self.codec.decode(outs, plan.offs, idx, self.cb, slab, 0, plan.flat, plan.flat, plan.flat, 0, B,
+                          nranks, 1 if self.op == "avg" else 0, plan.status_slot, 1, status)
+        if int(status.cpu()[0]) & N.A8_STATUS_NONFINITE:
+            raise InputError("cannot encode non-finite values (NaN or Inf present)")
+        return outs
+
+
 # ---------------------------------------------------------------------------
 # DDP communication hook
 

@@ -115,3 +115,43 @@ def make_quantizer(spec: DataTypeSpec, stats: Optional[HookStats] = None, site: 
         return y
 
     return quantize
+
+
+class ModelParallelFC:
+    """Column-sharded fully connected layer with 8-bit activations on the
+    wire (BASELINE config 5; the model-parallel seam of mlp.py:208-215 and
+    247-249, where the reference round-trips the tensors that cross devices).
+
+    Rank r of N owns ``weight_shard`` = W[:, r*k:(r+1)*k] (in x out_shard).
+      forward(x)   y_r = x @ W_r; the shards are 8-bit all-gathered (one
+                   absmax scale per shard) and concatenated: y = [q(y_0) .. q(y_N-1)]
+      backward(dy) dx_r = dy[:, shard r] @ W_r^T is a partial of dx; the
+                   partials are summed through the compressed exchange
+                   (op="sum"): dx = sum_r q(dx_r), rank order, float32;
+                   dW_r = x^T dy_r stays local.
+    ``comm`` is the collective backend (torch.distributed by default).
+    """
+
+    def __init__(self, weight_shard: torch.Tensor, spec: DataTypeSpec, group=None, comm=None, codec=None):
+        from .exchange import CompressedAllGather, GradientExchange
+
+        self.w = weight_shard
+        self.spec = spec
+        self.gather = CompressedAllGather(spec, group, codec=codec, comm=comm)
+        self.reduce = GradientExchange(spec, group, mode="allgather", op="sum", check="sync", codec=codec, comm=comm)
+        self._x = None
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        self._x = x
+        y_r = (x @ self.w).contiguous()
+        parts = self.gather(y_r)
+        return torch.cat(parts, dim=1)
+
+    def backward(self, dy: torch.Tensor):
+        n_r = self.w.shape[1]
+        nranks, rank = self.gather.comm.world()
+        dy_r = dy[:, rank * n_r:(rank + 1) * n_r]
+        dw = self._x.t() @ dy_r
+        dx = (dy_r @ self.w.t()).contiguous()
+        self.reduce([dx])
+        return dx, dw

@@ -142,3 +142,27 @@ def test_gloo_world_size_2(mode, op):
         p.join(timeout=300)
     results = dict(q.get(timeout=5) for _ in range(2))
     assert results == {0: True, 1: True}
+
+
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_model_parallel_fc_orchestration(nranks):
+    """ModelParallelFC's gather / compressed-sum plumbing on CPU (test codec)."""
+    spec = A.DataTypeSpec("dynamic-tree", "absmax")
+    rng = np.random.default_rng(7)
+    x = torch.from_numpy(rng.normal(0, 0.02, size=(16, 64)).astype(np.float32))
+    w = torch.from_numpy(rng.normal(0, 0.02, size=(64, 32)).astype(np.float32))
+    dy = torch.from_numpy(rng.normal(0, 1e-3, size=(16, 32)).astype(np.float32))
+    k = 32 // nranks
+
+    def body(rank, comm):
+        fc = A.ModelParallelFC(w[:, rank * k:(rank + 1) * k].contiguous(), spec, comm=comm, codec=NumpyCodec(spec))
+        y = fc.forward(x)
+        dx, _ = fc.backward(dy)
+        return y.numpy(), dx.numpy(), (x @ fc.w).numpy(), (dy[:, rank * k:(rank + 1) * k] @ fc.w.t()).numpy()
+
+    res = run_virtual_ranks(nranks, body)
+    y_want = np.concatenate([O.roundtrip(res[r][2], "dynamic-tree", "absmax") for r in range(nranks)], axis=1)
+    dx_want = O.exchange_allgather([[res[r][3]] for r in range(nranks)], "dynamic-tree", "absmax", op="sum")[0]
+    for r in range(nranks):
+        assert np.array_equal(res[r][0], y_want)
+        assert np.array_equal(res[r][1], dx_want)
