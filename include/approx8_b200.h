@@ -166,6 +166,22 @@ int a8_decode(const a8_dec_seg_t* segs, int nseg, const void* book_dev, a8_layou
               int nranks, int op, int status_idx, int status_blocks, uint32_t* status_out,
               void* workspace, size_t workspace_bytes, void* stream);
 
+/* 1-bit error-feedback quantizer: onebit_quantize (codecs.py:306-339).
+ *   g          n gradients, float32 (g_is_f64 = 0) or float64 (1)
+ *   residual   n float64, updated in place: corrected - reconstruction
+ *   bits       ceil(n/8) bytes, np.packbits order (first element in the MSB)
+ *   levels     device float[2] = {pos_level, neg_level}: float32 means of the
+ *              corrected values on each side of 0 (0 for an empty side)
+ *   status_out device uint32, overwritten (A8_STATUS_NONFINITE)
+ *   workspace  a8_onebit_workspace_bytes() bytes of device scratch          */
+size_t a8_onebit_workspace_bytes(void);
+int a8_onebit_quantize(const void* g, int g_is_f64, double* residual, int64_t n, uint8_t* bits,
+                       float* levels, uint32_t* status_out, void* workspace, size_t workspace_bytes,
+                       void* stream);
+
+/* onebit_decode (codecs.py:342-348): out[i] = bit ? levels[0] : levels[1]. */
+int a8_onebit_decode(const uint8_t* bits, int64_t n, const float* levels, float* out, void* stream);
+
 /* Diagnostics: globaltimer trace of the last a8_encode on `workspace`
  * (synchronous device->host copy).  out[0..3] = kernel start ns, end ns,
  * total CTA time spent waiting for segment tables (ns), number of waits;

@@ -14,10 +14,13 @@ from .codecs import (
     DataTypeKind,
     DataTypeSpec,
     NormKind,
+    OneBitState,
     QuantizedTensor,
     build_codebook,
     decode_buffer,
     encode_buffer,
+    onebit_decode,
+    onebit_quantize,
     parse_spec,
     roundtrip,
 )
@@ -30,6 +33,7 @@ from .exchange import (
     a8_comm_hook,
     exchange,
 )
+from .tensorfile import read_tensor, write_tensor
 from .hooks import (
     HookMode,
     HookStats,
@@ -57,6 +61,7 @@ __all__ = [
     "LocalExchange",
     "ModelParallelFC",
     "NormKind",
+    "OneBitState",
     "QuantHookConfig",
     "QuantizedTensor",
     "TrainingError",
@@ -68,6 +73,10 @@ __all__ = [
     "encode_buffer",
     "exchange",
     "make_quantizer",
+    "onebit_decode",
+    "onebit_quantize",
     "parse_spec",
+    "read_tensor",
     "roundtrip",
+    "write_tensor",
 ]

@@ -98,6 +98,13 @@ SIGNATURES = {
          C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p],
     ),
     "a8_encode_trace": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_uint64)]),
+    "a8_onebit_workspace_bytes": (C.c_size_t, []),
+    "a8_onebit_quantize": (
+        C.c_int,
+        [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+         C.c_size_t, C.c_void_p],
+    ),
+    "a8_onebit_decode": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
     "a8_device_info": (
         C.c_int,
         [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)],

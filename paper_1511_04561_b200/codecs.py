@@ -212,12 +212,36 @@ class QuantizedTensor:
         self.shape = tuple(int(d) for d in shape)
         self.spec = spec
         self.nbits = nbits
-        self.pos_level = pos_level
-        self.neg_level = neg_level
+        self._levels = (pos_level, neg_level)
+        self.levels_tensor: Optional[torch.Tensor] = None  # device float[2] (1-bit tensors)
         self._scale = None if scale is None else float(np.float32(scale))
         self.scale_tensor = scale_tensor
         self._meta = meta  # int32[2] = [status, scale bits] written by the encoder
         self._checked = meta is None
+
+    def _host_levels(self):
+        if self.levels_tensor is not None and self._levels is None:
+            lv = self.levels_tensor.cpu()
+            self._levels = (float(lv[0]), float(lv[1]))
+        return self._levels
+
+    @property
+    def pos_level(self) -> float:
+        return self._host_levels()[0]
+
+    @pos_level.setter
+    def pos_level(self, v: float) -> None:
+        self._levels = (float(v), self._host_levels()[1])
+        self.levels_tensor = None
+
+    @property
+    def neg_level(self) -> float:
+        return self._host_levels()[1]
+
+    @neg_level.setter
+    def neg_level(self, v: float) -> None:
+        self._levels = (self._host_levels()[0], float(v))
+        self.levels_tensor = None
 
     @property
     def count(self) -> int:
@@ -411,3 +435,88 @@ def roundtrip(x, spec: DataTypeSpec, *, device=None):
     if isinstance(x, torch.Tensor):
         return y
     return y.cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# 1-bit quantizer with error feedback (codecs.py:291-348)
+
+
+class OneBitState:
+    """Residual carried between successive 1-bit quantizations of one tensor
+    (codecs.py:295-303); a float64 tensor on the device."""
+
+    def __init__(self, residual) -> None:
+        self.residual = residual
+
+    @classmethod
+    def zeros(cls, shape, device=None) -> "OneBitState":
+        dev = _cuda_device(device)
+        return cls(torch.zeros(tuple(shape) if not isinstance(shape, int) else (shape,), dtype=torch.float64,
+                               device=dev))
+
+
+_ob_ws: dict = {}
+
+
+def onebit_quantize(g, state: OneBitState, *, sync: bool = True) -> QuantizedTensor:
+    """Quantize ``g + residual`` to one bit per element and update ``state``
+    (codecs.py:306-339): each side of 0 is reconstructed as its own float32
+    mean and the residual keeps exactly what the receiver cannot see."""
+    res = state.residual
+    if not isinstance(res, torch.Tensor) or not res.is_cuda or res.dtype != torch.float64:
+        state.residual = res = torch.as_tensor(np.asarray(res, dtype=np.float64)).to(_cuda_device(None))
+    if isinstance(g, torch.Tensor):
+        shape = tuple(g.shape)
+        t = g.to(res.device)
+    else:
+        arr = np.asarray(g)
+        shape = tuple(arr.shape)
+        t = torch.from_numpy(np.ascontiguousarray(arr)).to(res.device)
+    if shape != tuple(res.shape):
+        raise UsageError(f"gradient shape {shape} does not match residual shape {tuple(res.shape)}")
+    if t.dtype not in (torch.float32, torch.float64):
+        t = t.to(torch.float64)
+    t = t.contiguous()
+    res_c = res if res.is_contiguous() else res.contiguous()
+    n = t.numel()
+    dev = res.device
+    bits = torch.empty((n + 7) // 8, dtype=torch.uint8, device=dev)
+    lv = torch.zeros(2, dtype=torch.float32, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    if n:
+        with torch.cuda.device(dev):
+            key = dev.index
+            ws = _ob_ws.get(key)
+            if ws is None:
+                ws = _ob_ws[key] = torch.empty(N.lib.a8_onebit_workspace_bytes(), dtype=torch.uint8, device=dev)
+            N.check(N.lib.a8_onebit_quantize(t.data_ptr(), 1 if t.dtype == torch.float64 else 0, res_c.data_ptr(),
+                                             n, bits.data_ptr(), lv.data_ptr(), status.data_ptr(), ws.data_ptr(),
+                                             ws.numel(), _stream(dev)))
+        if res_c is not res:
+            res.copy_(res_c)
+    q = QuantizedTensor(bits, shape, None, 1.0, nbits=1)
+    q._levels = None
+    q.levels_tensor = lv
+    q._keepalive = (t, ws if n else None)
+    if sync and n and int(status.cpu()[0]) & N.A8_STATUS_NONFINITE:
+        raise InputError("cannot encode non-finite values (NaN or Inf present)")
+    return q
+
+
+def onebit_decode(q: QuantizedTensor, *, device=None) -> torch.Tensor:
+    """Reconstruct the two-level float32 tensor (codecs.py:342-348)."""
+    if q.nbits != 1:
+        raise UsageError("onebit_decode expects a 1-bit tensor")
+    codes = q.codes
+    dev = codes.device if isinstance(codes, torch.Tensor) and codes.is_cuda else _cuda_device(device)
+    if not isinstance(codes, torch.Tensor):
+        codes = torch.from_numpy(np.ascontiguousarray(np.asarray(codes, dtype=np.uint8))).to(dev)
+    codes = codes.to(dev).contiguous()
+    n = q.count
+    lv = q.levels_tensor if q.levels_tensor is not None else torch.tensor(
+        [np.float32(q.pos_level), np.float32(q.neg_level)], dtype=torch.float32, device=dev)
+    out = torch.empty(q.shape, dtype=torch.float32, device=dev)
+    if n:
+        with torch.cuda.device(dev):
+            N.check(N.lib.a8_onebit_decode(codes.data_ptr(), n, lv.data_ptr(), out.data_ptr(), _stream(dev)))
+    return out

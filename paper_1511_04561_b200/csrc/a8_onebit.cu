@@ -1,0 +1,192 @@
+// 1-bit error-feedback quantizer (approx8/codecs.py:291-348) on sm_100a.
+//
+//   corrected = float64(g) + residual
+//   positive  = corrected >= 0
+//   pos_level = float32(mean(corrected[positive]))   (0 if none), same for neg
+//   residual  = corrected - (positive ? pos_level : neg_level)     (float64)
+//   bits      = packbits(positive), first element in the MSB (np.packbits)
+//
+// Two launches: stats (per-CTA float64 sums and counts per sign, non-finite
+// flag) and apply (every CTA reduces the partials in the same fixed order,
+// so all CTAs see identical levels; then the residual update and the bit
+// packing, 8 elements -> 1 byte per thread).  The float64 sums are exact
+// to float64 rounding; the summation order differs from NumPy's pairwise
+// sum, which can only change a level when the float64 mean lies within a
+// float64 ulp of a float32 rounding boundary.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+
+#include "approx8_b200.h"
+
+namespace a8 {
+int fail(int code, const char* msg);
+extern thread_local std::string g_last_error;
+}  // namespace a8
+
+using a8::fail;
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kMaxGrid = 480;
+
+struct Partial {
+    double sum_pos, sum_neg;
+    unsigned long long cnt_pos, cnt_neg;
+    unsigned int bad;
+    unsigned int pad[3];
+};
+
+__device__ __forceinline__ double load_g(const void* g, int f64, int64_t i) {
+    return f64 ? reinterpret_cast<const double*>(g)[i] : (double)reinterpret_cast<const float*>(g)[i];
+}
+
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* red) {
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[w] = v;
+    __syncthreads();
+    T s = 0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < kThreads / 32; ++i) s += red[i];  // fixed order
+    return s;  // valid in thread 0
+}
+
+__global__ void __launch_bounds__(kThreads) onebit_stats(const void* g, int f64, const double* res, int64_t n,
+                                                          Partial* part) {
+    __shared__ double rd[kThreads / 32];
+    __shared__ unsigned long long ru[kThreads / 32];
+    double sp = 0.0, sn = 0.0;
+    unsigned long long cp = 0, cn = 0;
+    unsigned int bad = 0;
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads) {
+        const double gi = load_g(g, f64, i);
+        if (!isfinite(gi)) bad = 1;
+        const double c = __dadd_rn(gi, res[i]);
+        if (c >= 0.0) {
+            sp = __dadd_rn(sp, c);
+            ++cp;
+        } else {
+            sn = __dadd_rn(sn, c);
+            ++cn;
+        }
+    }
+    const double SP = block_sum(sp, rd);
+    const double SN = block_sum(sn, rd);
+    const unsigned long long CP = block_sum(cp, ru);
+    const unsigned long long CN = block_sum(cn, ru);
+    const int B = __syncthreads_or(bad);
+    if (threadIdx.x == 0) part[blockIdx.x] = Partial{SP, SN, CP, CN, (unsigned)B, {0, 0, 0}};
+}
+
+__global__ void __launch_bounds__(kThreads) onebit_apply(const void* g, int f64, double* res, int64_t n,
+                                                          const Partial* part, int nparts, uint8_t* bits,
+                                                          float* levels, uint32_t* status) {
+    __shared__ double rd[kThreads / 32];
+    __shared__ unsigned long long ru[kThreads / 32];
+    __shared__ float sLv[2];
+    double sp = 0.0, sn = 0.0;
+    unsigned long long cp = 0, cn = 0;
+    unsigned int bad = 0;
+    for (int i = threadIdx.x; i < nparts; i += kThreads) {
+        sp += part[i].sum_pos;
+        sn += part[i].sum_neg;
+        cp += part[i].cnt_pos;
+        cn += part[i].cnt_neg;
+        bad |= part[i].bad;
+    }
+    const double SP = block_sum(sp, rd);
+    const double SN = block_sum(sn, rd);
+    const unsigned long long CP = block_sum(cp, ru);
+    const unsigned long long CN = block_sum(cn, ru);
+    const int B = __syncthreads_or(bad);
+    if (threadIdx.x == 0) {
+        // codecs.py:327-328: float32 of the float64 mean, 0.0 for an empty side
+        sLv[0] = CP ? __double2float_rn(__ddiv_rn(SP, (double)CP)) : 0.0f;
+        sLv[1] = CN ? __double2float_rn(__ddiv_rn(SN, (double)CN)) : 0.0f;
+        if (blockIdx.x == 0) {
+            levels[0] = sLv[0];
+            levels[1] = sLv[1];
+            *status = B ? A8_STATUS_NONFINITE : 0u;
+        }
+    }
+    __syncthreads();
+    const double pl = (double)sLv[0], nl = (double)sLv[1];
+    const int64_t nbytes = (n + 7) / 8;
+    for (int64_t b = (int64_t)blockIdx.x * kThreads + threadIdx.x; b < nbytes; b += (int64_t)gridDim.x * kThreads) {
+        uint32_t byte = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int64_t i = b * 8 + k;
+            if (i < n) {
+                const double c = __dadd_rn(load_g(g, f64, i), res[i]);
+                const bool pos = c >= 0.0;
+                res[i] = __dsub_rn(c, pos ? pl : nl);
+                byte |= (uint32_t)pos << (7 - k);  // np.packbits: first element in the MSB
+            }
+        }
+        bits[b] = (uint8_t)byte;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) onebit_decode_k(const uint8_t* bits, int64_t n, const float* levels,
+                                                             float* out) {
+    const float pl = levels[0], nl = levels[1];
+    const int64_t nbytes = (n + 7) / 8;
+    for (int64_t b = (int64_t)blockIdx.x * kThreads + threadIdx.x; b < nbytes; b += (int64_t)gridDim.x * kThreads) {
+        const uint32_t byte = bits[b];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int64_t i = b * 8 + k;
+            if (i < n) out[i] = (byte >> (7 - k)) & 1u ? pl : nl;
+        }
+    }
+}
+
+int grid_for(int64_t n) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t want = (n + kThreads * 8 - 1) / (kThreads * 8);
+    return (int)std::max<int64_t>(1, std::min<int64_t>(want, std::min(kMaxGrid, sms * 3)));
+}
+
+int check(const char* what) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        a8::g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+        return A8_ERR_CUDA;
+    }
+    return A8_OK;
+}
+
+}  // namespace
+
+extern "C" size_t a8_onebit_workspace_bytes(void) { return sizeof(Partial) * kMaxGrid; }
+
+extern "C" int a8_onebit_quantize(const void* g, int g_is_f64, double* residual, int64_t n, uint8_t* bits,
+                                  float* levels, uint32_t* status_out, void* workspace, size_t workspace_bytes,
+                                  void* stream) {
+    if (n < 0 || (n > 0 && (!g || !residual || !bits)) || !levels || !status_out || !workspace)
+        return fail(A8_ERR_USAGE, "a8_onebit_quantize: bad argument");
+    if (workspace_bytes < sizeof(Partial) * kMaxGrid)
+        return fail(A8_ERR_USAGE, "a8_onebit_quantize: workspace too small");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Partial* part = static_cast<Partial*>(workspace);
+    const int grid = grid_for(n);
+    onebit_stats<<<grid, kThreads, 0, st>>>(g, g_is_f64, residual, n, part);
+    if (int rc = check("a8_onebit_quantize(stats)")) return rc;
+    onebit_apply<<<grid, kThreads, 0, st>>>(g, g_is_f64, residual, n, part, grid, bits, levels, status_out);
+    return check("a8_onebit_quantize(apply)");
+}
+
+extern "C" int a8_onebit_decode(const uint8_t* bits, int64_t n, const float* levels, float* out, void* stream) {
+    if (n < 0 || (n > 0 && (!bits || !out)) || !levels) return fail(A8_ERR_USAGE, "a8_onebit_decode: bad argument");
+    if (n == 0) return A8_OK;
+    onebit_decode_k<<<grid_for(n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(bits, n, levels, out);
+    return check("a8_onebit_decode");
+}

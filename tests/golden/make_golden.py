@@ -200,6 +200,44 @@ def main() -> None:
         arrays[key + "/sizes"] = np.array(sizes, np.int32)
         arrays[key + "/scales"] = np.array(scs, np.float64)
 
+    # A8T1 files written by the reference (tensorfile.py:56-88): byte images
+    import tempfile
+
+    from approx8 import tensorfile as TF
+
+    meta["a8t1"] = {}
+    with tempfile.TemporaryDirectory() as td:
+        def ref_file(obj, name):
+            fp = Path(td) / name
+            TF.write_tensor(fp, obj)
+            return fp.read_bytes()
+
+        x1 = EB.sample(EB.SampleSpec("normal", 2**20, seed=0, sigma=1.0))
+        cb = C.build_codebook(dspec("dynamic-tree", "absmax", 0))
+        meta["a8t1"]["c1_dynamic_absmax_sha"] = sha(np.frombuffer(ref_file(C.encode_buffer(x1, cb), "c1.a8t"), np.uint8))
+        r = np.random.default_rng(31)
+        small = (r.normal(size=(3, 4, 5)) * 0.1).astype(np.float32)
+        arrays["a8t1/small_x"] = small
+        for spec in [("dynamic-tree", "absmax", 0), ("mantissa", "decade", -2), ("linear", "none", 0)]:
+            q = C.encode_buffer(small, C.build_codebook(dspec(*spec)))
+            arrays[f"a8t1/codes/{tag(*spec)}"] = np.frombuffer(ref_file(q, "q.a8t"), np.uint8)
+        arrays["a8t1/float32"] = np.frombuffer(ref_file(small, "f.a8t"), np.uint8)
+        st = C.OneBitState.zeros(small.shape)
+        qb = C.onebit_quantize(small.astype(np.float64), st)
+        arrays["a8t1/onebit"] = np.frombuffer(ref_file(qb, "b.a8t"), np.uint8)
+
+    # 1-bit error-feedback quantizer (codecs.py:291-348): 12 chained steps
+    r = np.random.default_rng(41)
+    st = C.OneBitState.zeros((3000,))
+    for k in range(12):
+        g = (r.normal(size=3000) * 10.0 ** r.uniform(-3, 0)).astype(np.float32)
+        q = C.onebit_quantize(g, st)
+        arrays[f"onebit/{k}/g"] = g
+        arrays[f"onebit/{k}/bits"] = q.codes.copy()
+        arrays[f"onebit/{k}/levels"] = np.array([q.pos_level, q.neg_level], np.float64)
+        arrays[f"onebit/{k}/residual"] = st.residual.copy()
+        arrays[f"onebit/{k}/decoded"] = C.onebit_decode(q)
+
     # error suite at the paper's protocol size used by test_acceptance.py:132-149
     reps = EB.run_error_suite(seed=0, count=1_000_000)
     meta["suite"] = [
