@@ -97,6 +97,15 @@ typedef struct a8_enc_seg {
     int32_t pad;
 } a8_enc_seg_t;
 
+/* Encode segment with float64 input (a8_encode_f64). */
+typedef struct a8_enc_seg64 {
+    const double* x;
+    int64_t n;
+    int64_t flat_off;  /* multiple of 16 */
+    int32_t scale_idx;
+    int32_t pad;
+} a8_enc_seg64_t;
+
 /* Decode segment: a float32 output tensor (contiguous). */
 typedef struct a8_dec_seg {
     float* out;
@@ -153,6 +162,15 @@ int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_dev, int norm
               const void* static_lut_dev, a8_layout_t layout, void* workspace,
               size_t workspace_bytes, const uint32_t* status_in, uint32_t* status_out,
               void* stream);
+
+/* encode_buffer for float64 input, bit-exact with the reference's float64
+ * arithmetic (codecs.py:254-268): absmax over the float64 values rounded to
+ * float32, y = |x|/s in float64, searchsorted + clip + tie rule per element.
+ * 1..32 segments; `fixed_scale` is used for none/decade (see a8_fixed_scale).
+ * Same layout / workspace / status conventions as a8_encode.               */
+int a8_encode_f64(const a8_enc_seg64_t* segs, int nseg, const void* book_dev, int norm, float fixed_scale,
+                  a8_layout_t layout, void* workspace, size_t workspace_bytes, const uint32_t* status_in,
+                  uint32_t* status_out, void* stream);
 
 /* decode_buffer (codecs.py:272-282) fused with the cross-rank reduction:
  *   out = sum_{r<nranks} table[c_r] * s_r, accumulated in rank order in

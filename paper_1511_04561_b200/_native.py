@@ -56,6 +56,16 @@ class EncSeg(C.Structure):
     ]
 
 
+class EncSeg64(C.Structure):
+    _fields_ = [
+        ("x", C.c_void_p),
+        ("n", C.c_int64),
+        ("flat_off", C.c_int64),
+        ("scale_idx", C.c_int32),
+        ("pad", C.c_int32),
+    ]
+
+
 class DecSeg(C.Structure):
     _fields_ = [
         ("out", C.c_void_p),
@@ -91,6 +101,11 @@ SIGNATURES = {
         C.c_int,
         [C.POINTER(EncSeg), C.c_int, C.c_void_p, C.c_int, C.c_void_p, Layout, C.c_void_p,
          C.c_size_t, C.c_void_p, C.c_void_p, C.c_void_p],
+    ),
+    "a8_encode_f64": (
+        C.c_int,
+        [C.POINTER(EncSeg64), C.c_int, C.c_void_p, C.c_int, C.c_float, Layout, C.c_void_p, C.c_size_t,
+         C.c_void_p, C.c_void_p, C.c_void_p],
     ),
     "a8_decode": (
         C.c_int,

@@ -13,9 +13,9 @@ Differences a caller can see:
     device, so nothing syncs until it is read).
   * ``decode_buffer``/``roundtrip`` return a CUDA ``torch.float32`` tensor,
     or a NumPy array when the input to ``roundtrip`` was a NumPy array.
-  * Inputs are float32.  Other dtypes are converted to float32 first; the
-    reference computes float64 inputs in float64 (codecs.py:254), so for
-    float64 data that float32 cannot represent exactly the codes may differ.
+  * float32 and float64 inputs are encoded exactly as the reference does
+    (float64 input through a float64 kernel, codecs.py:254); other dtypes
+    are converted to float32 first.
 """
 
 from __future__ import annotations
@@ -367,6 +367,8 @@ def encode_buffer(x, codebook: Codebook, *, device=None, sync: bool = True) -> Q
     call is fully asynchronous and the check happens when ``scale`` is read.
     """
     spec = codebook.spec
+    if _is_f64(x):  # the reference computes float64 input in float64 (codecs.py:254)
+        return _encode_f64(x, codebook, device, sync)
     t, shape = as_device_f32(x, device)
     dev = t.device
     n = t.numel()
@@ -387,6 +389,48 @@ def encode_buffer(x, codebook: Codebook, *, device=None, sync: bool = True) -> Q
                                 ws.numel(), None, meta.data_ptr(), stream))
     q = QuantizedTensor(codes, shape, spec, scale_tensor=meta[1:].view(torch.float32), meta=meta)
     q._keepalive = t  # input must outlive the asynchronous kernel
+    if sync:
+        q._finish()
+    return q
+
+
+def _is_f64(x) -> bool:
+    if isinstance(x, torch.Tensor):
+        return x.dtype == torch.float64
+    return np.asarray(x).dtype == np.float64
+
+
+def _encode_f64(x, codebook: Codebook, device, sync: bool) -> QuantizedTensor:
+    """float64 input: the reference decision restated in float64 on the GPU
+    (a8_encode_f64), bit-exact with codecs.py:254-268 for any float64 data."""
+    spec = codebook.spec
+    if isinstance(x, torch.Tensor):
+        dev = _cuda_device(x.device if x.is_cuda else device)
+        shape = tuple(x.shape)
+        t = x.to(dev).contiguous().reshape(-1)
+    else:
+        arr = np.asarray(x)
+        shape = tuple(arr.shape)
+        dev = _cuda_device(device)
+        t = torch.from_numpy(np.ascontiguousarray(arr).reshape(-1)).to(dev)
+    n = t.numel()
+    if n == 0:
+        s = codebook.fixed_scale
+        return QuantizedTensor(torch.empty(0, dtype=torch.uint8, device=dev), shape, spec, 1.0 if s is None else s)
+    book, _ = codebook.device_tables(dev)
+    fixed = codebook.fixed_scale
+    with torch.cuda.device(dev):
+        stream = _stream(dev)
+        meta = torch.empty(2, dtype=torch.int32, device=dev)
+        codes = torch.empty(n, dtype=torch.uint8, device=dev)
+        seg = N.EncSeg64(t.data_ptr(), n, 0, 0, 0)
+        lay = N.Layout(codes.data_ptr(), meta.data_ptr() + 4, round16(n), round16(n), 0, 0, 1, 0)
+        ws = workspace(dev, stream, 1)
+        N.check(N.lib.a8_encode_f64(C.byref(seg), 1, book.data_ptr(), spec.norm_code,
+                                    1.0 if fixed is None else fixed, lay, ws.data_ptr(), ws.numel(),
+                                    None, meta.data_ptr(), stream))
+    q = QuantizedTensor(codes, shape, spec, scale_tensor=meta[1:].view(torch.float32), meta=meta)
+    q._keepalive = t
     if sync:
         q._finish()
     return q

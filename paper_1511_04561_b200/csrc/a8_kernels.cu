@@ -1088,3 +1088,182 @@ extern "C" int a8_decode(const a8_dec_seg_t* segs, int nseg, const void* book_de
     decode_kernel<<<(unsigned)grid, kDecThreads, smem, st>>>(p);
     return cuda_check("a8_decode");
 }
+
+// ---------------------------------------------------------------------------
+// float64 input: the reference decision restated directly (codecs.py:254-268)
+//   y = fl64(|x| / s), s = float32(max|x|) (absmax) | float32(10^d) | 1
+//   idx = clip(searchsorted_left(values, y), 1, D-1)
+//   pick = fl64(y - v[idx-1]) <= fl64(v[idx] - y) ? idx-1 : idx
+// Two launches for absmax (max over the 64-bit |x| patterns, then encode).
+
+namespace a8 {
+
+struct F64Seg {
+    const double* x;
+    int64_t n;
+    int64_t flat_off;
+    int32_t scale_idx;
+    int32_t pad;
+    int64_t cstart;
+};
+
+struct F64Params {
+    a8_layout_t lay;
+    const a8_book_t* book;
+    WsHead* head;
+    SegCtl* ctl;
+    const unsigned int* status_in;
+    unsigned int* status_out;
+    float fixed_scale;
+    int absmax;
+    int nseg;
+    int pad;
+    int64_t total;
+    F64Seg segs[kInlineSegs];
+};
+
+constexpr int kF64Chunk = 4096;
+
+__device__ __forceinline__ int f64_seg_of(const F64Params& p, int64_t c) {
+    int lo = 0, hi = p.nseg;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (p.segs[mid].cstart <= c)
+            lo = mid;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(256) f64_absmax_kernel(const __grid_constant__ F64Params p) {
+    __shared__ unsigned long long red[8];
+    for (int64_t c = blockIdx.x; c < p.total; c += gridDim.x) {
+        const int s = f64_seg_of(p, c);
+        const F64Seg& sg = p.segs[s];
+        const int64_t base = (c - sg.cstart) * kF64Chunk;
+        const int64_t cnt = min((int64_t)kF64Chunk, sg.n - base);
+        unsigned long long m = 0;
+        for (int64_t i = threadIdx.x; i < cnt; i += 256)
+            m = max(m, (unsigned long long)__double_as_longlong(sg.x[base + i]) & 0x7fffffffffffffffull);
+        for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long mm = 0;
+            for (int w = 0; w < 8; ++w) mm = max(mm, red[w]);
+            if (mm) atomicMax(reinterpret_cast<unsigned long long*>(&p.ctl[s].amax), mm);
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(256) f64_encode_kernel(const __grid_constant__ F64Params p) {
+    __shared__ double sV[128];
+    __shared__ uint8_t sC[128];
+    __shared__ int sFinal;
+    const int tid = threadIdx.x;
+    const int D = p.book->ndistinct;
+    if (tid < 128) {
+        sV[tid] = tid < D ? p.book->values[tid] : __longlong_as_double(0x7ff0000000000000ll);  // +inf pad
+        sC[tid] = p.book->codes[tid];
+    }
+    __syncthreads();
+    unsigned int bad = 0;
+    const int64_t L = p.lay.block_len;
+    const int64_t gap = p.lay.block_stride - p.lay.block_len;
+    for (int64_t c = blockIdx.x; c < p.total; c += gridDim.x) {
+        const int s = f64_seg_of(p, c);
+        const F64Seg& sg = p.segs[s];
+        float sf = p.fixed_scale;
+        if (p.absmax) {
+            const unsigned long long mb = __ldcg(reinterpret_cast<const unsigned long long*>(&p.ctl[s].amax));
+            if (mb >= 0x7ff0000000000000ull) bad = 1;
+            const double peak = __longlong_as_double((long long)mb);
+            sf = peak > 0.0 ? __double2float_rn(peak) : 1.0f;  // codecs.py:234-241
+        }
+        const double sd = (double)sf;
+        const int64_t base = (c - sg.cstart) * kF64Chunk;
+        const int64_t cnt = min((int64_t)kF64Chunk, sg.n - base);
+        if (base == 0 && tid < p.lay.scale_reps) p.lay.scales[tid * p.lay.scale_block_stride + sg.scale_idx] = sf;
+        for (int64_t i = tid; i < cnt; i += 256) {
+            const double xv = sg.x[base + i];
+            if (!isfinite(xv)) bad = 1;
+            const double y = __ddiv_rn(fabs(xv), sd);
+            int lo = 0;  // #{values < y} = searchsorted left
+#pragma unroll
+            for (int step = 64; step; step >>= 1)
+                if (sV[lo + step - 1] < y) lo += step;
+            const int idx = min(max(lo, 1), D - 1);
+            const int pick = (__dsub_rn(y, sV[idx - 1]) <= __dsub_rn(sV[idx], y)) ? idx - 1 : idx;
+            uint32_t code = sC[pick];
+            if (xv < 0.0 && pick != 0) code |= 0x80u;  // codecs.py:267-268
+            const int64_t f = sg.flat_off + base + i;
+            p.lay.codes[f + (f / L) * gap] = (uint8_t)code;
+        }
+    }
+    if (__syncthreads_or(bad) && tid == 0) atomicOr(&p.head->status, A8_STATUS_NONFINITE);
+    if (tid == 0) {
+        __threadfence();
+        sFinal = atomicAdd(&p.head->ctas_done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (sFinal) {
+        __threadfence();
+        for (int i = tid; i < p.nseg; i += 256) *reinterpret_cast<unsigned long long*>(&p.ctl[i].amax) = 0ull;
+        if (tid < p.lay.scale_reps) {
+            const unsigned int stt = atomicAdd(&p.head->status, 0u) | (p.status_in ? *p.status_in : 0u);
+            p.status_out[(int64_t)tid * p.lay.scale_block_stride] = stt;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            p.head->ctas_done = 0u;
+            p.head->status = 0u;
+        }
+        __threadfence();
+    }
+}
+
+}  // namespace a8
+
+extern "C" int a8_encode_f64(const a8_enc_seg64_t* segs, int nseg, const void* book_dev, int norm,
+                             float fixed_scale, a8_layout_t layout, void* workspace, size_t workspace_bytes,
+                             const uint32_t* status_in, uint32_t* status_out, void* stream) {
+    if (nseg <= 0 || nseg > kInlineSegs) return fail(A8_ERR_USAGE, "a8_encode_f64: 1..32 segments per call");
+    if (!segs || !book_dev || !workspace || !status_out) return fail(A8_ERR_USAGE, "a8_encode_f64: null argument");
+    if (int rc = check_layout(layout)) return rc;
+    if (layout.scale_reps < 1 || layout.scale_reps > 256) return fail(A8_ERR_USAGE, "a8_encode_f64: scale_reps out of range");
+    if (ws_capacity(workspace_bytes) < nseg) return fail(A8_ERR_USAGE, "a8_encode_f64: workspace too small");
+    int device = 0;
+    cudaGetDevice(&device);
+    DevInfo di;
+    if (int rc = dev_info(device, &di)) return rc;
+    F64Params p;
+    memset(&p, 0, sizeof(p));
+    p.lay = layout;
+    p.book = static_cast<const a8_book_t*>(book_dev);
+    uint8_t* ws = static_cast<uint8_t*>(workspace);
+    p.head = reinterpret_cast<WsHead*>(ws);
+    p.ctl = reinterpret_cast<SegCtl*>(ws + ctl_off());
+    p.status_in = status_in;
+    p.status_out = status_out;
+    p.fixed_scale = fixed_scale;
+    p.absmax = norm == A8_NORM_ABSMAX;
+    p.nseg = nseg;
+    int64_t ch = 0;
+    for (int i = 0; i < nseg; ++i) {
+        if (segs[i].n < 0 || (segs[i].n > 0 && !segs[i].x) || segs[i].flat_off % 16)
+            return fail(A8_ERR_USAGE, "a8_encode_f64: bad segment");
+        p.segs[i] = F64Seg{segs[i].x, segs[i].n, segs[i].flat_off, segs[i].scale_idx, 0, ch};
+        ch += std::max<int64_t>(1, (segs[i].n + kF64Chunk - 1) / kF64Chunk);
+    }
+    p.total = ch;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const unsigned grid = (unsigned)std::min<int64_t>((int64_t)di.sms * 8, ch);
+    if (p.absmax) {
+        f64_absmax_kernel<<<grid, 256, 0, st>>>(p);
+        if (int rc = cuda_check("a8_encode_f64(absmax)")) return rc;
+    }
+    f64_encode_kernel<<<grid, 256, 0, st>>>(p);
+    return cuda_check("a8_encode_f64");
+}

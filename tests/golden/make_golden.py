@@ -200,6 +200,19 @@ def main() -> None:
         arrays[key + "/sizes"] = np.array(sizes, np.int32)
         arrays[key + "/scales"] = np.array(scs, np.float64)
 
+    # float64 inputs (the reference's DP/MP seams feed float64, mlp.py:330):
+    # values float32 cannot represent, exact midpoints, wide magnitudes
+    r = np.random.default_rng(51)
+    for spec in SPECS:
+        x = r.normal(size=3000) * 10.0 ** r.integers(-8, 3, size=3000)
+        cb = C.build_codebook(dspec(*spec))
+        mids = (cb.sorted_values[:-1] + cb.sorted_values[1:]) / 2.0
+        x = np.concatenate([x, mids, -mids, mids * (1 + 2**-52), np.nextafter(mids, 0)])
+        codes, s, _ = ref_encode(x, spec)
+        arrays[f"f64/{tag(*spec)}/x"] = x
+        arrays[f"f64/{tag(*spec)}/codes"] = codes
+        meta.setdefault("f64", {})[tag(*spec)] = {"scale": s}
+
     # A8T1 files written by the reference (tensorfile.py:56-88): byte images
     import tempfile
 
