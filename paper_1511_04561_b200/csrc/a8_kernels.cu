@@ -753,6 +753,7 @@ struct DevInfo {
 };
 
 static std::mutex g_mu;
+static std::mutex g_plan_mu;  // serialises workspace plan upload + launch pairs
 static DevInfo g_dev[64];
 
 static int dev_info(int device, DevInfo* out) {
@@ -1014,19 +1015,23 @@ extern "C" int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_de
     p.total = blks[nblk].tstart;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if ((int)blks.size() > max_blocks(nseg)) return fail(A8_ERR_USAGE, "a8_encode: schedule overflow");
+    const int64_t grid = std::min<int64_t>((int64_t)di.sms * di.enc_occ, std::max<int64_t>(1, p.total));
     if (nseg <= kInlineSegs && (int)blks.size() <= kInlineBlks) {
         std::copy(d.begin(), d.end(), p.segs);
         std::copy(blks.begin(), blks.end(), p.blks);
+        encode_kernel<<<(unsigned)grid, kEncThreads, kEncDynSmem, st>>>(p);
     } else {
+        // the plan goes through the workspace: upload + launch must not be
+        // interleaved with another thread's upload to the same workspace
+        std::lock_guard<std::mutex> lk(g_plan_mu);
         uint8_t* plan = ws + plan_off(cap);
         const size_t sb = sizeof(EncSegD) * nseg;
         cudaMemcpyAsync(plan, d.data(), sb, cudaMemcpyHostToDevice, st);
         cudaMemcpyAsync(plan + sb, blks.data(), sizeof(EncBlk) * blks.size(), cudaMemcpyHostToDevice, st);
         p.segs_dev = reinterpret_cast<const EncSegD*>(plan);
         p.blks_dev = reinterpret_cast<const EncBlk*>(plan + sb);
+        encode_kernel<<<(unsigned)grid, kEncThreads, kEncDynSmem, st>>>(p);
     }
-    const int64_t grid = std::min<int64_t>((int64_t)di.sms * di.enc_occ, std::max<int64_t>(1, p.total));
-    encode_kernel<<<(unsigned)grid, kEncThreads, kEncDynSmem, st>>>(p);
     return cuda_check("a8_encode");
 }
 
@@ -1076,16 +1081,20 @@ extern "C" int a8_decode(const a8_dec_seg_t* segs, int nseg, const void* book_de
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (nseg <= kInlineSegs) {
         std::copy(d.begin(), d.begin() + nseg, p.segs);
+        const size_t smem = dec_smem(nranks);
+        const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)di.sms * di.dec_occ, chunks));
+        decode_kernel<<<(unsigned)grid, kDecThreads, smem, st>>>(p);
     } else {
         const int cap = ws_capacity(workspace_bytes);
         if (cap < nseg) return fail(A8_ERR_USAGE, "a8_decode: workspace too small for the segment count");
+        std::lock_guard<std::mutex> lk(g_plan_mu);  // upload + launch, not interleaved
         uint8_t* plan = static_cast<uint8_t*>(workspace) + plan_off(cap);
         cudaMemcpyAsync(plan, d.data(), sizeof(DecSegD) * nseg, cudaMemcpyHostToDevice, st);
         p.segs_dev = reinterpret_cast<const DecSegD*>(plan);
+        const size_t smem = dec_smem(nranks);
+        const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)di.sms * di.dec_occ, chunks));
+        decode_kernel<<<(unsigned)grid, kDecThreads, smem, st>>>(p);
     }
-    const size_t smem = dec_smem(nranks);
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)di.sms * di.dec_occ, chunks));
-    decode_kernel<<<(unsigned)grid, kDecThreads, smem, st>>>(p);
     return cuda_check("a8_decode");
 }
 

@@ -129,6 +129,12 @@ class TorchDistComm:
     def all_gather(self, out: torch.Tensor, slot: torch.Tensor) -> None:
         dist.all_gather_into_tensor(out, slot if self._inplace() else slot.clone(), group=self.group)
 
+    def all_gather_async(self, out: torch.Tensor, slot: torch.Tensor):
+        """Start the all-gather; ``.wait()`` on the result makes the current
+        stream wait for it (NCCL: no host block)."""
+        return dist.all_gather_into_tensor(out, slot if self._inplace() else slot.clone(), group=self.group,
+                                           async_op=True)
+
     def all_to_all(self, recv: torch.Tensor, send: torch.Tensor) -> None:
         dist.all_to_all_single(recv, send, group=self.group)
 
@@ -213,7 +219,8 @@ class GradientExchange:
     """
 
     def __init__(self, spec: DataTypeSpec, group=None, mode: str = "allgather", op: str = "avg",
-                 check: str = "deferred", codec: Optional[SegmentCodec] = None, comm=None):
+                 check: str = "deferred", codec: Optional[SegmentCodec] = None, comm=None,
+                 chunk_elems: int = 8 << 20, max_chunks: int = 8):
         if mode not in MODES:
             raise UsageError(f"mode must be one of {MODES}, got {mode!r}")
         if op not in OPS:
@@ -232,6 +239,8 @@ class GradientExchange:
         self._bufs: dict = {}
         self._pending = None  # (event or None, host status tensor)
         self.calls = 0
+        self.chunk_elems = int(chunk_elems)  # allgather: elements per pipelined chunk
+        self.max_chunks = int(max_chunks)
 
     # -- distributed context
     def _world(self):
@@ -302,20 +311,63 @@ class GradientExchange:
         self.calls += 1
         return outs
 
+    def _chunking(self, plan: Plan, nranks: int):
+        """K chunk-blocks of C elements for the pipelined all-gather (K = 1
+        on one rank or for small buckets).  Cached per plan."""
+        key = ("chunks", plan.sizes, nranks)
+        hit = self._plans.get(key)
+        if hit is None:
+            K = 1 if nranks == 1 else int(min(self.max_chunks, max(1, -(-plan.flat // self.chunk_elems))))
+            C = round16(-(-plan.flat // K))
+            K = -(-plan.flat // C)
+            pieces: list = [[] for _ in range(K)]
+            for t, n in enumerate(plan.sizes):
+                a = 0
+                while a < n:
+                    f = plan.offs[t] + a
+                    j = f // C
+                    b = min(n, (j + 1) * C - plan.offs[t])
+                    pieces[j].append((t, a, b - a, f))
+                    a = b
+            hit = self._plans[key] = (K, C, pieces)
+        return hit
+
     def _allgather(self, xs, outs, plan: Plan, nranks, rank, dev):
-        B = plan.allgather_block()
-        gathered = self._buffer("gather", nranks * B, dev)
+        """Encode into K chunk-blocks laid out [r0 codes | r0 scales+status |
+        r1 codes | ...] (rank stride = C + gap), all-gather each block in
+        place, and decode a block's pieces as soon as it has arrived, so the
+        decode of block j overlaps the all-gather of block j+1."""
+        K, C, pieces = self._chunking(plan, nranks)
+        P = C + plan.gap  # one rank's part of a block
+        BS = nranks * P  # one block
+        gathered = self._buffer("gather", K * BS, dev)
         idx = list(range(plan.nseg))
-        mine = rank * B
-        status_off = plan.flat + 4 * plan.status_slot
-        self.codec.encode(xs, plan.offs, idx, self.cb, gathered, mine, mine + plan.flat,
-                          plan.flat, plan.flat, 0, 1, mine + status_off)
-        if nranks > 1:
-            self.comm.all_gather(gathered, gathered[mine:mine + B])
+        mine = rank * P
+        self.codec.encode(xs, plan.offs, idx, self.cb, gathered, mine, mine + C, C, BS, BS // 4, K,
+                          mine + C + 4 * plan.status_slot)
         status = self._buffer("status", 4, dev)
-        self.codec.decode(outs, plan.offs, idx, self.cb, gathered, 0, plan.flat, plan.flat,
-                          plan.flat, 0, B, nranks, 1 if self.op == "avg" else 0,
-                          plan.status_slot, 1, status)
+        op = 1 if self.op == "avg" else 0
+        if nranks == 1:
+            self.codec.decode(outs, plan.offs, idx, self.cb, gathered, 0, C, C, BS, BS // 4, P, 1, op,
+                              plan.status_slot, 1, status)
+            self._collect_status(status)
+            return
+        start = getattr(self.comm, "all_gather_async", None)
+        handles = []
+        for j in range(K):
+            blk = gathered[j * BS:(j + 1) * BS]
+            if start is not None:
+                handles.append(start(blk, blk[mine:mine + P]))
+            else:
+                self.comm.all_gather(blk, blk[mine:mine + P])
+                handles.append(None)
+        for j in range(K):
+            if handles[j] is not None:
+                handles[j].wait()
+            po = [outs[t].view(-1)[a:a + n] for (t, a, n, f) in pieces[j]]
+            self.codec.decode(po, [f for (t, a, n, f) in pieces[j]], [t for (t, a, n, f) in pieces[j]], self.cb,
+                              gathered, 0, C, C, BS, BS // 4, P, nranks, op, plan.status_slot, 1,
+                              status if j == K - 1 else None)
         self._collect_status(status)
 
     def _two_round(self, xs, outs, plan: Plan, nranks, rank, dev):

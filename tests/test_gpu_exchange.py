@@ -73,6 +73,26 @@ def test_virtual_ranks_match_oracle(nranks, mode, op, cuda):
             assert a.tobytes() == b.tobytes(), (r, mode, op)  # bit-exact in practice
 
 
+@pytest.mark.parametrize("nranks", [2, 4, 8])
+@pytest.mark.parametrize("chunk", [4096, 20000])
+def test_pipelined_allgather_chunks(nranks, chunk, cuda):
+    """allgather with K > 1 chunk-blocks (pieces split at chunk boundaries)."""
+    spec = A.DataTypeSpec("dynamic-tree", "absmax")
+
+    def body(rank, comm):
+        ex = A.GradientExchange(spec, mode="allgather", check="sync", comm=comm, chunk_elems=chunk)
+        ts = [torch.from_numpy(g).to(cuda) for g in grads(rank, SMALL, 7)]
+        ex(ts)
+        torch.cuda.synchronize()
+        return [t.cpu().numpy() for t in ts]
+
+    res = run_virtual_ranks(nranks, body)
+    want = O.exchange_allgather([grads(r, SMALL, 7) for r in range(nranks)], "dynamic-tree", "absmax")
+    for r in range(nranks):
+        for a, b in zip(res[r], want):
+            assert a.tobytes() == b.tobytes(), (r, nranks, chunk)
+
+
 @pytest.mark.parametrize("spec", [A.DataTypeSpec("linear", "absmax"), A.DataTypeSpec("mantissa", "none"),
                                   A.DataTypeSpec("static-tree", "decade", -2)], ids=lambda s: s.label())
 def test_other_specs_three_ranks(spec, cuda):
