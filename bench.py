@@ -301,6 +301,26 @@ def run_b200(args, nranks, rank, local_rank):
                 "kernel_ms_per_step": kms,
                 "codec_roundtrip_GBps": (alg["encode"] + alg["decode"]) / ((kms["encode"] + kms["decode"]) * 1e-3) / 1e9}
 
+    # north-star comparison at N > 1: a 32-bit NCCL all-reduce of the same
+    # gradient bucket (one flat fp32 buffer), fp32-equivalent GB/s
+    nccl = None
+    if nranks > 1:
+        flat = torch.cat([g.reshape(-1) for g in grads])
+        for _ in range(3):
+            dist.all_reduce(flat)
+        torch.cuda.synchronize()
+        barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record()
+        for _ in range(args.steps):
+            dist.all_reduce(flat)
+        a1.record()
+        torch.cuda.synchronize()
+        nms = max_over_ranks(a0.elapsed_time(a1) / args.steps)
+        nccl = {"value": nranks * 4.0 * n / (nms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": nms,
+                "algo": os.environ.get("NCCL_ALGO", "default"), "speedup_8bit": value / (nranks * 4.0 * n / (nms * 1e-3) / 1e9)}
+        del flat
+
     # e2e: host buffers through the public API, copies inside the timed region.
     # Every step copies its gradients host->device (pinned), exchanges them
     # and copies the averaged result device->host.  Steps are software
@@ -376,6 +396,7 @@ def run_b200(args, nranks, rank, local_rank):
             "config": workload_config(args, nranks), "roofline": roofline, "cpu_baseline": cpu,
             "e2e": e2e, "clocks": clk.summary(), "gpu_launches": int(sum(launches.values())),
             "gpu_launches_per_step": {k: v / args.steps for k, v in launches.items()},
+            "nccl_fp32_allreduce": nccl,
         }
         print(json.dumps(line), flush=True)
 
@@ -386,7 +407,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--mode", default="allgather", choices=["allgather", "two_round"])
+    ap.add_argument("--mode", default="auto", choices=["auto", "allgather", "two_round"])
     ap.add_argument("--cpu-elems", type=int, default=1 << 23)
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu", action="store_true")
@@ -395,6 +416,8 @@ def main():
         args.warmup = 3
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.mode == "auto":  # ingress (N-1)n vs 2(N-1)/N n: two_round wins from N = 4
+        args.mode = "allgather" if max(world, args.gpus) <= 2 else "two_round"
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus and world > 1:
