@@ -13,7 +13,7 @@ from pathlib import Path
 
 from .errors import ConfigError, InputError, UsageError
 
-_LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libapprox8_b200.so"
+_LIB_PATH = Path(os.environ.get("A8_LIB") or Path(__file__).resolve().parent / "_lib" / "libapprox8_b200.so")
 
 A8_OK, A8_ERR_INPUT, A8_ERR_CONFIG, A8_ERR_USAGE, A8_ERR_CUDA = 0, 1, 2, 3, 4
 A8_STATUS_NONFINITE = 1

@@ -41,16 +41,19 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, ticket_trace: bool = False) -> Path:
+    """``ticket_trace``: a debug build with per-ticket timestamps into
+    ``_lib_trace/`` (load it with A8_LIB=<path>); never the product library."""
+    lib = (PKG / "_lib_trace" / LIB.name) if ticket_trace else LIB
+    if not force and not ticket_trace and not _stale():
         return LIB
-    LIBDIR.mkdir(exist_ok=True)
-    tmp = LIB.with_suffix(".so.tmp")
+    lib.parent.mkdir(exist_ok=True)
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [
         nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo",
         "-Xcompiler", "-fPIC,-O3", "-shared", "-cudart", "static",
         "-Xptxas", "-v" if verbose else "-O3",
-        f"-I{INCLUDE}", f"-I{CSRC}",
+        f"-I{INCLUDE}", f"-I{CSRC}", *(["-DA8_TICKET_TRACE"] if ticket_trace else []),
         *[str(CSRC / s) for s in SOURCES],
         "-o", str(tmp),
     ]
@@ -59,9 +62,9 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + res.stdout + res.stderr)
     if verbose:
         sys.stderr.write(res.stdout + res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, ticket_trace="--ticket-trace" in sys.argv))

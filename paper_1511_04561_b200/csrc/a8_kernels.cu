@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <deque>
 #include <mutex>
 #include <string>
@@ -43,8 +44,6 @@ constexpr int kMaxRanks = 16;
 constexpr int kInlineSegs = 32;
 constexpr int kInlineBlks = 3 * kInlineSegs + 2;
 static int max_blocks(int nseg) { return 6 * nseg + 8; }
-constexpr int64_t kGroupMin = 2 << 20;  // schedule segments in groups of at least this many elements
-constexpr int64_t kFill = 768;          // E-chunks of the previous group that cover a table build
 
 // ---------------------------------------------------------------------------
 // device-side plan / workspace
@@ -161,44 +160,104 @@ static size_t plan_bytes(int nseg) {
 }
 
 // ---------------------------------------------------------------------------
-// K2: thresholds + bucket table for one scale, built by the consumer warps
-// into global memory (`dst`), staged through shared memory.
+// K2: thresholds for one scale, built by the consumer warps of one CTA and
+// published to global memory.  Each threshold travels as a tagged 64-bit
+// word (1 << 32 | T): a reader spins on its own word until the tag is set,
+// so the publish needs neither a fence nor a flag (one L2 round trip instead
+// of three -- under full HBM load each is 1-3 us).  Every CTA that encodes
+// the segment expands the thresholds into its own shared-memory bucket
+// table (fill_lut_local).  The last CTA of the launch clears the tags.
 
 __device__ __forceinline__ unsigned long long gtime();
 
+__device__ __forceinline__ unsigned long long* seg_thresholds(a8_lut_t* luts, int seg) {
+    return reinterpret_cast<unsigned long long*>(luts + seg);  // first 1 KB of the segment's table slot
+}
+
 // sV / sCanon: the codebook's distinct values and canonical codes, staged
 // in shared memory at kernel start; D = number of distinct values.
-__device__ void build_lut(const double* sV, const uint8_t* sCanon, int D, float scale, a8_lut_t* dst,
-                          uint32_t* sT, int ctid, unsigned long long* tr) {
+__device__ void build_thresholds(const double* sV, int D, float scale, unsigned long long* dst, int ctid) {
     if (ctid < 128) {
         uint32_t t = kInfBits;
         if (scale_ok(scale) && ctid + 1 < D) t = threshold((double)scale, sV[ctid], sV[ctid + 1]);
+        st_relaxed_u64(dst + ctid, (1ull << 32) | t);
+    }
+}
+
+// Wait for a segment's thresholds and stage them in shared memory; returns
+// (to every consumer thread) the number of finite thresholds.
+__device__ int load_thresholds(const unsigned long long* src, const unsigned long long* pre, uint32_t* sT,
+                               int ctid) {
+    uint32_t t = kInfBits;
+    if (ctid < 128) {
+        // `pre`: a bulk-copied snapshot; words not yet tagged in it are re-read
+        unsigned long long v = pre ? pre[ctid] : 0ull;
+        if (!(v >> 32)) v = ld_relaxed_u64(src + ctid);
+        unsigned int ns = 32;
+        while (!(v >> 32)) {
+            __nanosleep(ns);
+            ns = min(ns * 2u, 256u);
+            v = ld_relaxed_u64(src + ctid);
+        }
+        t = (uint32_t)v;
         sT[ctid] = t;
     }
-    const int F = nbar_popc(kBarC, kConsumers, ctid < 127 && sT[ctid < 128 ? ctid : 0] < kInfBits);
-    if (tr && ctid == 0) tr[0] = gtime();
-    int32_t kbase;
-    uint32_t len;
-    lut_geometry(sT, (uint32_t)F, &kbase, &len);
+    return nbar_popc(kBarC, kConsumers, ctid < 127 && t < kInfBits);
+}
+
+// Expand thresholds into the bucket table in shared memory (kConsumers
+// threads, 16 consecutive buckets each): count thresholds per bucket with
+// shared atomics, exclusive-scan the counts (lo = #(key < k), hi = lo +
+// count), then write the entries in place.  Entry-for-entry equal to
+// lut_entry(); returns false (for this thread) if one of its buckets holds
+// two distinct thresholds.  Needs len <= kLutMax = 16 * kConsumers.
+static_assert(kLutMax == 16 * kConsumers, "one thread per 16 buckets");
+__device__ bool fill_lut_local(const uint32_t* T, uint32_t F, const uint8_t* canon, int32_t kbase, uint32_t* e,
+                               unsigned int* sWarp, int ctid) {
+    const int lane = ctid & 31, w = ctid >> 5;
+    uint4* e4 = reinterpret_cast<uint4*>(e) + 4 * ctid;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) e4[q] = make_uint4(0u, 0u, 0u, 0u);
+    nbar_sync(kBarC, kConsumers);
+    if ((uint32_t)ctid < F) atomicAdd(&e[(int32_t)(T[ctid] >> kKeyShift) - kbase], 1u);
+    nbar_sync(kBarC, kConsumers);
+    uint32_t c[16];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint4 v = e4[q];
+        c[4 * q] = v.x;
+        c[4 * q + 1] = v.y;
+        c[4 * q + 2] = v.z;
+        c[4 * q + 3] = v.w;
+    }
+    uint32_t tot = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) tot += c[i];
+    uint32_t inc = tot;  // inclusive warp scan of the per-thread totals
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) sWarp[w] = inc;
+    nbar_sync(kBarC, kConsumers);
+    uint32_t lo = inc - tot;
+    for (int i = 0; i < w; ++i) lo += sWarp[i];
     bool ok = true;
-    if (len <= (uint32_t)kLutMax) {  // independent entries, strided: ILP + coalesced stores
-#pragma unroll 4
-        for (uint32_t j = ctid; j < len; j += kConsumers) {
-            uint32_t v;
-            ok &= lut_entry(sT, (uint32_t)F, sCanon, kbase, j, &v);
-            dst->e[j] = v;
+    uint32_t v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const uint32_t hi = lo + c[i];
+        v[i] = (uint32_t)canon[lo] | ((uint32_t)canon[hi] << 8);
+        if (c[i]) {
+            v[i] |= (T[lo] & 0xffffu) << 16;
+            ok &= T[lo] == T[hi - 1];
         }
+        lo = hi;
     }
-    const int valid = nbar_and(kBarC, kConsumers, ok) && len <= (uint32_t)kLutMax;
-    if (tr && ctid == 0) tr[1] = gtime();
-    if (ctid < 128) dst->T[ctid] = sT[ctid];
-    if (ctid == 0) {
-        dst->len = len;
-        dst->kbase = kbase;
-        dst->valid = valid;
-        dst->nfinite = F;
-        dst->scale = scale;
-    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) e4[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    return ok;
 }
 
 // Copy a table into shared memory.  Readers bypass L1: the table may have
@@ -232,10 +291,21 @@ struct StageMeta {
     int32_t seg;
     int32_t kind;      // 0 A, 1 E, 2 end
     int32_t simple;    // full chunk inside one block of the code layout
-    int32_t pad;
+    int32_t last;      // the producer's next ticket is not in this run: flush after this A-chunk
+    int32_t tkt;       // A8_TICKET_TRACE builds: the ticket
+    int32_t tpref;     // the stage also carries a prefetch of the segment's tagged thresholds
 };
 
-constexpr unsigned int kTicketBatch = 4;  // tickets per atomic (one batch prefetched)
+#ifdef A8_TICKET_TRACE
+// Debug builds only (build.py --ticket-trace): per-ticket issue / done times.
+constexpr int kTraceTickets = 1 << 17;
+__device__ unsigned long long g_ticket_trace[kTraceTickets][5];  // issue, done, kind|seg|cta, t known, stage free
+__device__ unsigned long long g_flush_trace[32][512][4];  // per (seg, cta): flush start, atom back, amax back, chunks
+#endif
+
+constexpr unsigned int kTicketBatch = 4;  // tickets per atomic (two batches prefetched)
+constexpr int kSmemSegs = 64;
+constexpr int kSmemBlks = 6 * kSmemSegs + 8;  // max_blocks(kSmemSegs)
 
 // ---------------------------------------------------------------------------
 // K1+K2+K3: persistent encode.
@@ -261,16 +331,27 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
     __shared__ __align__(8) uint64_t sFull[kStages];
     __shared__ __align__(8) uint64_t sEmpty[kStages];
     __shared__ StageMeta sMeta[kStages];
+    __shared__ __align__(16) unsigned long long sTpre[kStages][128];  // threshold prefetch per stage
     __shared__ int sHdr[4];
     __shared__ unsigned int sRed[kConsumerWarps];
     __shared__ int sLast;
     __shared__ int sFinal;
+    // the plan, staged in shared memory when it fits: the producer reads it
+    // on every ticket, and kernel-parameter / global reads cost it latency
+    __shared__ EncSegD sSeg[kSmemSegs];
+    __shared__ EncBlk sBlk[kSmemBlks];
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int lane = tid & 31;
     const EncSegD* segs = p.segs_dev ? p.segs_dev : p.segs;
     const EncBlk* blks = p.blks_dev ? p.blks_dev : p.blks;
+    if (p.nseg <= kSmemSegs && p.nblk + 1 <= kSmemBlks) {
+        for (int i = tid; i < p.nseg; i += kEncThreads) sSeg[i] = segs[i];
+        for (int i = tid; i <= p.nblk; i += kEncThreads) sBlk[i] = blks[i];
+        segs = sSeg;
+        blks = sBlk;
+    }
 
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -297,18 +378,31 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
             const int64_t gap = p.lay.block_stride - p.lay.block_len;
             // tickets come in batches; the next batch is requested one batch
             // ahead so the atomic's round trip never stalls the ring
+            // tickets come in batches, requested two batches ahead so the
+            // atomic's round trip (1-3 us under full HBM load) never stalls
             int64_t tb = (int64_t)atomicAdd(&p.head->ticket, kTicketBatch);
-            int64_t tnext = 0;
+            int64_t tq1 = (int64_t)atomicAdd(&p.head->ticket, kTicketBatch);
+            int64_t tq2 = 0;
+            int last_e = -1;  // segment of the last E-chunk issued
+            int lo = 0;       // block of the current ticket (tickets only increase)
             unsigned int g = 0;
             for (int it = 0;; ++it) {
                 const int st = it % kStages;
-                if (g == 0) tnext = (int64_t)atomicAdd(&p.head->ticket, kTicketBatch);
+                if (g == 0) tq2 = (int64_t)atomicAdd(&p.head->ticket, kTicketBatch);
                 const int64_t t = tb + g;
                 if (++g == kTicketBatch) {
                     g = 0;
-                    tb = tnext;
+                    tb = tq1;
+                    tq1 = tq2;
                 }
+#ifdef A8_TICKET_TRACE
+                asm volatile("" ::"l"(t));
+                const unsigned long long tr_known = gtime();
+#endif
                 mbar_wait(&sEmpty[st], ((it / kStages) & 1) ^ 1);
+#ifdef A8_TICKET_TRACE
+                const unsigned long long tr_free = gtime();
+#endif
                 StageMeta m;
                 if (t >= p.total) {
                     m.kind = kEnd;
@@ -316,14 +410,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                     mbar_arrive(&sFull[st]);
                     break;
                 }
-                int lo = 0, hi = p.nblk;  // blks[lo].tstart <= t < blks[hi].tstart
-                while (hi - lo > 1) {
-                    const int mid = (lo + hi) >> 1;
-                    if (blks[mid].tstart <= t)
-                        lo = mid;
-                    else
-                        hi = mid;
-                }
+                while (blks[lo + 1].tstart <= t) ++lo;  // blks[lo].tstart <= t < blks[lo+1].tstart
                 const EncBlk bk = blks[lo];
                 const EncSegD& sg = segs[bk.seg];
                 const int64_t k = t - bk.tstart;
@@ -341,11 +428,36 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                     m.code_off = f0 + j * gap;
                     m.simple = m.bulk == kChunk && f0 + kChunk <= (j + 1) * L;
                 }
+                {   // peek at this CTA's next ticket (tb + g after the advance above): an
+                    // A run's partial max is published as soon as its last chunk is
+                    // reduced, not when the next chunk's data arrives
+                    const int64_t tn = tb + g;
+                    m.last = !(tn < blks[lo + 1].tstart);
+                }
+#ifdef A8_TICKET_TRACE
+                m.tkt = (int32_t)t;
+                if (t < kTraceTickets) {
+                    g_ticket_trace[t][0] = gtime();
+                    g_ticket_trace[t][2] = ((uint64_t)kind << 40) | ((uint64_t)bk.seg << 20) | blockIdx.x;
+                    g_ticket_trace[t][3] = tr_known;
+                    g_ticket_trace[t][4] = tr_free;
+                }
+#endif
+                // first E-chunk of a segment in this CTA: the segment's tagged
+                // thresholds ride along with the chunk (one more bulk copy), so
+                // the consumers usually find them in shared memory instead of
+                // paying an L2 round trip at the segment switch
+                m.tpref = p.absmax && kind == kE && m.seg != last_e;
+                if (kind == kE) last_e = m.seg;
                 sMeta[st] = m;
-                if (m.bulk > 0) {
-                    mbar_arrive_expect_tx(&sFull[st], (uint32_t)m.bulk * 4u);
-                    bulk_g2s(sStage + (size_t)st * kChunk, sg.x + m.base, (uint32_t)m.bulk * 4u, &sFull[st],
-                             kind == kA ? keep : drop);
+                const uint32_t tx = (uint32_t)m.bulk * 4u + (m.tpref ? 1024u : 0u);
+                if (tx > 0) {
+                    mbar_arrive_expect_tx(&sFull[st], tx);
+                    if (m.bulk > 0)
+                        bulk_g2s(sStage + (size_t)st * kChunk, sg.x + m.base, (uint32_t)m.bulk * 4u, &sFull[st],
+                                 kind == kA ? keep : drop);
+                    if (m.tpref)
+                        bulk_g2s(sTpre[st], seg_thresholds(p.luts, m.seg), 1024u, &sFull[st], keep);
                 } else {
                     mbar_arrive(&sFull[st]);
                 }
@@ -356,6 +468,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
         const int ctid = tid - 32;
         const int cw = warp - 1;
         int cur = p.absmax ? -1 : -2;  // segment whose table is in shared memory (-2: static)
+        int tvalid = sHdr[0], tkbase = sHdr[1], tlenm1 = sHdr[2];  // that table's geometry
         uint8_t* const codes_base = p.lay.codes;
         const int64_t L = p.lay.block_len;
         const int64_t gap = p.lay.block_stride - p.lay.block_len;
@@ -378,30 +491,38 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
 #pragma unroll
                 for (int w = 0; w < kConsumerWarps; ++w) mm = max(mm, sRed[w]);
                 SegCtl* c = p.ctl + aseg;
+#ifdef A8_TICKET_TRACE
+                const unsigned long long f0 = gtime();
+#endif
                 if (mm) atomicMax(&c->amax, mm);
                 // acq_rel: publishes our max before the count, and (for the
                 // last contributor) makes every other CTA's max visible
                 const unsigned int done = atom_add_acq_rel(&c->a_done, acnt) + acnt;
                 sLast = (done == (unsigned int)segs[aseg].nA);
+#ifdef A8_TICKET_TRACE
+                const unsigned long long f1 = gtime();
+#endif
                 if (sLast) sHdr[3] = (int)ld_acquire(&c->amax);
+#ifdef A8_TICKET_TRACE
+                if (aseg < 32 && blockIdx.x < 512) {
+                    g_flush_trace[aseg][blockIdx.x][0] = f0;
+                    g_flush_trace[aseg][blockIdx.x][1] = f1;
+                    g_flush_trace[aseg][blockIdx.x][2] = sLast ? gtime() : 0ull;
+                    g_flush_trace[aseg][blockIdx.x][3] = acnt;
+                }
+#endif
             }
             nbar_sync(kBarC, kConsumers);
             if (sLast) {
-                // K2 for this segment: scale, thresholds, bucket table
+                // K2 for this segment: scale and thresholds
                 const EncSegD& sa = segs[aseg];
                 const unsigned int amax = (unsigned int)sHdr[3];
                 const float scale = amax == 0u ? 1.0f : __uint_as_float(amax);
                 if (ctid == 0) p.ctl[aseg].t_b0 = gtime();
                 if (amax >= kInfBits && ctid == 0) atomicOr(&p.head->status, A8_STATUS_NONFINITE);
-                build_lut(sV, sCanon, p.book->ndistinct, scale, p.luts + aseg, sT, ctid, &p.ctl[aseg].t_thr);
+                build_thresholds(sV, p.book->ndistinct, scale, seg_thresholds(p.luts, aseg), ctid);
                 if (ctid < p.lay.scale_reps) p.lay.scales[ctid * p.lay.scale_block_stride + sa.scale_idx] = scale;
-                __threadfence();  // each thread's table writes are gpu-visible ...
-                nbar_sync(kBarC, kConsumers);
-                if (ctid == 0) {  // ... before the flag is released
-                    p.ctl[aseg].t_b1 = gtime();
-                    st_release(&p.ctl[aseg].ready, 1u);
-                }
-                cur = -1;  // sT / sCanon / sHdr were used as scratch
+                if (ctid == 0) p.ctl[aseg].t_thr = p.ctl[aseg].t_fill = p.ctl[aseg].t_b1 = gtime();
             }
             aseg = -1;
             amx = 0;
@@ -446,8 +567,12 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                 amx = max(amx, part_max());
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&sEmpty[st]);  // stage consumed
+#ifdef A8_TICKET_TRACE
+                if (ctid == 0 && m.tkt < kTraceTickets) g_ticket_trace[m.tkt][1] = gtime();
+#endif
                 aseg = m.seg;
                 ++acnt;
+                if (m.last) flush();
                 continue;
             }
 
@@ -479,26 +604,29 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
             // ---------------- E: encode the chunk ----------------------------
             if (cur != m.seg && cur != -2) {
                 nbar_sync(kBarC, kConsumers);  // everyone is done with the old table
-                if (ctid == 0 && ld_acquire(&p.ctl[m.seg].ready) == 0u) {
-                    const unsigned long long w0 = gtime();
-                    unsigned int ns = 32;
-                    while (ld_acquire(&p.ctl[m.seg].ready) == 0u) {
-                        __nanosleep(ns);
-                        ns = min(ns * 2u, 256u);
+                const unsigned long long w0 = ctid == 0 ? gtime() : 0ull;
+                const int nf = load_thresholds(seg_thresholds(p.luts, m.seg), m.tpref ? sTpre[st] : nullptr, sT, ctid);
+                if (ctid == 0) {
+                    const unsigned long long w = gtime() - w0;
+                    if (w > 2000) {  // trace: waits longer than an L2 round trip
+                        atomicAdd(&p.head->wait_ns, w);
+                        atomicAdd(&p.head->waits, 1u);
                     }
-                    atomicAdd(&p.head->wait_ns, gtime() - w0);
-                    atomicAdd(&p.head->waits, 1u);
                 }
-                nbar_sync(kBarC, kConsumers);
-                load_lut_smem(p.luts + m.seg, sE, sT, sCanon, p.book, sHdr, ctid, kConsumers);
-                nbar_sync(kBarC, kConsumers);
+                int32_t kb;
+                uint32_t len;
+                lut_geometry(sT, (uint32_t)nf, &kb, &len);
+                tkbase = kb;
+                tlenm1 = (int)len - 1;
+                const bool ok = len <= (uint32_t)kLutMax && fill_lut_local(sT, nf, sCanon, kb, sE, sRed, ctid);
+                tvalid = nbar_and(kBarC, kConsumers, ok);  // also: sE complete
                 cur = m.seg;
             }
             if (cur == -2 && m.base == 0 && ctid < p.lay.scale_reps)
                 p.lay.scales[ctid * p.lay.scale_block_stride + sg.scale_idx] = p.static_lut->scale;
-            valid = sHdr[0];
-            kbase = sHdr[1];
-            lenm1 = sHdr[2];
+            valid = tvalid;
+            kbase = tkbase;
+            lenm1 = tlenm1;
             }
             unsigned int big = 0;  // max |x| bits (fixed-scale specs detect NaN/Inf here)
             if (m.simple && valid) {
@@ -566,6 +694,9 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                 atomicOr(&p.head->status, A8_STATUS_NONFINITE);
             __syncwarp();
             if (lane == 0) mbar_arrive(&sEmpty[st]);
+#ifdef A8_TICKET_TRACE
+            if (ctid == 0 && m.tkt < kTraceTickets) g_ticket_trace[m.tkt][1] = gtime();
+#endif
         }
     }
 
@@ -583,6 +714,8 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
             p.ctl[i].a_done = 0u;
             p.ctl[i].ready = 0u;
         }
+        if (p.absmax)
+            for (int i = tid; i < p.nseg * 128; i += kEncThreads) seg_thresholds(p.luts, i >> 7)[i & 127] = 0ull;
         if (tid < p.lay.scale_reps) {
             const unsigned int stt = atomicAdd(&p.head->status, 0u) | (p.status_in ? *p.status_in : 0u);
             p.status_out[(int64_t)tid * p.lay.scale_block_stride] = stt;
@@ -804,14 +937,17 @@ static int cuda_check(const char* what) {
 // Ticket order (host).
 //  * Fixed-scale specs: E-chunks only.
 //  * absmax: single-chunk segments become one F ticket each (no dependency),
-//    issued first.  The other segments, in descending size, form groups of
-//    >= kGroupMin elements.  Group i's E pass (reverse chunk order, so the
-//    data the A pass read last -- still in L2 -- comes first) can start only
-//    once its tables are built; the kFill tickets before it are independent
-//    work that covers the build: the first A-chunks of group i+1, topped up
-//    with held-back tail E-chunks of earlier groups (the L2-cold part of
-//    their E pass, whose tables are long done).
-static void schedule(const std::vector<EncSegD>& d, bool absmax, std::vector<EncBlk>* blks) {
+//    issued first.  Then the A-chunks of the multi-chunk segments, largest
+//    first.  A segment's E-chunks (reverse chunk order, so the data its A
+//    pass read last -- still in L2 -- comes first) are issued `wf` tickets
+//    after its last A-chunk, interrupting the A stream: `wf` covers the
+//    tickets the CTAs hold reserved in their rings plus the table build, so
+//    by the time a CTA reaches an E-chunk its table is normally published.
+//    When no A work is left to fill that distance, the filler is a
+//    held-back part of the largest segment's E pass (its L2-cold head,
+//    whose table is long done); what remains of it ends the launch, so the
+//    launch tail is dependency-free streaming.
+static void schedule(const std::vector<EncSegD>& d, bool absmax, int64_t wf, std::vector<EncBlk>* blks) {
     struct Run {
         int s;
         int kind;
@@ -824,27 +960,6 @@ static void schedule(const std::vector<EncSegD>& d, bool absmax, std::vector<Enc
         blks->push_back(EncBlk{t, r.s, (int32_t)((r.c0 << 2) | r.kind)});
         t += r.cnt;
     };
-    auto emit_all = [&](std::deque<Run>& q) {
-        for (const Run& r : q) emit(r);
-        q.clear();
-    };
-    auto total = [](const std::deque<Run>& q) {
-        int64_t n = 0;
-        for (const Run& r : q) n += r.cnt;
-        return n;
-    };
-    // move the first `want` chunks of q into out (splitting a run if needed)
-    auto take = [](std::deque<Run>& q, int64_t want, std::deque<Run>& out) {
-        while (want > 0 && !q.empty()) {
-            Run& r = q.front();
-            const int64_t now = std::min(want, r.cnt);
-            out.push_back(Run{r.s, r.kind, r.c0, now});
-            r.c0 += r.kind == kE ? -now : now;
-            r.cnt -= now;
-            want -= now;
-            if (r.cnt == 0) q.pop_front();
-        }
-    };
     const int nseg = (int)d.size();
     if (!absmax) {
         for (int s = 0; s < nseg; ++s) emit(Run{s, kE, d[s].nE - 1, d[s].nE});
@@ -853,43 +968,66 @@ static void schedule(const std::vector<EncSegD>& d, bool absmax, std::vector<Enc
     }
     for (int s = 0; s < nseg; ++s)
         if (d[s].n <= kChunk) emit(Run{s, kF, 0, 1});
-    // groups over the multi-chunk segments, largest first (d is ascending)
-    std::vector<std::deque<Run>> gA, gE;
-    {
-        int s = nseg - 1;
-        while (s >= 0 && d[s].n > kChunk) {
-            std::deque<Run> a, e;
-            int64_t sum = 0;
-            int first = s;
-            while (s >= 0 && d[s].n > kChunk && (sum < kGroupMin || s == first)) {
-                a.push_back(Run{s, kA, 0, d[s].nA});
-                sum += d[s].n;
-                --s;
-            }
-            for (auto it = a.rbegin(); it != a.rend(); ++it)  // last-read segment first
-                e.push_back(Run{it->s, kE, d[it->s].nE - 1, d[it->s].nE});
-            gA.push_back(std::move(a));
-            gE.push_back(std::move(e));
+    std::deque<Run> aq;  // A runs, largest segment first (d is ascending)
+    for (int s = nseg - 1; s >= 0 && d[s].n > kChunk; --s) aq.push_back(Run{s, kA, 0, d[s].nA});
+    struct Pending {
+        int64_t ready;
+        int s;
+    };
+    std::deque<Pending> pend;  // E passes waiting for their fill distance, in A order
+    Run pool{-1, kE, 0, 0};    // held-back E chunks (one segment's cold head)
+    const bool hold = aq.size() > 1;
+    auto emit_e = [&](int s) {
+        Run e{s, kE, d[s].nE - 1, d[s].nE};
+        if (hold && pool.s < 0) {  // first E pass: keep its cold head as filler
+            const int64_t h = std::min<int64_t>(e.cnt / 2, 2 * wf);
+            pool = Run{s, kE, h - 1, h};
+            e.cnt -= h;
         }
+        emit(e);
+    };
+    while (!aq.empty() || !pend.empty()) {
+        if (!pend.empty() && pend.front().ready <= t) {
+            emit_e(pend.front().s);
+            pend.pop_front();
+            continue;
+        }
+        const int64_t until = pend.empty() ? INT64_MAX : pend.front().ready;
+        if (!aq.empty()) {
+            Run& r = aq.front();
+            const int64_t now = std::min(r.cnt, until - t);
+            emit(Run{r.s, kA, r.c0, now});
+            r.c0 += now;
+            r.cnt -= now;
+            if (r.cnt == 0) {
+                pend.push_back(Pending{t + wf, r.s});
+                aq.pop_front();
+            }
+            continue;
+        }
+        if (pool.cnt > 0) {  // no A work left: fill from the pool
+            const int64_t now = std::min(pool.cnt, until - t);
+            emit(Run{pool.s, kE, pool.c0, now});
+            pool.c0 -= now;
+            pool.cnt -= now;
+            continue;
+        }
+        emit_e(pend.front().s);  // nothing independent left: the wait is unavoidable
+        pend.pop_front();
     }
-    const int ng = (int)gA.size();
-    std::deque<Run> held;  // L2-cold E tails, available as filler
-    if (ng > 0) emit_all(gA[0]);
-    for (int i = 0; i < ng; ++i) {
-        std::deque<Run> fill;
-        if (i + 1 < ng) take(gA[i + 1], kFill, fill);
-        take(held, kFill - total(fill), fill);
-        emit_all(fill);
-        std::deque<Run> head;
-        const int64_t te = total(gE[i]);
-        take(gE[i], i + 1 < ng ? te - std::min<int64_t>(kFill, te / 2) : te, head);
-        emit_all(head);
-        for (const Run& r : gE[i]) held.push_back(r);  // this group's tail
-        gE[i].clear();
-        if (i + 1 < ng) emit_all(gA[i + 1]);
-    }
-    emit_all(held);
+    emit(pool);
     blks->push_back(EncBlk{t, -1, 0});  // sentinel: total tickets
+}
+
+// Fill distance in tickets: what 2 CTAs/SM hold reserved (ring + ticket
+// batches) plus a table build's worth of throughput.  A8_SCHED_FILL
+// overrides it (tuning).
+static int64_t fill_distance(int64_t ctas) {
+    static const int64_t env = [] {
+        const char* e = getenv("A8_SCHED_FILL");
+        return e ? atoll(e) : -1ll;
+    }();
+    return env >= 0 ? env : ctas * 8 + 512;
 }
 
 }  // namespace a8
@@ -936,6 +1074,18 @@ extern "C" int a8_encode_trace(const void* workspace, int nseg, uint64_t* out) {
     }
     return A8_OK;
 }
+
+#ifdef A8_TICKET_TRACE
+extern "C" int a8_debug_ticket_trace(uint64_t* out, int64_t n) {
+    if (n > a8::kTraceTickets) n = a8::kTraceTickets;
+    cudaError_t e = cudaMemcpyFromSymbol(out, a8::g_ticket_trace, sizeof(uint64_t) * 5 * n);
+    return e == cudaSuccess ? A8_OK : fail(A8_ERR_CUDA, cudaGetErrorString(e));
+}
+extern "C" int a8_debug_flush_trace(uint64_t* out) {  // [32][512][4]
+    cudaError_t e = cudaMemcpyFromSymbol(out, a8::g_flush_trace, sizeof(a8::g_flush_trace));
+    return e == cudaSuccess ? A8_OK : fail(A8_ERR_CUDA, cudaGetErrorString(e));
+}
+#endif
 
 extern "C" size_t a8_workspace_bytes(int nseg) {
     if (nseg < 1) nseg = 1;
@@ -993,7 +1143,7 @@ extern "C" int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_de
         d[i].aligned = (reinterpret_cast<uintptr_t>(s.x) % 16) == 0;
     }
     std::vector<EncBlk> blks;
-    schedule(d, absmax, &blks);
+    schedule(d, absmax, fill_distance((int64_t)di.sms * di.enc_occ), &blks);
     const int nblk = (int)blks.size() - 1;
 
     uint8_t* ws = static_cast<uint8_t*>(workspace);
