@@ -1,0 +1,3 @@
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
+tail -15 gpurun_out/pytest_gpu.log
+bash tools/ab_encode.sh

@@ -105,6 +105,8 @@ def main():
         cases = [("mlp", [(784, 1200), (1200,), (1200, 1200), (1200,), (1200, 10), (10,)])]
     elif a.case == "single":
         cases = [("single_2^26", [(1 << 26,)])]
+    elif a.case == "big":
+        cases = [("single_2^26", [(1 << 26,)]), ("single_2^28", [(1 << 28,)]), ("single_2^30", [(1 << 30,)])]
     elif a.case == "bw":
         # torch reference kernels on 2^28 floats: read-only / write-only / copy
         x = torch.randn(1 << 28, device=dev)
