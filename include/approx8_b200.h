@@ -200,6 +200,19 @@ int a8_onebit_quantize(const void* g, int g_is_f64, double* residual, int64_t n,
 /* onebit_decode (codecs.py:342-348): out[i] = bit ? levels[0] : levels[1]. */
 int a8_onebit_decode(const uint8_t* bits, int64_t n, const float* levels, float* out, void* stream);
 
+/* Round-trip error aggregates: measure_error (errorbench.py:79-99) and the
+ * hook statistics _HookStats.record (mlp.py:146-153).  Over n elements:
+ *   d      = float32(table[codes[i]] * *scale_dev)  (codes != NULL, the
+ *            decode of codecs.py:281), else after[i] (a decoded float32 tensor)
+ *   out[0] = sum |x - d|, out[1] = sum over x != 0 of |x - d| / |x|,
+ *   out[2] = #(x != 0), all float64 (x widened exactly from float32, or
+ *            float64 when x_is_f64); accumulate = 1 adds to out[] instead.
+ * Deterministic for a given device (fixed-order reduction).  workspace:
+ * a8_error_workspace_bytes() bytes, zero-filled once (left zeroed).         */
+size_t a8_error_workspace_bytes(void);
+int a8_error_stats(const void* x, int x_is_f64, int64_t n, const uint8_t* codes, const float* scale_dev,
+                   const void* book_dev, const float* after, double* out_dev, int accumulate, void* workspace,
+                   size_t workspace_bytes, void* stream);
 /* Diagnostics: globaltimer trace of the last a8_encode on `workspace`
  * (synchronous device->host copy).  out[0..3] = kernel start ns, end ns,
  * total CTA time spent waiting for segment tables (ns), number of waits;

@@ -24,6 +24,7 @@ from .codecs import (
     parse_spec,
     roundtrip,
 )
+from .errorbench import ErrorReport, SampleSpec, measure_error, run_error_suite
 from .errors import ApproxError, ConfigError, InputError, TrainingError, UsageError
 from .exchange import (
     CompressedAllGather,
@@ -54,6 +55,7 @@ __all__ = [
     "DDPHookState",
     "DataTypeKind",
     "DataTypeSpec",
+    "ErrorReport",
     "GradientExchange",
     "HookMode",
     "HookStats",
@@ -64,6 +66,7 @@ __all__ = [
     "OneBitState",
     "QuantHookConfig",
     "QuantizedTensor",
+    "SampleSpec",
     "TrainingError",
     "UsageError",
     "a8_comm_hook",
@@ -73,10 +76,12 @@ __all__ = [
     "encode_buffer",
     "exchange",
     "make_quantizer",
+    "measure_error",
     "onebit_decode",
     "onebit_quantize",
     "parse_spec",
     "read_tensor",
     "roundtrip",
+    "run_error_suite",
     "write_tensor",
 ]

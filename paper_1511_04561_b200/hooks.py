@@ -73,23 +73,41 @@ def default_hook_spec(kind: DataTypeKind, mode: HookMode) -> DataTypeSpec:
 
 class HookStats:
     """Per (site, layer) sums of |x - q(x)| and |x - q(x)|/|x| over non-zero
-    x, accumulated on the device (mlp.py:140-164); ``summary`` syncs."""
+    x (mlp.py:140-164), accumulated on the device by the a8_error_stats
+    kernel; ``summary`` syncs."""
 
     def __init__(self) -> None:
         self._acc: dict = {}
 
-    def record(self, site: str, layer: int, before: torch.Tensor, after: torch.Tensor) -> None:
-        b = before.reshape(-1).to(torch.float64)
-        d = (b - after.reshape(-1).to(torch.float64)).abs()
-        nz = b != 0
-        rel = torch.where(nz, d / b.abs().clamp_min(torch.finfo(torch.float64).tiny), torch.zeros_like(d))
-        row = torch.stack([d.sum(), rel.sum(), nz.sum().to(torch.float64)])
+    def _row(self, site: str, layer: int, n: int, dev: torch.device) -> torch.Tensor:
         key = (site, layer)
-        if key in self._acc:
-            acc, n = self._acc[key]
-            self._acc[key] = (acc + row, n + b.numel())
-        else:
-            self._acc[key] = (row, b.numel())
+        if key not in self._acc:
+            self._acc[key] = [torch.zeros(3, dtype=torch.float64, device=dev), 0]
+        self._acc[key][1] += n
+        return self._acc[key][0]
+
+    @staticmethod
+    def _flat(x: torch.Tensor) -> torch.Tensor:
+        x = x.reshape(-1)
+        if x.dtype not in (torch.float32, torch.float64):
+            x = x.to(torch.float32)  # narrower floats widen exactly
+        return x.contiguous()
+
+    def record(self, site: str, layer: int, before: torch.Tensor, after: torch.Tensor) -> None:
+        """mlp.py:146-153 with ``after`` a decoded tensor (float32 values)."""
+        from .errorbench import error_sums
+
+        b = self._flat(before)
+        a = after.reshape(-1).to(device=b.device, dtype=torch.float32).contiguous()
+        error_sums(b, self._row(site, layer, b.numel(), b.device), after=a, accumulate=True)
+
+    def record_codes(self, site: str, layer: int, before: torch.Tensor, q, codebook) -> None:
+        """Same sums from the 8-bit codes (decode fused into the reduction)."""
+        from .errorbench import error_sums
+
+        b = self._flat(before)
+        error_sums(b, self._row(site, layer, b.numel(), b.device), codes=q.codes, scale=q.scale_tensor,
+                   codebook=codebook, accumulate=True)
 
     def summary(self) -> dict:
         out: dict = {}
@@ -109,10 +127,10 @@ def make_quantizer(spec: DataTypeSpec, stats: Optional[HookStats] = None, site: 
 
     def quantize(x: torch.Tensor, layer: int) -> torch.Tensor:
         q = encode_buffer(x, cb, sync=False)
-        y = decode_buffer(q, cb).to(x.dtype)
+        y = decode_buffer(q, cb)
         if stats is not None:
-            stats.record(site, layer, x, y)
-        return y
+            stats.record_codes(site, layer, q._keepalive, q, cb)
+        return y.to(x.dtype)
 
     return quantize
 
