@@ -206,7 +206,10 @@ def run_b200(args, nranks, rank, local_rank):
     pinned = [torch.from_numpy(g).pin_memory() for g in host]
     grads = [p.to(dev) for p in pinned]
     outs = [torch.empty_like(g) for g in grads]
-    ex = A.GradientExchange(spec, mode=args.mode, op="avg", check="deferred")
+    # one rank: the step is captured in a CUDA graph (one launch per step, no
+    # host work between the kernels); N > 1 runs eagerly (NCCL in the step)
+    graphed = nranks == 1 and not args.eager
+    ex = A.GradientExchange(spec, mode=args.mode, op="avg", check="deferred", graph=graphed)
 
     def barrier():
         if nranks > 1:
@@ -224,19 +227,23 @@ def run_b200(args, nranks, rank, local_rank):
     ev_log = []
 
     class TimedCodec:
-        def encode(self, *a, **k):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        """CUDA events on the launching stream around every codec call.  The
+        events are `external` so that, in graph mode, they are captured into
+        the graph and re-recorded by every replay."""
+
+        def _timed(self, name, fn, *a, **k):
+            e0 = torch.cuda.Event(enable_timing=True, external=graphed)
+            e1 = torch.cuda.Event(enable_timing=True, external=graphed)
             e0.record()
-            codec.encode(*a, **k)
+            fn(*a, **k)
             e1.record()
-            ev_log.append(("encode", e0, e1))
+            ev_log.append((name, e0, e1))
+
+        def encode(self, *a, **k):
+            self._timed("encode", codec.encode, *a, **k)
 
         def decode(self, *a, **k):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            codec.decode(*a, **k)
-            e1.record()
-            ev_log.append(("decode", e0, e1))
+            self._timed("decode", codec.decode, *a, **k)
 
     ex.codec = TimedCodec()
 
@@ -244,6 +251,9 @@ def run_b200(args, nranks, rank, local_rank):
         ex(grads, out=outs)
     ex.synchronize()
     torch.cuda.synchronize()
+    # graph mode: the events of the captured step (the codec calls of the
+    # capture are the last ones logged; replays log nothing)
+    captured = list(ev_log[-2:]) if graphed else []
     ev_log.clear()
 
     def soak(seconds):
@@ -275,8 +285,17 @@ def run_b200(args, nranks, rank, local_rank):
     ms = max_over_ranks(ms)
     value = nranks * 4.0 * n / (ms * 1e-3) / 1e9
 
-    # per-kernel durations inside the timed region
+    # per-kernel durations: eager mode, the events logged inside the timed
+    # region; graph mode, the captured events read after each of `steps`
+    # further replays (the replay that re-records them runs the same graph)
     kt: dict = {}
+    if graphed:
+        for _ in range(args.steps):
+            ex(grads, out=outs)
+            torch.cuda.synchronize()
+            for name, e0, e1 in captured:
+                kt.setdefault(name, []).append(e0.elapsed_time(e1))
+        ex.synchronize()
     for name, e0, e1 in ev_log:
         kt.setdefault(name, []).append(e0.elapsed_time(e1))
     kms = {k: float(np.mean(v)) * len(v) / args.steps for k, v in kt.items()}  # ms per step
@@ -393,7 +412,8 @@ def run_b200(args, nranks, rank, local_rank):
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": nranks, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": workload_config(args, nranks), "roofline": roofline, "cpu_baseline": cpu,
+            "config": {**workload_config(args, nranks), "cuda_graph": graphed},
+            "roofline": roofline, "cpu_baseline": cpu,
             "e2e": e2e, "clocks": clk.summary(), "gpu_launches": int(sum(launches.values())),
             "gpu_launches_per_step": {k: v / args.steps for k, v in launches.items()},
             "nccl_fp32_allreduce": nccl,
@@ -411,6 +431,7 @@ def main():
     ap.add_argument("--cpu-elems", type=int, default=1 << 23)
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--eager", action="store_true", help="no CUDA graph for the N=1 step")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

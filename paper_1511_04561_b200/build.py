@@ -41,19 +41,24 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False, ticket_trace: bool = False) -> Path:
+def build(force: bool = False, verbose: bool = False, ticket_trace: bool = False, defines=(), variant: str = "") -> Path:
     """``ticket_trace``: a debug build with per-ticket timestamps into
-    ``_lib_trace/`` (load it with A8_LIB=<path>); never the product library."""
-    lib = (PKG / "_lib_trace" / LIB.name) if ticket_trace else LIB
-    if not force and not ticket_trace and not _stale():
+    ``_lib_trace/`` (load it with A8_LIB=<path>); never the product library.
+    ``defines`` + ``variant``: a tuning build (-D flags) into ``_lib_var/<variant>/``
+    for A/B measurements; never the product library."""
+    if variant:
+        lib = PKG / "_lib_var" / variant / LIB.name
+    else:
+        lib = (PKG / "_lib_trace" / LIB.name) if ticket_trace else LIB
+    if not force and not ticket_trace and not variant and not _stale():
         return LIB
-    lib.parent.mkdir(exist_ok=True)
+    lib.parent.mkdir(parents=True, exist_ok=True)
     tmp = lib.with_suffix(".so.tmp")
     cmd = [
         nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo",
         "-Xcompiler", "-fPIC,-O3", "-shared", "-cudart", "static",
         "-Xptxas", "-v" if verbose else "-O3",
-        f"-I{INCLUDE}", f"-I{CSRC}", *(["-DA8_TICKET_TRACE"] if ticket_trace else []),
+        f"-I{INCLUDE}", f"-I{CSRC}", *(["-DA8_TICKET_TRACE"] if ticket_trace else []), *[f"-D{d}" for d in defines],
         *[str(CSRC / s) for s in SOURCES],
         "-o", str(tmp),
     ]
@@ -67,4 +72,7 @@ def build(force: bool = False, verbose: bool = False, ticket_trace: bool = False
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, ticket_trace="--ticket-trace" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    var = next((a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--variant=")), "")
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, ticket_trace="--ticket-trace" in sys.argv,
+                defines=defs, variant=var))

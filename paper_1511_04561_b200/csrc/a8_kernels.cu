@@ -32,7 +32,10 @@ extern thread_local std::string g_last_error;
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = kConsumerWarps * 32;  // threads doing reduce / encode
 constexpr int kEncThreads = kConsumers + 32;     // + one producer warp
-constexpr int kStages = 4;                       // bulk-copy ring depth per CTA
+#ifndef A8_STAGES
+#define A8_STAGES 4
+#endif
+constexpr int kStages = A8_STAGES;               // bulk-copy ring depth per CTA
 constexpr int kChunk = 4096;                     // elements per stage (16 KB)
 constexpr int kBarC = 1;                         // named barrier of the consumer warps
 constexpr size_t kEncDynSmem = (size_t)kStages * kChunk * sizeof(float);
@@ -745,7 +748,10 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
 // rank in shared memory, replicated 4 times.  Each thread decodes 4 groups
 // of 4 elements of a chunk with all code words loaded before any store.
 
-constexpr int kDecGroups = 4;
+#ifndef A8_DEC_GROUPS
+#define A8_DEC_GROUPS 4
+#endif
+constexpr int kDecGroups = A8_DEC_GROUPS;
 constexpr int kDecChunkD = kDecThreads * kDecGroups * 4;  // 4096 elements
 
 // 4 copies: 1-4 copies measured equal; 8 and 32 (lane-private) were slower

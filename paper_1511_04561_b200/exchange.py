@@ -32,6 +32,7 @@ independent of it, which is what the CPU gloo tests exercise.
 
 from __future__ import annotations
 
+import collections
 import ctypes as C
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
@@ -215,12 +216,18 @@ class GradientExchange:
     ``check``  "deferred": the non-finite status of call k is checked at call
                k+1 (or ``synchronize()``) without stalling the stream;
                "sync": checked before returning; "none".
+    ``graph``  capture the step (encode, decode, status copy) in a CUDA graph
+               per (shapes, input/output addresses) and replay it: one launch
+               per step and no host work between the kernels.  Applies on a
+               single rank (N = 1); collectives run eagerly.  With deferred
+               checks a non-finite status is reported at the next check of a
+               later call (graph replays share one host status word).
     Every rank must call it with the same tensor shapes in the same order.
     """
 
     def __init__(self, spec: DataTypeSpec, group=None, mode: str = "allgather", op: str = "avg",
                  check: str = "deferred", codec: Optional[SegmentCodec] = None, comm=None,
-                 chunk_elems: int = 8 << 20, max_chunks: int = 8):
+                 chunk_elems: int = 8 << 20, max_chunks: int = 8, graph: bool = False):
         if mode not in MODES:
             raise UsageError(f"mode must be one of {MODES}, got {mode!r}")
         if op not in OPS:
@@ -237,10 +244,16 @@ class GradientExchange:
         self.comm = comm or TorchDistComm(group)
         self._plans: dict = {}
         self._bufs: dict = {}
-        self._pending = None  # (event or None, host status tensor)
+        self._pending = collections.deque()  # (event or None, host status word, call)
+        self._ring = None
+        self._slot = 0
         self.calls = 0
         self.chunk_elems = int(chunk_elems)  # allgather: elements per pipelined chunk
         self.max_chunks = int(max_chunks)
+        self.graph = bool(graph)
+        self._graphs: dict = {}
+        self._gstream = None
+        self._capturing = None  # pinned host status word while capturing
 
     # -- distributed context
     def _world(self):
@@ -250,42 +263,69 @@ class GradientExchange:
         key = (name, device)
         b = self._bufs.get(key)
         if b is None or b.numel() < nbytes:
+            if self._capturing is not None:
+                raise UsageError("exchange buffer grew during graph capture")
             b = torch.zeros(nbytes, dtype=dtype, device=device)
             self._bufs[key] = b
+            self._graphs.clear()  # captured graphs hold the old buffer's address
         return b[:nbytes]
 
     # -- status handling
+    #
+    # The final decode writes the collective status word (OR of every rank's
+    # encoder status) straight into pinned host memory (UVA: the kernel
+    # stores to the host-mapped word; no device->host copy in the stream).
+    # Eager calls take a fresh word from a ring of _RING slots, so every
+    # call's status is checked; graph mode bakes one word into each graph.
+
+    _RING = 64
+
+    def _status_word(self, dev) -> torch.Tensor:
+        """Where this call's final decode writes its status (uint8[4] view)."""
+        if self._capturing is not None:
+            return self._capturing
+        if self._ring is None:
+            pin = dev.type == "cuda"
+            self._ring = torch.zeros(self._RING, dtype=torch.int32, pin_memory=pin)
+        w = self._ring[self._slot % self._RING:self._slot % self._RING + 1]
+        self._slot += 1
+        if len(self._pending) >= self._RING - 1:  # the oldest unchecked word is about to be reused
+            self._check_one(block=True)
+        return w.view(torch.uint8)
+
     def _collect_status(self, word: torch.Tensor):
-        if self.check == "none":
+        if self._capturing is not None or self.check == "none":
             return
-        if word.is_cuda:
-            host = torch.empty(1, dtype=torch.int32, pin_memory=True)
-            host.copy_(word.view(torch.int32)[:1], non_blocking=True)
+        ev = None
+        if word.device.type == "cpu" and torch.cuda.is_available() and word.is_pinned():
             ev = torch.cuda.Event()
             ev.record()
-        else:
-            host, ev = word.view(torch.int32)[:1].clone(), None
-        self._pending = (ev, host, self.calls)
+        self._pending.append((ev, word.view(torch.int32), self.calls))
         if self.check == "sync":
             self.synchronize()
 
-    def synchronize(self) -> None:
-        """Wait for the last exchange's status and raise InputError if any
-        rank's input held NaN/Inf (codecs.py:251-252)."""
-        if self._pending is None:
-            return
-        ev, host, call = self._pending
-        self._pending = None
+    def _check_one(self, block: bool) -> bool:
+        """Check the oldest pending status; False if it is not ready (non-blocking)."""
+        ev, word, call = self._pending[0]
         if ev is not None:
+            if not block and not ev.query():
+                return False
             ev.synchronize()
-        if int(host[0]) & N.A8_STATUS_NONFINITE:
+        self._pending.popleft()
+        if int(word[0]) & N.A8_STATUS_NONFINITE:
+            self._pending.clear()
             raise InputError(f"exchange call {call}: cannot encode non-finite values (NaN or Inf present)")
+        return True
+
+    def synchronize(self) -> None:
+        """Wait for every pending exchange status and raise InputError if any
+        rank's input held NaN/Inf (codecs.py:251-252)."""
+        while self._pending:
+            self._check_one(block=True)
 
     def _poll(self) -> None:
-        if self._pending is not None:
-            ev = self._pending[0]
-            if ev is None or ev.query():
-                self.synchronize()
+        while self._pending and self._check_one(block=False):
+            pass
 
     # -- main entry
     def __call__(self, tensors: Sequence[torch.Tensor], out: Optional[Sequence[torch.Tensor]] = None):
@@ -304,12 +344,54 @@ class GradientExchange:
         plan = self._plans.get(key)
         if plan is None:
             plan = self._plans[key] = make_plan(sizes, nranks)
+        # graphs need launch-inline plans (<= 32 tensors: no host->device plan upload)
+        if self.graph and nranks == 1 and dev.type == "cuda" and plan.nseg <= 32:
+            self._replay(tensors, outs, plan, nranks, rank, dev)
+        else:
+            self._step(tensors, outs, plan, nranks, rank, dev)
+        self.calls += 1
+        return outs
+
+    def _step(self, tensors, outs, plan, nranks, rank, dev):
         if self.mode == "allgather" or nranks == 1:
             self._allgather(tensors, outs, plan, nranks, rank, dev)
         else:
             self._two_round(tensors, outs, plan, nranks, rank, dev)
-        self.calls += 1
-        return outs
+
+    def _replay(self, tensors, outs, plan, nranks, rank, dev):
+        """Graph mode: the first call with a given (shapes, addresses) runs
+        eagerly on a side stream (allocating every buffer and workspace the
+        step uses) and captures the step; later calls replay it."""
+        key = (plan.sizes, nranks, self.mode, tuple(t.data_ptr() for t in tensors),
+               tuple(o.data_ptr() for o in outs))
+        hit = self._graphs.get(key)
+        cur = torch.cuda.current_stream(dev)
+        if hit is None:
+            if self._gstream is None:
+                self._gstream = torch.cuda.Stream(dev)
+            s = self._gstream
+            s.wait_stream(cur)
+            with torch.cuda.stream(s):
+                self._step(tensors, outs, plan, nranks, rank, dev)  # this call's result
+            cur.wait_stream(s)
+            host = torch.zeros(4, dtype=torch.uint8, pin_memory=True)  # this graph's status word
+            g = torch.cuda.CUDAGraph()
+            self._capturing = host
+            try:
+                with torch.cuda.graph(g, stream=s):
+                    self._step(tensors, outs, plan, nranks, rank, dev)
+            finally:
+                self._capturing = None
+            self._graphs[key] = (g, host)
+            return
+        g, host = hit
+        g.replay()
+        if self.check != "none":
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            self._pending.append((ev, host.view(torch.int32), self.calls))
+            if self.check == "sync":
+                self.synchronize()
 
     def _chunking(self, plan: Plan, nranks: int):
         """K chunk-blocks of C elements for the pipelined all-gather (K = 1
@@ -345,7 +427,7 @@ class GradientExchange:
         mine = rank * P
         self.codec.encode(xs, plan.offs, idx, self.cb, gathered, mine, mine + C, C, BS, BS // 4, K,
                           mine + C + 4 * plan.status_slot)
-        status = self._buffer("status", 4, dev)
+        status = self._status_word(dev)
         op = 1 if self.op == "avg" else 0
         if nranks == 1:
             self.codec.decode(outs, plan.offs, idx, self.cb, gathered, 0, C, C, BS, BS // 4, P, 1, op,
@@ -406,7 +488,7 @@ class GradientExchange:
             fouts.append(outs[p.tensor].view(-1)[p.start:p.start + p.n])
             foffs.append(p.flat)
             fidx.append(p.idx)
-        status = self._buffer("status", 4, dev)
+        status = self._status_word(dev)
         self.codec.decode(fouts, foffs, fidx, self.cb, gathered, 0, L, L, B, sbs, 0, 1, 0,
                           plan.status_slot, nranks, status)
         self._collect_status(status)

@@ -150,3 +150,76 @@ def test_model_parallel_quantizer_seam(cuda):
     assert torch.equal(y, A.roundtrip(x, spec))
     s = stats.summary()["forward"][0]
     assert s[0] > 0 and 0 < s[1] < 5
+
+
+def test_graph_mode_replays_match_roundtrip(cuda):
+    """graph=True: first call eager + capture, later calls replay; every call
+    equals the per-tensor round trip of that call's data (buffers reused)."""
+    spec = A.DataTypeSpec("dynamic-tree", "absmax")
+    ex = A.GradientExchange(spec, check="sync", graph=True)
+    sizes = SMALL + ALEXNET[:6]
+    ins = [torch.empty(s, device=cuda) for s in sizes]
+    outs = [torch.empty(s, device=cuda) for s in sizes]
+    for step in range(4):
+        gs = grads(0, sizes, seed=10 + step)
+        for t, g in zip(ins, gs):
+            t.copy_(torch.from_numpy(g))
+        ex(ins, out=outs)
+        for o, g in zip(outs, gs):
+            assert o.cpu().numpy().tobytes() == O.roundtrip(g, "dynamic-tree", "absmax").tobytes(), step
+    assert len(ex._graphs) == 1
+    # other output buffers -> a second graph
+    outs2 = [torch.empty_like(o) for o in outs]
+    ex(ins, out=outs2)
+    ex(ins, out=outs2)
+    assert len(ex._graphs) == 2
+    for a, b in zip(outs, outs2):
+        assert torch.equal(a, b)
+
+
+def test_graph_mode_reports_non_finite(cuda):
+    spec = A.DataTypeSpec("linear", "absmax")
+    ex = A.GradientExchange(spec, check="sync", graph=True)
+    ts = [torch.randn(1000, device=cuda), torch.randn(77, device=cuda)]
+    outs = [torch.empty_like(t) for t in ts]
+    ex(ts, out=outs)
+    ex(ts, out=outs)  # replay
+    ts[1][5] = float("inf")
+    with pytest.raises(A.InputError):
+        ex(ts, out=outs)
+    ts[1][5] = 0.0
+    ex(ts, out=outs)  # clean again
+    assert torch.isfinite(outs[1]).all()
+
+
+def test_graph_mode_many_tensors_runs_eagerly(cuda):
+    """> 32 tensors: the launch plan goes through device memory, no capture."""
+    spec = A.DataTypeSpec("dynamic-tree", "absmax")
+    ex = A.GradientExchange(spec, check="sync", graph=True)
+    sizes = [(int(n),) for n in np.random.default_rng(9).integers(1, 500, size=40)]
+    gs = grads(0, sizes, seed=3)
+    ts = [torch.from_numpy(g).to(cuda) for g in gs]
+    ex(ts)
+    assert not ex._graphs
+    for t, g in zip(ts, gs):
+        assert t.cpu().numpy().tobytes() == O.roundtrip(g, "dynamic-tree", "absmax").tobytes()
+
+
+def test_deferred_checks_every_call(cuda):
+    """check="deferred": a non-finite input in call k is reported even when
+    later calls were issued before it was checked (status ring, one
+    host-mapped word per call)."""
+    spec = A.DataTypeSpec("dynamic-tree", "absmax")
+    ex = A.GradientExchange(spec, check="deferred")
+    good = [torch.randn(5000, device=cuda), torch.randn(33, device=cuda)]
+    bad = [good[0].clone(), good[1].clone()]
+    bad[0][123] = float("nan")
+    outs = [torch.empty_like(t) for t in good]
+    ex(good, out=outs)
+    ex(bad, out=outs)
+    with pytest.raises(A.InputError, match="call 1"):
+        for _ in range(5):  # raised by a later call's poll, or at the latest by synchronize
+            ex(good, out=outs)
+        ex.synchronize()
+    ex(good, out=outs)
+    ex.synchronize()  # clean again

@@ -36,11 +36,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--case", default="alexnet")
     ap.add_argument("--out", default="gpurun_out/ticket_trace.json")
+    ap.add_argument("--spec", default="dynamic-tree/absmax")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     sizes = ALEXNET if a.case == "alexnet" else [(1 << 26,)]
     prof_codec.TRACE = True  # also read the per-segment build stamps
-    n, res = run(sizes, A.parse_spec("dynamic-tree/absmax"), 5, dev)  # last call = the traced one
+    n, res = run(sizes, A.parse_spec(a.spec), 5, dev)  # last call = the traced one
     torch.cuda.synchronize()
     ntk = 1 << 17
     buf = (C.c_uint64 * (5 * ntk))()
