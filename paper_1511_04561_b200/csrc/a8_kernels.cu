@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <deque>
 #include <mutex>
 #include <string>
@@ -742,6 +743,250 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
 }
 
 // ---------------------------------------------------------------------------
+// K1+K2+K3 resident: absmax calls whose data fits in the shared memory of the
+// whole GPU (148 SMs x ~200 KB ~ 30 MB: small models, DDP-sized buckets).
+//
+// One CTA per SM, cooperative launch.  Each CTA owns one contiguous slice of
+// the concatenated elements and streams it global->shared ONCE with bulk
+// async copies (the 16-byte aligned middle of every segment piece; scalar
+// loads for the ragged ends).  Per-piece max-abs from shared memory ->
+// atomicMax per segment -> one grid barrier -> every CTA builds the
+// thresholds and bucket table of the segments it holds and encodes them
+// from shared memory.  DRAM traffic is the 5 B/element floor (4 read + 1
+// written) instead of 9, and there is one global synchronisation instead of
+// per-segment ticket dependencies.
+
+#ifdef A8_TICKET_TRACE
+__device__ unsigned long long g_res_trace[2][8];  // CTA 0 and the last CTA: phase stamps (debug builds)
+#define RES_STAMP(i)                                                                       \
+    do {                                                                                   \
+        if (tid == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))                  \
+            g_res_trace[blockIdx.x == 0 ? 0 : 1][i] = gtime();                             \
+    } while (0)
+#else
+#define RES_STAMP(i) \
+    do {             \
+    } while (0)
+#endif
+
+// The 127 decision thresholds of one scale with 4 threads per threshold
+// (threads 0..511): the 8 float32 patterns around the rounded midpoint are
+// tested in parallel and the first one resolving upward is T_i -- the same
+// result as threshold() (the reference decision is monotone), in one
+// predicate evaluation instead of a sequential walk.  If the transition is
+// outside the window, lane 0 of the group falls back to threshold().
+__device__ void threshold_parallel(float scale, const a8_book_t* book, uint32_t* sT, int tid) {
+    const int i = tid >> 2, j = tid & 3;
+    uint32_t t = kInfBits;
+    bool fallback = false;
+    const bool active = i < 128 && scale_ok(scale) && i + 1 < book->ndistinct;
+    double s = scale, vlo = 0.0, vhi = 0.0;
+    uint32_t g = 0;
+    if (active) {
+        vlo = book->values[i];
+        vhi = book->values[i + 1];
+        const double m = 0.5 * (vlo + vhi) * s;
+        g = m < 3.4028234663852886e38 ? f32_bits((float)m) : kInfBits;
+        fallback = g < 8u || g >= kInfBits - 8u;
+    }
+    bool p0 = false, p1 = false;
+    if (active && !fallback) {
+        const uint32_t c0 = g - 3u + 2u * (uint32_t)j;
+        p0 = picks_upper(c0, s, vlo, vhi);
+        p1 = picks_upper(c0 + 1u, s, vlo, vhi);
+    }
+    // the group's 8 predicates, candidate order g-3 .. g+4
+    const unsigned int b = __ballot_sync(0xffffffffu, p0) , c = __ballot_sync(0xffffffffu, p1);
+    const int base = (tid & 31) & ~3;
+    unsigned int bits = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) bits |= (((b >> (base + q)) & 1u) << (2 * q)) | (((c >> (base + q)) & 1u) << (2 * q + 1));
+    if (active && !fallback) {
+        if (bits == 0u || bits == 0xffu)
+            fallback = true;  // transition not inside the window
+        else
+            t = g - 3u + (uint32_t)__popc(~bits & 0xffu);  // predicates are false...false true...true
+    }
+    if (j == 0 && i < 128) sT[i] = (active && fallback) ? threshold(s, vlo, vhi) : t;
+}
+
+constexpr int kRThreads = 512;
+constexpr size_t kRDynSmem = 200u * 1024u;
+constexpr int kRCap = (int)(kRDynSmem / sizeof(float));  // floats per CTA
+
+struct RSeg {
+    const float* x;
+    int64_t n;
+    int64_t flat_off;
+    int32_t scale_idx;
+    int32_t aligned;  // x is 16-byte aligned
+    int32_t cta0;     // first CTA of the segment; its CTAs are [cta0, next segment's cta0)
+    int32_t pad;
+};
+
+struct RParams {
+    a8_layout_t lay;
+    const a8_book_t* book;
+    WsHead* head;
+    SegCtl* ctl;
+    const unsigned int* status_in;
+    unsigned int* status_out;
+    int nseg;
+    int pad;
+    RSeg segs[kInlineSegs + 1];  // segs[nseg].cta0 = grid
+};
+
+__global__ void __launch_bounds__(kRThreads, 1) resident_encode_kernel(const __grid_constant__ RParams p) {
+    extern __shared__ __align__(128) float sData[];
+    __shared__ __align__(16) uint32_t sE[kLutMax];
+    __shared__ uint32_t sT[128];
+    __shared__ uint8_t sCanon[128];
+    __shared__ unsigned int sWarp[kRThreads / 32];
+    __shared__ int sFinal;
+    __shared__ unsigned int sAmax;
+    __shared__ __align__(8) uint64_t sBar;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+
+    // this CTA's piece: part q of c of segment s, elements [lo, hi); shared
+    // offset off = lo (mod 4) keeps 16-byte groups aligned in both spaces
+    int s = 0;
+    while (s + 1 < p.nseg && p.segs[s + 1].cta0 <= (int)blockIdx.x) ++s;
+    const RSeg& g = p.segs[s];
+    const int c = p.segs[s + 1].cta0 - g.cta0, q = (int)blockIdx.x - g.cta0;
+    const int64_t lo = g.n * q / c, hi = g.n * (q + 1) / c;
+    const int off = (int)(lo & 3);
+    float* const dst = sData + off - lo;  // dst[i], i in [lo, hi)
+    const int64_t a0 = min(hi, (int64_t)((lo + 3) & ~3ll)), a1 = max(a0, (int64_t)(hi & ~3ll));
+    if (tid == 0) {
+        mbar_init(&sBar, 1);
+        mbar_fence_init();
+    }
+    if (tid < 128) sCanon[tid] = p.book->codes[tid];
+    RES_STAMP(0);
+    __syncthreads();
+
+    // ---- phase 1: global -> shared, once; max |x| of the piece ----------------
+    if (tid == 0) {
+        const bool bulk = g.aligned && a1 > a0;
+        mbar_arrive_expect_tx(&sBar, bulk ? (uint32_t)(a1 - a0) * 4u : 0u);
+        if (bulk) bulk_g2s(dst + a0, g.x + a0, (uint32_t)(a1 - a0) * 4u, &sBar, policy_evict_first());
+    }
+    if (g.aligned) {  // ragged ends by plain loads
+        if (tid < a0 - lo) dst[lo + tid] = g.x[lo + tid];
+        if (tid < hi - a1) dst[a1 + tid] = g.x[a1 + tid];
+    } else {
+        for (int64_t i = lo + tid; i < hi; i += kRThreads) dst[i] = g.x[i];
+    }
+    mbar_wait(&sBar, 0);
+    __syncthreads();
+    RES_STAMP(1);
+    {
+        unsigned int mx = 0;  // bits * 2 (drops the sign)
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(dst);
+        for (int64_t i = a0 + 4 * (int64_t)tid; i < a1; i += 4 * kRThreads) {
+            const uint4 v = *reinterpret_cast<const uint4*>(src + i);
+            mx = __vimax3_u32(mx, v.x * 2u, v.y * 2u);
+            mx = __vimax3_u32(mx, v.z * 2u, v.w * 2u);
+        }
+        if (tid < a0 - lo) mx = max(mx, src[lo + tid] * 2u);
+        if (tid < hi - a1) mx = max(mx, src[a1 + tid] * 2u);
+        mx = __reduce_max_sync(0xffffffffu, mx);
+        if (lane == 0) sWarp[w] = mx;
+        __syncthreads();
+        if (tid == 0) {
+            unsigned int m = 0;
+            for (int i = 0; i < kRThreads / 32; ++i) m = max(m, sWarp[i]);
+            if (m) atomicMax(&p.ctl[s].amax, m >> 1);
+        }
+    }
+
+    // ---- phase 2: grid barrier (cooperative launch: all CTAs are resident) ----
+    RES_STAMP(2);
+    if (tid == 0) {
+        __threadfence();
+        atomicAdd(&p.head->ticket, 1u);
+        unsigned int ns = 32;
+        while (ld_acquire(&p.head->ticket) < gridDim.x) {
+            __nanosleep(ns);
+            ns = min(ns * 2u, 256u);
+        }
+        sAmax = __ldcg(&p.ctl[s].amax);
+    }
+    __syncthreads();
+    RES_STAMP(3);
+
+    // ---- phase 3: this CTA's own table (no cross-CTA dependency), encode ------
+    const unsigned int amax = sAmax;
+    const float scale = amax == 0u ? 1.0f : __uint_as_float(amax);
+    threshold_parallel(scale, p.book, sT, tid);
+    __syncthreads();  // sT[i] is written by thread 4i; the count below reads sT[tid]
+    const int F = __syncthreads_count(tid < 127 && sT[tid] < kInfBits);
+    int32_t kb;
+    uint32_t len;
+    lut_geometry(sT, (uint32_t)F, &kb, &len);
+    bool ok = len <= (uint32_t)kLutMax;
+    if (ok && tid < kConsumers) ok = fill_lut_local(sT, (uint32_t)F, sCanon, kb, sE, sWarp, tid);
+    const int valid = __syncthreads_and(ok);
+    RES_STAMP(4);
+    if (q == 0) {  // the segment's first CTA publishes its scale
+        if (tid < p.lay.scale_reps) p.lay.scales[tid * p.lay.scale_block_stride + g.scale_idx] = scale;
+        if (tid == 0 && amax >= kInfBits) atomicOr(&p.head->status, A8_STATUS_NONFINITE);
+    }
+    if (blockIdx.x == 0) {  // empty segments own no CTA: scale of an empty buffer (codecs.py:257-258)
+        for (int e = 0; e < p.nseg; ++e)
+            if (p.segs[e].n == 0 && tid < p.lay.scale_reps)
+                p.lay.scales[tid * p.lay.scale_block_stride + p.segs[e].scale_idx] = 1.0f;
+    }
+    const int64_t L = p.lay.block_len;
+    const int64_t gap = p.lay.block_stride - p.lay.block_len;
+    if (hi > lo) {
+        const int64_t f_lo = g.flat_off + lo, f_hi = g.flat_off + hi - 1;
+        const int32_t kmax = kb + (int32_t)len - 1;
+        if (valid && (f_lo / L) == (f_hi / L)) {
+            uint8_t* cb = p.lay.codes + (f_lo / L) * gap + g.flat_off;  // code of element i at cb[i]
+            const uint32_t* eb = sE - kb;
+            for (int64_t i = a0 + 4 * (int64_t)tid; i < a1; i += 4 * kRThreads) {
+                const uint4 v = *reinterpret_cast<const uint4*>(dst + i);
+                *reinterpret_cast<uint32_t*>(cb + i) = encode4_lut(v, eb, kb, kmax);
+            }
+            if (tid < a0 - lo) cb[lo + tid] = (uint8_t)encode_lut(__float_as_uint(dst[lo + tid]), sE, kb, (int32_t)len - 1);
+            if (tid < hi - a1) cb[a1 + tid] = (uint8_t)encode_lut(__float_as_uint(dst[a1 + tid]), sE, kb, (int32_t)len - 1);
+        } else {
+            for (int64_t i = lo + tid; i < hi; i += kRThreads) {
+                const uint32_t b = __float_as_uint(dst[i]);
+                const uint32_t cc = valid ? encode_lut(b, sE, kb, (int32_t)len - 1) : encode_search(b, sT, sCanon);
+                const int64_t f = g.flat_off + i;
+                p.lay.codes[f + (f / L) * gap] = (uint8_t)cc;
+            }
+        }
+    }
+
+    // ---- phase 4: last CTA out publishes the status and re-zeroes the workspace ----
+    __syncthreads();
+    RES_STAMP(5);
+    if (tid == 0) {
+        __threadfence();
+        sFinal = atomicAdd(&p.head->ctas_done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (sFinal) {
+        __threadfence();
+        for (int i = tid; i < p.nseg; i += kRThreads) p.ctl[i].amax = 0u;
+        if (tid < p.lay.scale_reps) {
+            const unsigned int stt = atomicAdd(&p.head->status, 0u) | (p.status_in ? *p.status_in : 0u);
+            p.status_out[(int64_t)tid * p.lay.scale_block_stride] = stt;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            p.head->ticket = 0u;
+            p.head->ctas_done = 0u;
+            p.head->status = 0u;
+        }
+        __threadfence();
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K4/K5: decode (+ rank-ordered sum, + 1/N average).
 //
 // Per segment, each CTA keeps pre-scaled tables fl(table[c] * s_r) for every
@@ -889,6 +1134,7 @@ struct DevInfo {
     int sms = 0;
     int enc_occ = 0;
     int dec_occ = 0;
+    int res_occ = 0;  // resident encode: CTAs per SM (1, or 0 if it cannot run)
 };
 
 static std::mutex g_mu;
@@ -911,6 +1157,10 @@ static int dev_info(int device, DevInfo* out) {
         if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
         const size_t dsm = dec_smem(1);
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.dec_occ, decode_kernel, kDecThreads, dsm);
+        if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
+        e = cudaFuncSetAttribute(resident_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRDynSmem);
+        if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.res_occ, resident_encode_kernel, kRThreads, kRDynSmem);
         if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
         d.enc_occ = std::max(1, d.enc_occ);
         d.dec_occ = std::max(1, d.dec_occ);
@@ -1087,6 +1337,10 @@ extern "C" int a8_debug_ticket_trace(uint64_t* out, int64_t n) {
     cudaError_t e = cudaMemcpyFromSymbol(out, a8::g_ticket_trace, sizeof(uint64_t) * 5 * n);
     return e == cudaSuccess ? A8_OK : fail(A8_ERR_CUDA, cudaGetErrorString(e));
 }
+extern "C" int a8_debug_res_trace(uint64_t* out) {  // [2][8]
+    cudaError_t e = cudaMemcpyFromSymbol(out, a8::g_res_trace, sizeof(a8::g_res_trace));
+    return e == cudaSuccess ? A8_OK : fail(A8_ERR_CUDA, cudaGetErrorString(e));
+}
 extern "C" int a8_debug_flush_trace(uint64_t* out) {  // [32][512][4]
     cudaError_t e = cudaMemcpyFromSymbol(out, a8::g_flush_trace, sizeof(a8::g_flush_trace));
     return e == cudaSuccess ? A8_OK : fail(A8_ERR_CUDA, cudaGetErrorString(e));
@@ -1108,6 +1362,77 @@ extern "C" int a8_device_info(int device, int* num_sms, int* enc_ctas_per_sm, in
     return A8_OK;
 }
 
+// Resident encode (absmax calls that fit in shared memory).  A8_RESIDENT=0
+// disables it (A/B measurements).
+static bool resident_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("A8_RESIDENT");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// Launches the resident kernel if the call fits; *done = false otherwise.
+// Every non-empty segment gets its own CTAs (at least enough for its data to
+// fit, then a share of the remaining SMs proportional to its size), so each
+// CTA holds one piece of one segment and builds one table.
+static int encode_resident(const a8_enc_seg_t* segs, int nseg, const void* book_dev, const a8_layout_t& layout,
+                           void* workspace, const uint32_t* status_in, uint32_t* status_out, const DevInfo& di,
+                           cudaStream_t st, bool* done) {
+    *done = false;
+    if (!resident_enabled() || di.res_occ < 1 || nseg > kInlineSegs) return A8_OK;
+    const int64_t per = kRCap - 4;  // elements per CTA (+ up to 3 of alignment offset)
+    int64_t total = 0, need = 0;
+    std::vector<int64_t> c(nseg, 0);
+    for (int i = 0; i < nseg; ++i) {
+        total += segs[i].n;
+        c[i] = (segs[i].n + per - 1) / per;
+        need += c[i];
+    }
+    if (total == 0 || need > di.sms) return A8_OK;
+    // spread the rest of the SMs (about 2048 elements per CTA at least)
+    const int64_t target = std::min<int64_t>(di.sms, std::max<int64_t>(need, (total + 2047) / 2048));
+    int64_t extra = target - need;
+    for (int i = 0; i < nseg && extra > 0; ++i) {
+        const int64_t add = std::min<int64_t>(extra * segs[i].n / total, std::max<int64_t>(0, segs[i].n - c[i]));
+        c[i] += add;
+    }
+    RParams p;
+    memset(&p, 0, sizeof(p));
+    p.lay = layout;
+    p.book = static_cast<const a8_book_t*>(book_dev);
+    uint8_t* ws = static_cast<uint8_t*>(workspace);
+    p.head = reinterpret_cast<WsHead*>(ws);
+    p.ctl = reinterpret_cast<SegCtl*>(ws + ctl_off());
+    p.status_in = status_in;
+    p.status_out = status_out;
+    p.nseg = nseg;
+    int64_t grid = 0;
+    for (int i = 0; i < nseg; ++i) {
+        p.segs[i].x = segs[i].x;
+        p.segs[i].n = segs[i].n;
+        p.segs[i].flat_off = segs[i].flat_off;
+        p.segs[i].scale_idx = segs[i].scale_idx;
+        p.segs[i].aligned = (reinterpret_cast<uintptr_t>(segs[i].x) % 16) == 0;
+        p.segs[i].cta0 = (int32_t)grid;
+        grid += c[i];
+    }
+    p.segs[nseg].cta0 = (int32_t)grid;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kRThreads);
+    cfg.dynamicSmemBytes = kRDynSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;  // the grid barrier needs every CTA resident
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, resident_encode_kernel, p);
+    *done = true;
+    return cuda_check("a8_encode (resident)");
+}
+
 extern "C" int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_dev, int norm,
                          const void* static_lut_dev, a8_layout_t layout, void* workspace,
                          size_t workspace_bytes, const uint32_t* status_in, uint32_t* status_out,
@@ -1125,6 +1450,18 @@ extern "C" int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_de
     if (int rc = dev_info(device, &di)) return rc;
 
     const bool absmax = norm == A8_NORM_ABSMAX;
+    if (absmax) {
+        for (int i = 0; i < nseg; ++i) {
+            const a8_enc_seg_t& s = segs[i];
+            if (s.n < 0 || (s.n > 0 && !s.x)) return fail(A8_ERR_USAGE, "a8_encode: bad segment");
+            if (s.flat_off % 16 || s.flat_off < 0) return fail(A8_ERR_USAGE, "a8_encode: flat_off must be a multiple of 16");
+        }
+        if (ws_capacity(workspace_bytes) < nseg) return fail(A8_ERR_USAGE, "a8_encode: workspace too small for the segment count");
+        bool done = false;
+        const int rc = encode_resident(segs, nseg, book_dev, layout, workspace, status_in, status_out, di,
+                                       static_cast<cudaStream_t>(stream), &done);
+        if (rc || done) return rc;
+    }
 
     std::vector<int> order(nseg);
     for (int i = 0; i < nseg; ++i) order[i] = i;

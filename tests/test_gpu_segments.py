@@ -126,3 +126,32 @@ def test_calls_with_different_segment_counts_share_a_workspace(cuda):
                   [1], [1200, 1, 17, 300, 64, 5000, 12544]):
         xs = [(rng.normal(size=n) * 1e-2).astype(np.float32) for n in sizes]
         check(xs, spec, cuda)
+
+
+def test_resident_and_ticket_encoders_interleave(cuda):
+    """Calls that fit in shared memory take the resident single-pass kernel,
+    larger ones the ticket kernel; both share one workspace on the stream and
+    must leave it as the other expects (alternating calls, all bit-exact)."""
+    spec = A.DataTypeSpec("dynamic-tree", "absmax")
+    rng = np.random.default_rng(77)
+    small = [rng.normal(0, 0.1, size=n).astype(np.float32) for n in (3000, 1, 70001, 5)]
+    large = [rng.normal(0, 0.01, size=n).astype(np.float32) for n in (8_000_003, 4097)]
+    for xs in (small, large, small, large, small):
+        check(xs, spec, cuda)
+
+
+@pytest.mark.parametrize("sizes", [
+    [(1,)], [(3,)], [(4096,)], [(7,), (0,), (9,)], [(51195,)], [(51196,)], [(51197,)],
+    [(7_500_000,)], [(1_000_001,), (17,), (0,), (3_000_000,)],
+    [(int(n),) for n in np.random.default_rng(3).integers(0, 20000, size=32)],
+])
+def test_resident_sizes(cuda, sizes):
+    """Piece boundaries of the resident kernel: single elements, ragged ends,
+    empty segments, per-CTA capacity edges (51196 = 200 KB / 4 - 4) and the
+    largest call that still fits."""
+    spec = A.DataTypeSpec("linear", "absmax")
+    rng = np.random.default_rng(len(sizes))
+    xs = [rng.normal(0, 1.0, size=s).astype(np.float32) for s in sizes]
+    check(xs, spec, cuda)
+    if len(xs) > 1:
+        check(xs, spec, cuda, nblocks=3)  # two_round-style multi-block layout
