@@ -164,50 +164,13 @@ static size_t plan_bytes(int nseg) {
 }
 
 // ---------------------------------------------------------------------------
-// K2: thresholds for one scale, built by the consumer warps of one CTA and
-// published to global memory.  Each threshold travels as a tagged 64-bit
-// word (1 << 32 | T): a reader spins on its own word until the tag is set,
-// so the publish needs neither a fence nor a flag (one L2 round trip instead
-// of three -- under full HBM load each is 1-3 us).  Every CTA that encodes
-// the segment expands the thresholds into its own shared-memory bucket
-// table (fill_lut_local).  The last CTA of the launch clears the tags.
+// K2: the decision table of one scale.  Every CTA that encodes a segment
+// builds its own copy in shared memory once the segment's max is final: 128
+// threads evaluate the thresholds (threshold(), two predicate evaluations
+// each), then fill_lut_local expands them into the bucket table.  No table
+// travels between CTAs.
 
 __device__ __forceinline__ unsigned long long gtime();
-
-__device__ __forceinline__ unsigned long long* seg_thresholds(a8_lut_t* luts, int seg) {
-    return reinterpret_cast<unsigned long long*>(luts + seg);  // first 1 KB of the segment's table slot
-}
-
-// sV / sCanon: the codebook's distinct values and canonical codes, staged
-// in shared memory at kernel start; D = number of distinct values.
-__device__ void build_thresholds(const double* sV, int D, float scale, unsigned long long* dst, int ctid) {
-    if (ctid < 128) {
-        uint32_t t = kInfBits;
-        if (scale_ok(scale) && ctid + 1 < D) t = threshold((double)scale, sV[ctid], sV[ctid + 1]);
-        st_relaxed_u64(dst + ctid, (1ull << 32) | t);
-    }
-}
-
-// Wait for a segment's thresholds and stage them in shared memory; returns
-// (to every consumer thread) the number of finite thresholds.
-__device__ int load_thresholds(const unsigned long long* src, const unsigned long long* pre, uint32_t* sT,
-                               int ctid) {
-    uint32_t t = kInfBits;
-    if (ctid < 128) {
-        // `pre`: a bulk-copied snapshot; words not yet tagged in it are re-read
-        unsigned long long v = pre ? pre[ctid] : 0ull;
-        if (!(v >> 32)) v = ld_relaxed_u64(src + ctid);
-        unsigned int ns = 32;
-        while (!(v >> 32)) {
-            __nanosleep(ns);
-            ns = min(ns * 2u, 256u);
-            v = ld_relaxed_u64(src + ctid);
-        }
-        t = (uint32_t)v;
-        sT[ctid] = t;
-    }
-    return nbar_popc(kBarC, kConsumers, ctid < 127 && t < kInfBits);
-}
 
 // Expand thresholds into the bucket table in shared memory (kConsumers
 // threads, 16 consecutive buckets each): count thresholds per bucket with
@@ -297,7 +260,6 @@ struct StageMeta {
     int32_t simple;    // full chunk inside one block of the code layout
     int32_t last;      // the producer's next ticket is not in this run: flush after this A-chunk
     int32_t tkt;       // A8_TICKET_TRACE builds: the ticket
-    int32_t tpref;     // the stage also carries a prefetch of the segment's tagged thresholds
 };
 
 #ifdef A8_TICKET_TRACE
@@ -335,10 +297,9 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
     __shared__ __align__(8) uint64_t sFull[kStages];
     __shared__ __align__(8) uint64_t sEmpty[kStages];
     __shared__ StageMeta sMeta[kStages];
-    __shared__ __align__(16) unsigned long long sTpre[kStages][128];  // threshold prefetch per stage
     __shared__ int sHdr[4];
     __shared__ unsigned int sRed[kConsumerWarps];
-    __shared__ int sLast;
+    __shared__ unsigned int sRed2[2][kConsumerWarps];  // A-run flushes
     __shared__ int sFinal;
     // the plan, staged in shared memory when it fits: the producer reads it
     // on every ticket, and kernel-parameter / global reads cost it latency
@@ -387,7 +348,6 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
             int64_t tb = (int64_t)atomicAdd(&p.head->ticket, kTicketBatch);
             int64_t tq1 = (int64_t)atomicAdd(&p.head->ticket, kTicketBatch);
             int64_t tq2 = 0;
-            int last_e = -1;  // segment of the last E-chunk issued
             int lo = 0;       // block of the current ticket (tickets only increase)
             unsigned int g = 0;
             for (int it = 0;; ++it) {
@@ -451,17 +411,13 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                 // thresholds ride along with the chunk (one more bulk copy), so
                 // the consumers usually find them in shared memory instead of
                 // paying an L2 round trip at the segment switch
-                m.tpref = p.absmax && kind == kE && m.seg != last_e;
-                if (kind == kE) last_e = m.seg;
                 sMeta[st] = m;
-                const uint32_t tx = (uint32_t)m.bulk * 4u + (m.tpref ? 1024u : 0u);
+                const uint32_t tx = (uint32_t)m.bulk * 4u;
                 if (tx > 0) {
                     mbar_arrive_expect_tx(&sFull[st], tx);
                     if (m.bulk > 0)
                         bulk_g2s(sStage + (size_t)st * kChunk, sg.x + m.base, (uint32_t)m.bulk * 4u, &sFull[st],
                                  kind == kA ? keep : drop);
-                    if (m.tpref)
-                        bulk_g2s(sTpre[st], seg_thresholds(p.luts, m.seg), 1024u, &sFull[st], keep);
                 } else {
                     mbar_arrive(&sFull[st]);
                 }
@@ -473,6 +429,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
         const int cw = warp - 1;
         int cur = p.absmax ? -1 : -2;  // segment whose table is in shared memory (-2: static)
         int tvalid = sHdr[0], tkbase = sHdr[1], tlenm1 = sHdr[2];  // that table's geometry
+        unsigned int tamax = 0;  // that table's max |x| bits
         uint8_t* const codes_base = p.lay.codes;
         const int64_t L = p.lay.block_len;
         const int64_t gap = p.lay.block_stride - p.lay.block_len;
@@ -486,48 +443,25 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
         unsigned int amx = 0;   // per-thread max of bits(|x|) * 2
         unsigned int acnt = 0;  // A-chunks in the pending run
 
+        // A-run flush: the CTA's partial max and chunk count go out as
+        // fire-and-forget reductions (the count with release semantics, so
+        // the max is visible before it); nobody waits for a round trip here.
+        // The E side builds each segment's table locally once the count is
+        // complete (see the E switch below).
+        int fpar = 0;  // sRed2 buffer of this flush (double-buffered: no trailing barrier)
         auto flush = [&]() {
             const unsigned int wmx = __reduce_max_sync(0xffffffffu, amx) >> 1;
-            if (lane == 0) sRed[cw] = wmx;
+            if (lane == 0) sRed2[fpar][cw] = wmx;
             nbar_sync(kBarC, kConsumers);
             if (ctid == 0) {
                 unsigned int mm = 0;
 #pragma unroll
-                for (int w = 0; w < kConsumerWarps; ++w) mm = max(mm, sRed[w]);
+                for (int w = 0; w < kConsumerWarps; ++w) mm = max(mm, sRed2[fpar][w]);
                 SegCtl* c = p.ctl + aseg;
-#ifdef A8_TICKET_TRACE
-                const unsigned long long f0 = gtime();
-#endif
-                if (mm) atomicMax(&c->amax, mm);
-                // acq_rel: publishes our max before the count, and (for the
-                // last contributor) makes every other CTA's max visible
-                const unsigned int done = atom_add_acq_rel(&c->a_done, acnt) + acnt;
-                sLast = (done == (unsigned int)segs[aseg].nA);
-#ifdef A8_TICKET_TRACE
-                const unsigned long long f1 = gtime();
-#endif
-                if (sLast) sHdr[3] = (int)ld_acquire(&c->amax);
-#ifdef A8_TICKET_TRACE
-                if (aseg < 32 && blockIdx.x < 512) {
-                    g_flush_trace[aseg][blockIdx.x][0] = f0;
-                    g_flush_trace[aseg][blockIdx.x][1] = f1;
-                    g_flush_trace[aseg][blockIdx.x][2] = sLast ? gtime() : 0ull;
-                    g_flush_trace[aseg][blockIdx.x][3] = acnt;
-                }
-#endif
+                if (mm) red_max_u32(&c->amax, mm);
+                red_add_release(&c->a_done, acnt);
             }
-            nbar_sync(kBarC, kConsumers);
-            if (sLast) {
-                // K2 for this segment: scale and thresholds
-                const EncSegD& sa = segs[aseg];
-                const unsigned int amax = (unsigned int)sHdr[3];
-                const float scale = amax == 0u ? 1.0f : __uint_as_float(amax);
-                if (ctid == 0) p.ctl[aseg].t_b0 = gtime();
-                if (amax >= kInfBits && ctid == 0) atomicOr(&p.head->status, A8_STATUS_NONFINITE);
-                build_thresholds(sV, p.book->ndistinct, scale, seg_thresholds(p.luts, aseg), ctid);
-                if (ctid < p.lay.scale_reps) p.lay.scales[ctid * p.lay.scale_block_stride + sa.scale_idx] = scale;
-                if (ctid == 0) p.ctl[aseg].t_thr = p.ctl[aseg].t_fill = p.ctl[aseg].t_b1 = gtime();
-            }
+            fpar ^= 1;
             aseg = -1;
             amx = 0;
             acnt = 0;
@@ -608,15 +542,33 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
             // ---------------- E: encode the chunk ----------------------------
             if (cur != m.seg && cur != -2) {
                 nbar_sync(kBarC, kConsumers);  // everyone is done with the old table
-                const unsigned long long w0 = ctid == 0 ? gtime() : 0ull;
-                const int nf = load_thresholds(seg_thresholds(p.luts, m.seg), m.tpref ? sTpre[st] : nullptr, sT, ctid);
                 if (ctid == 0) {
-                    const unsigned long long w = gtime() - w0;
-                    if (w > 2000) {  // trace: waits longer than an L2 round trip
-                        atomicAdd(&p.head->wait_ns, w);
+                    // every A-chunk of the segment reduced -> its max is final
+                    const SegCtl* c = p.ctl + m.seg;
+                    const unsigned int nA = (unsigned int)segs[m.seg].nA;
+                    if (ld_acquire(&c->a_done) != nA) {
+                        const unsigned long long w0 = gtime();
+                        unsigned int ns = 32;
+                        while (ld_acquire(&c->a_done) != nA) {
+                            __nanosleep(ns);
+                            ns = min(ns * 2u, 256u);
+                        }
+                        atomicAdd(&p.head->wait_ns, gtime() - w0);  // trace
                         atomicAdd(&p.head->waits, 1u);
                     }
+                    sHdr[3] = (int)__ldcg(&c->amax);
                 }
+                nbar_sync(kBarC, kConsumers);
+                // K2, locally: scale, thresholds (2 predicate evaluations
+                // each), bucket table in shared memory
+                const unsigned int amax = (unsigned int)sHdr[3];
+                const float scale = amax == 0u ? 1.0f : __uint_as_float(amax);
+                uint32_t t = kInfBits;
+                if (ctid < 128) {
+                    if (scale_ok(scale) && ctid + 1 < p.book->ndistinct) t = threshold((double)scale, sV[ctid], sV[ctid + 1]);
+                    sT[ctid] = t;
+                }
+                const int nf = nbar_popc(kBarC, kConsumers, ctid < 127 && t < kInfBits);
                 int32_t kb;
                 uint32_t len;
                 lut_geometry(sT, (uint32_t)nf, &kb, &len);
@@ -624,7 +576,13 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                 tlenm1 = (int)len - 1;
                 const bool ok = len <= (uint32_t)kLutMax && fill_lut_local(sT, nf, sCanon, kb, sE, sRed, ctid);
                 tvalid = nbar_and(kBarC, kConsumers, ok);  // also: sE complete
+                tamax = amax;
                 cur = m.seg;
+            }
+            if (cur != -2 && m.base == 0) {  // the CTA encoding chunk 0 publishes scale and status
+                const float scale = tamax == 0u ? 1.0f : __uint_as_float(tamax);
+                if (ctid < p.lay.scale_reps) p.lay.scales[ctid * p.lay.scale_block_stride + sg.scale_idx] = scale;
+                if (ctid == 0 && tamax >= kInfBits) atomicOr(&p.head->status, A8_STATUS_NONFINITE);
             }
             if (cur == -2 && m.base == 0 && ctid < p.lay.scale_reps)
                 p.lay.scales[ctid * p.lay.scale_block_stride + sg.scale_idx] = p.static_lut->scale;
@@ -718,8 +676,6 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
             p.ctl[i].a_done = 0u;
             p.ctl[i].ready = 0u;
         }
-        if (p.absmax)
-            for (int i = tid; i < p.nseg * 128; i += kEncThreads) seg_thresholds(p.luts, i >> 7)[i & 127] = 0ull;
         if (tid < p.lay.scale_reps) {
             const unsigned int stt = atomicAdd(&p.head->status, 0u) | (p.status_in ? *p.status_in : 0u);
             p.status_out[(int64_t)tid * p.lay.scale_block_stride] = stt;
