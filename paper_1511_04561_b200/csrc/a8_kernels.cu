@@ -300,6 +300,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
     __shared__ int sHdr[4];
     __shared__ unsigned int sRed[kConsumerWarps];
     __shared__ unsigned int sRed2[2][kConsumerWarps];  // A-run flushes
+    __shared__ int sMode;                              // E switch: build / copy / build + publish
     __shared__ int sFinal;
     // the plan, staged in shared memory when it fits: the producer reads it
     // on every ticket, and kernel-parameter / global reads cost it latency
@@ -557,25 +558,64 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                         atomicAdd(&p.head->waits, 1u);
                     }
                     sHdr[3] = (int)__ldcg(&c->amax);
+                    // the first CTA here builds the table and publishes it in the
+                    // workspace (ready: 0 none, 1 being built, 2 published); later
+                    // CTAs copy it (one 12-16 KB L2 read) instead of rebuilding
+                    unsigned int r = ld_acquire(&p.ctl[m.seg].ready);
+                    int mode = 1;  // 1 build locally, 2 copy, 3 build + publish
+                    if (r == 2u)
+                        mode = 2;
+                    else if (r == 0u && atomicCAS(&p.ctl[m.seg].ready, 0u, 1u) == 0u)
+                        mode = 3;
+                    sMode = mode;
                 }
                 nbar_sync(kBarC, kConsumers);
-                // K2, locally: scale, thresholds (2 predicate evaluations
-                // each), bucket table in shared memory
                 const unsigned int amax = (unsigned int)sHdr[3];
-                const float scale = amax == 0u ? 1.0f : __uint_as_float(amax);
-                uint32_t t = kInfBits;
-                if (ctid < 128) {
-                    if (scale_ok(scale) && ctid + 1 < p.book->ndistinct) t = threshold((double)scale, sV[ctid], sV[ctid + 1]);
-                    sT[ctid] = t;
+                const int mode = sMode;
+                if (mode == 2) {
+                    load_lut_smem(p.luts + m.seg, sE, sT, sCanon, p.book, sHdr, ctid, kConsumers);
+                    nbar_sync(kBarC, kConsumers);
+                    tvalid = sHdr[0];
+                    tkbase = sHdr[1];
+                    tlenm1 = sHdr[2];
+                } else {
+                    // K2, locally: scale, thresholds (2 predicate evaluations
+                    // each), bucket table in shared memory
+                    const float scale = amax == 0u ? 1.0f : __uint_as_float(amax);
+                    uint32_t t = kInfBits;
+                    if (ctid < 128) {
+                        if (scale_ok(scale) && ctid + 1 < p.book->ndistinct) t = threshold((double)scale, sV[ctid], sV[ctid + 1]);
+                        sT[ctid] = t;
+                    }
+                    const int nf = nbar_popc(kBarC, kConsumers, ctid < 127 && t < kInfBits);
+                    int32_t kb;
+                    uint32_t len;
+                    lut_geometry(sT, (uint32_t)nf, &kb, &len);
+                    tkbase = kb;
+                    tlenm1 = (int)len - 1;
+                    const bool ok = len <= (uint32_t)kLutMax && fill_lut_local(sT, nf, sCanon, kb, sE, sRed, ctid);
+                    tvalid = nbar_and(kBarC, kConsumers, ok);  // also: sE complete
+                    if (mode == 3) {  // publish for the CTAs that come later
+                        a8_lut_t* L = p.luts + m.seg;
+                        if (ctid < 128) L->T[ctid] = sT[ctid];
+                        if (tvalid) {
+                            uint4* d4 = reinterpret_cast<uint4*>(L->e);
+                            const uint4* s4 = reinterpret_cast<const uint4*>(sE);
+                            for (uint32_t j = ctid; j < (len + 3) >> 2; j += kConsumers) d4[j] = s4[j];
+                        }
+                        if (ctid == 0) {
+                            L->len = len;
+                            L->kbase = kb;
+                            L->valid = (uint32_t)tvalid;
+                            L->nfinite = (uint32_t)nf;
+                        }
+                        nbar_sync(kBarC, kConsumers);
+                        if (ctid == 0) {
+                            __threadfence();
+                            st_release(&p.ctl[m.seg].ready, 2u);
+                        }
+                    }
                 }
-                const int nf = nbar_popc(kBarC, kConsumers, ctid < 127 && t < kInfBits);
-                int32_t kb;
-                uint32_t len;
-                lut_geometry(sT, (uint32_t)nf, &kb, &len);
-                tkbase = kb;
-                tlenm1 = (int)len - 1;
-                const bool ok = len <= (uint32_t)kLutMax && fill_lut_local(sT, nf, sCanon, kb, sE, sRed, ctid);
-                tvalid = nbar_and(kBarC, kConsumers, ok);  // also: sE complete
                 tamax = amax;
                 cur = m.seg;
             }
