@@ -202,3 +202,25 @@ def test_thresholds_at_random_scales_match_bisection(kind):
         N.check(N.lib.a8_build_lut_host(C.byref(cb._book), float(s), C.byref(lut)))
         T = np.frombuffer(bytes(lut.T), np.uint32)[:127]
         assert np.array_equal(T, O.thresholds(kind, float(s))), (kind, s)
+
+
+def test_parallel_threshold_window(tmp_path):
+    """The resident kernel tests the 8 float32 patterns around the rounded
+    midpoint in parallel (threshold_parallel); on the host, over random
+    normal scales and all four codebooks, that window must give exactly
+    threshold()'s result (or fall back to it)."""
+    import shutil
+    import subprocess
+
+    gxx = shutil.which("g++")
+    if gxx is None:
+        pytest.skip("g++ not available")
+    root = ROOT
+    exe = tmp_path / "threshold_window"
+    subprocess.run([gxx, "-O2", "-std=c++17", f"-I{root / 'paper_1511_04561_b200' / 'csrc'}", f"-I{root / 'include'}",
+                    str(root / "tests" / "cpp" / "threshold_window.cpp"),
+                    str(root / "paper_1511_04561_b200" / "csrc" / "a8_codebook.cpp"), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe), "1500"], capture_output=True, text=True)
+    total, bad, fallback = (int(v) for v in out.stdout.split())
+    assert out.returncode == 0 and bad == 0, out.stdout
+    assert total > 700_000 and fallback < total // 100
