@@ -823,6 +823,7 @@ struct RSeg {
 struct RParams {
     a8_layout_t lay;
     const a8_book_t* book;
+    const a8_lut_t* static_lut;  // fixed-scale specs: the one table (no max pass, no barrier)
     WsHead* head;
     SegCtl* ctl;
     const unsigned int* status_in;
@@ -832,13 +833,71 @@ struct RParams {
     RSeg segs[kInlineSegs + 1];  // segs[nseg].cta0 = grid
 };
 
+// Encode elements [lo, hi) of segment g from shared memory (dst[i]) with the
+// table in sE (valid) or the thresholds in sT; codes through the layout.
+__device__ void resident_encode_piece(const RParams& p, const RSeg& g, const float* dst, int64_t lo, int64_t hi,
+                                      int64_t a0, int64_t a1, int valid, int32_t kb, uint32_t len, const uint32_t* sE,
+                                      const uint32_t* sT, const uint8_t* sCanon, int tid) {
+    const int64_t L = p.lay.block_len;
+    const int64_t gap = p.lay.block_stride - p.lay.block_len;
+    if (hi > lo) {
+        const int64_t f_lo = g.flat_off + lo, f_hi = g.flat_off + hi - 1;
+        const int32_t kmax = kb + (int32_t)len - 1;
+        if (valid && (f_lo / L) == (f_hi / L)) {
+            uint8_t* cb = p.lay.codes + (f_lo / L) * gap + g.flat_off;  // code of element i at cb[i]
+            const uint32_t* eb = sE - kb;
+            for (int64_t i = a0 + 4 * (int64_t)tid; i < a1; i += 4 * kRThreads) {
+                const uint4 v = *reinterpret_cast<const uint4*>(dst + i);
+                *reinterpret_cast<uint32_t*>(cb + i) = encode4_lut(v, eb, kb, kmax);
+            }
+            if (tid < a0 - lo) cb[lo + tid] = (uint8_t)encode_lut(__float_as_uint(dst[lo + tid]), sE, kb, (int32_t)len - 1);
+            if (tid < hi - a1) cb[a1 + tid] = (uint8_t)encode_lut(__float_as_uint(dst[a1 + tid]), sE, kb, (int32_t)len - 1);
+        } else {
+            for (int64_t i = lo + tid; i < hi; i += kRThreads) {
+                const uint32_t b = __float_as_uint(dst[i]);
+                const uint32_t cc = valid ? encode_lut(b, sE, kb, (int32_t)len - 1) : encode_search(b, sT, sCanon);
+                const int64_t f = g.flat_off + i;
+                p.lay.codes[f + (f / L) * gap] = (uint8_t)cc;
+            }
+        }
+    }
+
+}
+
+// Phase 4: the last CTA out publishes the status and re-zeroes the workspace.
+__device__ void resident_finish(const RParams& p, int tid) {
+    __shared__ int sFinal;
+    __syncthreads();
+    RES_STAMP(5);
+    if (tid == 0) {
+        __threadfence();
+        sFinal = atomicAdd(&p.head->ctas_done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (sFinal) {
+        __threadfence();
+        for (int i = tid; i < p.nseg; i += kRThreads) p.ctl[i].amax = 0u;
+        if (tid < p.lay.scale_reps) {
+            const unsigned int stt = atomicAdd(&p.head->status, 0u) | (p.status_in ? *p.status_in : 0u);
+            p.status_out[(int64_t)tid * p.lay.scale_block_stride] = stt;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            p.head->ticket = 0u;
+            p.head->ctas_done = 0u;
+            p.head->status = 0u;
+        }
+        __threadfence();
+    }
+}
+
 __global__ void __launch_bounds__(kRThreads, 1) resident_encode_kernel(const __grid_constant__ RParams p) {
     extern __shared__ __align__(128) float sData[];
     __shared__ __align__(16) uint32_t sE[kLutMax];
     __shared__ uint32_t sT[128];
     __shared__ uint8_t sCanon[128];
     __shared__ unsigned int sWarp[kRThreads / 32];
-    __shared__ int sFinal;
+    __shared__ int sHdr[4];
     __shared__ unsigned int sAmax;
     __shared__ __align__(8) uint64_t sBar;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -892,8 +951,28 @@ __global__ void __launch_bounds__(kRThreads, 1) resident_encode_kernel(const __g
         if (tid == 0) {
             unsigned int m = 0;
             for (int i = 0; i < kRThreads / 32; ++i) m = max(m, sWarp[i]);
-            if (m) atomicMax(&p.ctl[s].amax, m >> 1);
+            if (p.static_lut) {
+                sAmax = m >> 1;  // fixed scale: only the non-finite check needs the max
+            } else if (m) {
+                atomicMax(&p.ctl[s].amax, m >> 1);
+            }
         }
+    }
+
+    if (p.static_lut) {  // fixed-scale spec: one shared table, no cross-CTA dependency
+        if (tid == 0 && sAmax >= kInfBits) atomicOr(&p.head->status, A8_STATUS_NONFINITE);
+        int* hdr = sHdr;  // [valid, kbase, len-1]
+        load_lut_smem(p.static_lut, sE, sT, sCanon, p.book, hdr, tid, kRThreads);
+        __syncthreads();
+        const float scale = p.static_lut->scale;
+        if (q == 0 && tid < p.lay.scale_reps) p.lay.scales[tid * p.lay.scale_block_stride + g.scale_idx] = scale;
+        if (blockIdx.x == 0)
+            for (int e = 0; e < p.nseg; ++e)
+                if (p.segs[e].n == 0 && tid < p.lay.scale_reps)
+                    p.lay.scales[tid * p.lay.scale_block_stride + p.segs[e].scale_idx] = scale;
+        resident_encode_piece(p, g, dst, lo, hi, a0, a1, hdr[0], hdr[1], (uint32_t)hdr[2] + 1u, sE, sT, sCanon, tid);
+        resident_finish(p, tid);
+        return;
     }
 
     // ---- phase 2: grid barrier (cooperative launch: all CTAs are resident) ----
@@ -933,53 +1012,8 @@ __global__ void __launch_bounds__(kRThreads, 1) resident_encode_kernel(const __g
             if (p.segs[e].n == 0 && tid < p.lay.scale_reps)
                 p.lay.scales[tid * p.lay.scale_block_stride + p.segs[e].scale_idx] = 1.0f;
     }
-    const int64_t L = p.lay.block_len;
-    const int64_t gap = p.lay.block_stride - p.lay.block_len;
-    if (hi > lo) {
-        const int64_t f_lo = g.flat_off + lo, f_hi = g.flat_off + hi - 1;
-        const int32_t kmax = kb + (int32_t)len - 1;
-        if (valid && (f_lo / L) == (f_hi / L)) {
-            uint8_t* cb = p.lay.codes + (f_lo / L) * gap + g.flat_off;  // code of element i at cb[i]
-            const uint32_t* eb = sE - kb;
-            for (int64_t i = a0 + 4 * (int64_t)tid; i < a1; i += 4 * kRThreads) {
-                const uint4 v = *reinterpret_cast<const uint4*>(dst + i);
-                *reinterpret_cast<uint32_t*>(cb + i) = encode4_lut(v, eb, kb, kmax);
-            }
-            if (tid < a0 - lo) cb[lo + tid] = (uint8_t)encode_lut(__float_as_uint(dst[lo + tid]), sE, kb, (int32_t)len - 1);
-            if (tid < hi - a1) cb[a1 + tid] = (uint8_t)encode_lut(__float_as_uint(dst[a1 + tid]), sE, kb, (int32_t)len - 1);
-        } else {
-            for (int64_t i = lo + tid; i < hi; i += kRThreads) {
-                const uint32_t b = __float_as_uint(dst[i]);
-                const uint32_t cc = valid ? encode_lut(b, sE, kb, (int32_t)len - 1) : encode_search(b, sT, sCanon);
-                const int64_t f = g.flat_off + i;
-                p.lay.codes[f + (f / L) * gap] = (uint8_t)cc;
-            }
-        }
-    }
-
-    // ---- phase 4: last CTA out publishes the status and re-zeroes the workspace ----
-    __syncthreads();
-    RES_STAMP(5);
-    if (tid == 0) {
-        __threadfence();
-        sFinal = atomicAdd(&p.head->ctas_done, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (sFinal) {
-        __threadfence();
-        for (int i = tid; i < p.nseg; i += kRThreads) p.ctl[i].amax = 0u;
-        if (tid < p.lay.scale_reps) {
-            const unsigned int stt = atomicAdd(&p.head->status, 0u) | (p.status_in ? *p.status_in : 0u);
-            p.status_out[(int64_t)tid * p.lay.scale_block_stride] = stt;
-        }
-        __syncthreads();
-        if (tid == 0) {
-            p.head->ticket = 0u;
-            p.head->ctas_done = 0u;
-            p.head->status = 0u;
-        }
-        __threadfence();
-    }
+    resident_encode_piece(p, g, dst, lo, hi, a0, a1, valid, kb, len, sE, sT, sCanon, tid);
+    resident_finish(p, tid);
 }
 
 // ---------------------------------------------------------------------------
@@ -1358,7 +1392,7 @@ extern "C" int a8_device_info(int device, int* num_sms, int* enc_ctas_per_sm, in
     return A8_OK;
 }
 
-// Resident encode (absmax calls that fit in shared memory).  A8_RESIDENT=0
+// Resident encode (calls that fit in shared memory, any spec).  A8_RESIDENT=0
 // disables it (A/B measurements).
 static bool resident_enabled() {
     static const bool on = [] {
@@ -1372,9 +1406,9 @@ static bool resident_enabled() {
 // Every non-empty segment gets its own CTAs (at least enough for its data to
 // fit, then a share of the remaining SMs proportional to its size), so each
 // CTA holds one piece of one segment and builds one table.
-static int encode_resident(const a8_enc_seg_t* segs, int nseg, const void* book_dev, const a8_layout_t& layout,
-                           void* workspace, const uint32_t* status_in, uint32_t* status_out, const DevInfo& di,
-                           cudaStream_t st, bool* done) {
+static int encode_resident(const a8_enc_seg_t* segs, int nseg, const void* book_dev, const void* static_lut_dev,
+                           const a8_layout_t& layout, void* workspace, const uint32_t* status_in,
+                           uint32_t* status_out, const DevInfo& di, cudaStream_t st, bool* done) {
     *done = false;
     if (!resident_enabled() || di.res_occ < 1 || nseg > kInlineSegs) return A8_OK;
     const int64_t per = kRCap - 4;  // elements per CTA (+ up to 3 of alignment offset)
@@ -1397,6 +1431,7 @@ static int encode_resident(const a8_enc_seg_t* segs, int nseg, const void* book_
     memset(&p, 0, sizeof(p));
     p.lay = layout;
     p.book = static_cast<const a8_book_t*>(book_dev);
+    p.static_lut = static_cast<const a8_lut_t*>(static_lut_dev);
     uint8_t* ws = static_cast<uint8_t*>(workspace);
     p.head = reinterpret_cast<WsHead*>(ws);
     p.ctl = reinterpret_cast<SegCtl*>(ws + ctl_off());
@@ -1423,7 +1458,7 @@ static int encode_resident(const a8_enc_seg_t* segs, int nseg, const void* book_
     at[0].id = cudaLaunchAttributeCooperative;  // the grid barrier needs every CTA resident
     at[0].val.cooperative = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = static_lut_dev ? 0 : 1;  // fixed scales: no barrier
     cudaLaunchKernelEx(&cfg, resident_encode_kernel, p);
     *done = true;
     return cuda_check("a8_encode (resident)");
@@ -1446,7 +1481,7 @@ extern "C" int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_de
     if (int rc = dev_info(device, &di)) return rc;
 
     const bool absmax = norm == A8_NORM_ABSMAX;
-    if (absmax) {
+    {
         for (int i = 0; i < nseg; ++i) {
             const a8_enc_seg_t& s = segs[i];
             if (s.n < 0 || (s.n > 0 && !s.x)) return fail(A8_ERR_USAGE, "a8_encode: bad segment");
@@ -1454,8 +1489,8 @@ extern "C" int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_de
         }
         if (ws_capacity(workspace_bytes) < nseg) return fail(A8_ERR_USAGE, "a8_encode: workspace too small for the segment count");
         bool done = false;
-        const int rc = encode_resident(segs, nseg, book_dev, layout, workspace, status_in, status_out, di,
-                                       static_cast<cudaStream_t>(stream), &done);
+        const int rc = encode_resident(segs, nseg, book_dev, absmax ? nullptr : static_lut_dev, layout, workspace,
+                                       status_in, status_out, di, static_cast<cudaStream_t>(stream), &done);
         if (rc || done) return rc;
     }
 
