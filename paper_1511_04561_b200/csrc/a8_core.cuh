@@ -185,13 +185,15 @@ A8_HD uint32_t encode_lut(uint32_t b, const uint32_t* e, int32_t kbase, int32_t 
 
 #if defined(__CUDACC__)
 // Canonical code (no sign) in the low byte of the result, garbage above.
-// `eb` is the table base pre-offset by -kbase entries, so the clamped key
-// indexes it directly.  Key and operand arithmetic use IMAD (FMA pipe); the
-// ALU pipe does the clamp, compare and select.
-__device__ __forceinline__ uint32_t lut_code_lo(uint32_t b, const uint32_t* eb, int32_t kmin, int32_t kmax) {
+// Key and operand arithmetic use IMAD (FMA pipe); the ALU pipe does the
+// clamp, compare and select.
+// `ebase` is the 32-bit shared-memory address of the table pre-offset by
+// -kbase entries: one IMAD forms the entry's address from the clamped key.
+__device__ __forceinline__ uint32_t lut_code_lo(uint32_t b, uint32_t ebase, int32_t kmin, int32_t kmax) {
     const int32_t key = (int32_t)__umulhi(b * 2u, 1u << (31 - kKeyShift));  // (b & 0x7fffffff) >> 16
     const int32_t k = min(max(key, kmin), kmax);
-    const uint32_t v = eb[k];
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(ebase + (uint32_t)k * 4u));
     return (b * 65536u + 0xffffu >= v) ? (v >> 8) : v;
 }
 
@@ -205,12 +207,36 @@ __device__ __forceinline__ uint32_t attach_signs4(uint32_t packed, uint32_t b0, 
     return packed | ((packed + 0x7f7f7f7fu) & s & 0x80808080u);
 }
 
+// One element as lut_code_lo, also returning the unclamped key (>= 0x7f80
+// iff |x| is Inf or NaN: the fixed-scale specs' non-finite check).
+__device__ __forceinline__ uint32_t lut_code_lo_k(uint32_t b, uint32_t ebase, int32_t kmin, int32_t kmax,
+                                                  int32_t& key) {
+    key = (int32_t)__umulhi(b * 2u, 1u << (31 - kKeyShift));  // (b & 0x7fffffff) >> 16
+    const int32_t k = min(max(key, kmin), kmax);
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(ebase + (uint32_t)k * 4u));
+    return (b * 65536u + 0xffffu >= v) ? (v >> 8) : v;
+}
+
+// encode4_lut that also folds the four keys into `kacc` (running max).
+__device__ __forceinline__ uint32_t encode4_lut_k(uint4 v, uint32_t ebase, int32_t kmin, int32_t kmax,
+                                                  int32_t& kacc) {
+    int32_t k0, k1, k2, k3;
+    const uint32_t c0 = lut_code_lo_k(v.x, ebase, kmin, kmax, k0);
+    const uint32_t c1 = lut_code_lo_k(v.y, ebase, kmin, kmax, k1);
+    const uint32_t c2 = lut_code_lo_k(v.z, ebase, kmin, kmax, k2);
+    const uint32_t c3 = lut_code_lo_k(v.w, ebase, kmin, kmax, k3);
+    kacc = max(max(kacc, k0), max(k1, max(k2, k3)));
+    const uint32_t packed = __byte_perm(__byte_perm(c0, c1, 0x0040), __byte_perm(c2, c3, 0x0040), 0x5410);
+    return attach_signs4(packed, v.x, v.y, v.z, v.w);
+}
+
 // Four elements -> four codes packed little-endian (bucket table).
-__device__ __forceinline__ uint32_t encode4_lut(uint4 v, const uint32_t* eb, int32_t kmin, int32_t kmax) {
-    const uint32_t c0 = lut_code_lo(v.x, eb, kmin, kmax);
-    const uint32_t c1 = lut_code_lo(v.y, eb, kmin, kmax);
-    const uint32_t c2 = lut_code_lo(v.z, eb, kmin, kmax);
-    const uint32_t c3 = lut_code_lo(v.w, eb, kmin, kmax);
+__device__ __forceinline__ uint32_t encode4_lut(uint4 v, uint32_t ebase, int32_t kmin, int32_t kmax) {
+    const uint32_t c0 = lut_code_lo(v.x, ebase, kmin, kmax);
+    const uint32_t c1 = lut_code_lo(v.y, ebase, kmin, kmax);
+    const uint32_t c2 = lut_code_lo(v.z, ebase, kmin, kmax);
+    const uint32_t c3 = lut_code_lo(v.w, ebase, kmin, kmax);
     const uint32_t packed = __byte_perm(__byte_perm(c0, c1, 0x0040), __byte_perm(c2, c3, 0x0040), 0x5410);
     return attach_signs4(packed, v.x, v.y, v.z, v.w);
 }

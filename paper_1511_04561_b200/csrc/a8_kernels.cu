@@ -635,20 +635,18 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                 // fast path: a full chunk inside one block, bucket table
                 uint32_t* out = reinterpret_cast<uint32_t*>(codes_base + m.code_off) + ctid;
                 const uint4* in = reinterpret_cast<const uint4*>(stage) + ctid;
-                const uint32_t* eb = sE - kbase;  // indexed by the clamped key
+                const uint32_t eb = smem_addr(sE) - (uint32_t)kbase * 4u;  // indexed by the clamped key
                 const int32_t kmax = kbase + lenm1;
                 if (p.absmax) {
 #pragma unroll
                     for (int q = 0; q < kChunk / (kConsumers * 4); ++q)
                         out[q * kConsumers] = encode4_lut(in[q * kConsumers], eb, kbase, kmax);
                 } else {
+                    int32_t kacc = 0;  // max key: >= 0x7f80 iff some |x| is Inf/NaN
 #pragma unroll
-                    for (int q = 0; q < kChunk / (kConsumers * 4); ++q) {
-                        const uint4 v = in[q * kConsumers];
-                        out[q * kConsumers] = encode4_lut(v, eb, kbase, kmax);
-                        big = max(big, max(max(v.x & 0x7fffffffu, v.y & 0x7fffffffu),
-                                           max(v.z & 0x7fffffffu, v.w & 0x7fffffffu)));
-                    }
+                    for (int q = 0; q < kChunk / (kConsumers * 4); ++q)
+                        out[q * kConsumers] = encode4_lut_k(in[q * kConsumers], eb, kbase, kmax, kacc);
+                    big = (uint32_t)kacc << kKeyShift;
                 }
             } else {
             const int64_t f0 = sg.flat_off + m.base;
@@ -845,7 +843,7 @@ __device__ void resident_encode_piece(const RParams& p, const RSeg& g, const flo
         const int32_t kmax = kb + (int32_t)len - 1;
         if (valid && (f_lo / L) == (f_hi / L)) {
             uint8_t* cb = p.lay.codes + (f_lo / L) * gap + g.flat_off;  // code of element i at cb[i]
-            const uint32_t* eb = sE - kb;
+            const uint32_t eb = smem_addr(sE) - (uint32_t)kb * 4u;
             for (int64_t i = a0 + 4 * (int64_t)tid; i < a1; i += 4 * kRThreads) {
                 const uint4 v = *reinterpret_cast<const uint4*>(dst + i);
                 *reinterpret_cast<uint32_t*>(cb + i) = encode4_lut(v, eb, kb, kmax);

@@ -222,3 +222,19 @@ def test_error_suite_cells_on_gpu(cuda):
         nz = x64 != 0
         assert float(err.mean()) == c["mean_abs_error"]
         assert float(np.mean(err[nz] / np.abs(x64[nz])) * 100.0) == c["mean_rel_error_pct"]
+
+
+@pytest.mark.parametrize("spec", [ALL_SPECS[1], ALL_SPECS[5]], ids=tag)
+@pytest.mark.parametrize("bad", [float("nan"), float("-inf")])
+def test_non_finite_in_large_call_ticket_kernel(spec, bad, cuda):
+    """Beyond the resident kernel's capacity the ticket kernel runs: a
+    non-finite value inside a full, aligned chunk (fast path) must still
+    raise, and the workspace must be clean for the next call."""
+    x = torch.randn(8_000_000, device=cuda)
+    x[5_000_003] = bad
+    cb = A.build_codebook(S(spec))
+    with pytest.raises(A.InputError):
+        A.encode_buffer(x, cb)
+    x[5_000_003] = 0.0
+    q = A.encode_buffer(x, cb)
+    assert q.scale > 0
