@@ -334,6 +334,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
     if (!p.absmax && tid >= 32)  // fixed scale: one table for every segment
         load_lut_smem(p.static_lut, sE, sT, sCanon, p.book, sHdr, tid - 32, kConsumers);
     __syncthreads();
+    const uint32_t full0 = smem_addr(&sFull[0]), empty0 = smem_addr(&sEmpty[0]);  // ring barriers
 
     if (warp == 0) {
         // ===================== producer =====================
@@ -364,7 +365,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                 asm volatile("" ::"l"(t));
                 const unsigned long long tr_known = gtime();
 #endif
-                mbar_wait(&sEmpty[st], ((it / kStages) & 1) ^ 1);
+                mbar_wait_a(empty0 + 8u * st, ((it / kStages) & 1) ^ 1);
 #ifdef A8_TICKET_TRACE
                 const unsigned long long tr_free = gtime();
 #endif
@@ -470,7 +471,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
 
         for (int it = 0;; ++it) {
             const int st = it % kStages;
-            mbar_wait(&sFull[st], (it / kStages) & 1);
+            mbar_wait_a(full0 + 8u * st, (it / kStages) & 1);
             const StageMeta m = sMeta[st];
             if (aseg >= 0 && (m.kind != kA || m.seg != aseg)) flush();
             if (m.kind == kEnd) break;
@@ -505,7 +506,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                 // ---------------- A: max |x| over the chunk ----------------
                 amx = max(amx, part_max());
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&sEmpty[st]);  // stage consumed
+                if (lane == 0) mbar_arrive_a(empty0 + 8u * st);  // stage consumed
 #ifdef A8_TICKET_TRACE
                 if (ctid == 0 && m.tkt < kTraceTickets) g_ticket_trace[m.tkt][1] = gtime();
 #endif
@@ -693,7 +694,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
             if (!p.absmax && __any_sync(0xffffffffu, big >= kInfBits) && lane == 0)
                 atomicOr(&p.head->status, A8_STATUS_NONFINITE);
             __syncwarp();
-            if (lane == 0) mbar_arrive(&sEmpty[st]);
+            if (lane == 0) mbar_arrive_a(empty0 + 8u * st);
 #ifdef A8_TICKET_TRACE
             if (ctid == 0 && m.tkt < kTraceTickets) g_ticket_trace[m.tkt][1] = gtime();
 #endif

@@ -3,7 +3,7 @@ timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
 for rep in 1; do
 for v in base head; do
   if [ $v = base ]; then lib=paper_1511_04561_b200/_lib/libapprox8_b200.so; else lib=paper_1511_04561_b200/_lib_var/$v/libapprox8_b200.so; fi
-  for spec in mantissa/decade+1; do
+  for spec in dynamic-tree/absmax mantissa/decade+1; do
   for c in alexnet big; do A8_LIB=$lib A8_RESIDENT=0 timeout 300 python tools/prof_codec.py --case $c --spec $spec | python -c "
 import sys,json
 for l in sys.stdin:
