@@ -1032,7 +1032,9 @@ constexpr int kDecChunkD = kDecThreads * kDecGroups * 4;  // 4096 elements
 // (the larger shared-memory carveout costs more than the conflicts save).
 __host__ __device__ __forceinline__ int dec_rep_shift(int) { return 2; }
 
-__global__ void __launch_bounds__(kDecThreads) decode_kernel(const __grid_constant__ DecParams p) {
+// 4 CTAs/SM (64 registers).  Measured: 2 CTAs (96 registers, the default
+// when min-blocks is 1) 30% slower, 5-8 CTAs (48-32 registers) slower at 2^30.
+__global__ void __launch_bounds__(kDecThreads, 4) decode_kernel(const __grid_constant__ DecParams p) {
     extern __shared__ float sTab[];  // [nranks][256][rep]
     const int tid = threadIdx.x;
     const int rsh = dec_rep_shift(p.nranks);
@@ -1063,7 +1065,7 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(const __grid_consta
         if (tid == 0) *p.status_out = sSt;
     }
 
-    for (int64_t c = blockIdx.x; c < p.total; c += gridDim.x) {
+    auto seg_of = [&](int64_t c) {
         int lo = 0, hi = p.nseg;
         while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
@@ -1072,6 +1074,11 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(const __grid_consta
             else
                 hi = mid;
         }
+        return lo;
+    };
+
+    for (int64_t c = blockIdx.x; c < p.total; c += gridDim.x) {
+        const int lo = seg_of(c);
         const DecSegD sg = segs[lo];
         if (lo != cur) {
             __syncthreads();
