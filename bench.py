@@ -346,19 +346,20 @@ def run_b200(args, nranks, rank, local_rank):
     # pipelined over two device buffers on three streams, so the H2D of
     # step k+1 and the D2H of step k use both PCIe directions at once.
     ex.codec = codec
-    host_out = [[torch.empty_like(p).pin_memory() for p in pinned] for _ in range(2)]
-    dev_in = [[torch.empty_like(g) for g in grads] for _ in range(2)]
+    NB = 2  # device buffers in flight (3 measured no better: the copies share PCIe)
+    host_out = [[torch.empty_like(p).pin_memory() for p in pinned] for _ in range(NB)]
+    dev_in = [[torch.empty_like(g) for g in grads] for _ in range(NB)]
     s_h2d, s_d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     comp = torch.cuda.current_stream(dev)
-    ev_in = [torch.cuda.Event() for _ in range(2)]
-    ev_done = [torch.cuda.Event() for _ in range(2)]
-    ev_out = [torch.cuda.Event() for _ in range(2)]
-    for b in range(2):  # buffers start free
+    ev_in = [torch.cuda.Event() for _ in range(NB)]
+    ev_done = [torch.cuda.Event() for _ in range(NB)]
+    ev_out = [torch.cuda.Event() for _ in range(NB)]
+    for b in range(NB):  # buffers start free
         ev_done[b].record(comp)
         ev_out[b].record(comp)
 
     def e2e_step(i):
-        b = i & 1
+        b = i % NB
         with torch.cuda.stream(s_h2d):
             s_h2d.wait_event(ev_out[b])  # the previous D2H from this buffer has finished
             for d, p in zip(dev_in[b], pinned):
@@ -373,7 +374,7 @@ def run_b200(args, nranks, rank, local_rank):
                 h.copy_(d, non_blocking=True)
             ev_out[b].record(s_d2h)
 
-    for i in range(max(2, args.warmup)):
+    for i in range(max(NB, args.warmup)):
         e2e_step(i)
     torch.cuda.synchronize()
     barrier()
@@ -381,16 +382,40 @@ def run_b200(args, nranks, rank, local_rank):
     e0.record(comp)
     for i in range(args.steps):
         e2e_step(i)
-    for b in range(2):
+    for b in range(NB):
         comp.wait_event(ev_out[b])
     e1.record(comp)
     torch.cuda.synchronize()
     barrier()
     ex.synchronize()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    # the PCIe bound of that step: the same bytes copied H2D and D2H
+    # concurrently (pinned), no compute
+    a_in, a_out = torch.empty(n, device=dev), torch.empty(n, device=dev)
+    h_in, h_out = torch.empty(n).pin_memory(), torch.empty(n).pin_memory()
+    pcie = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record(comp)
+        s_h2d.wait_event(p0)
+        s_d2h.wait_event(p0)
+        with torch.cuda.stream(s_h2d):
+            a_in.copy_(h_in, non_blocking=True)
+        with torch.cuda.stream(s_d2h):
+            h_out.copy_(a_out, non_blocking=True)
+        comp.wait_stream(s_h2d)
+        comp.wait_stream(s_d2h)
+        p1.record(comp)
+        torch.cuda.synchronize()
+        pcie.append(p0.elapsed_time(p1))
+    pcie_ms = float(np.median(pcie))
+    del a_in, a_out, h_in, h_out
     e2e = {"value": nranks * 4.0 * n / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
            "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n, "ms_per_step": e2e_ms,
-           "how": "pinned H2D + exchange + D2H every step, pipelined over 2 buffers / 3 streams"}
+           "pcie_bound_ms": pcie_ms, "frac_of_pcie_bound": pcie_ms / e2e_ms,
+           "how": f"pinned H2D + exchange + D2H every step, pipelined over {NB} buffers / 3 streams; "
+                  "pcie_bound_ms = the same H2D and D2H bytes copied concurrently without compute"}
 
     cpu = None
     if rank == 0 and nranks == 1 and not args.no_cpu:
