@@ -200,6 +200,19 @@ int a8_onebit_quantize(const void* g, int g_is_f64, double* residual, int64_t n,
 /* onebit_decode (codecs.py:342-348): out[i] = bit ? levels[0] : levels[1]. */
 int a8_onebit_decode(const uint8_t* bits, int64_t n, const float* levels, float* out, void* stream);
 
+/* Per-block max-abs codec (north star: "optional per-block max-abs"; not a
+ * reference feature).  Block b = elements [b*block, (b+1)*block) is encoded
+ * exactly as encode_buffer(x[block b]) with absmax normalisation
+ * (codecs.py:232-269): scales[b] = float32(max |x| of the block), 0 -> 1.
+ * block is 1024, 2048 or 4096; codes 4-byte aligned; scales holds
+ * ceil(n/block) floats; status_out (device uint32) is overwritten with
+ * A8_STATUS_* bits.  Single pass: 4 B read + 1 B written per element.     */
+int a8_encode_blocked(const float* x, int64_t n, int64_t block, const void* book_dev, uint8_t* codes,
+                      float* scales, uint32_t* status_out, void* stream);
+/* decode of a8_encode_blocked: out[i] = table[codes[i]] * scales[i / block]
+ * (one RN multiply, codecs.py:281).                                          */
+int a8_decode_blocked(const uint8_t* codes, int64_t n, int64_t block, const float* scales, const void* book_dev,
+                      float* out, void* stream);
 /* Round-trip error aggregates: measure_error (errorbench.py:79-99) and the
  * hook statistics _HookStats.record (mlp.py:146-153).  Over n elements:
  *   d      = float32(table[codes[i]] * *scale_dev)  (codes != NULL, the

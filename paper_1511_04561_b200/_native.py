@@ -120,6 +120,12 @@ SIGNATURES = {
          C.c_size_t, C.c_void_p],
     ),
     "a8_onebit_decode": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "a8_encode_blocked": (
+        C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],
+    ),
+    "a8_decode_blocked": (
+        C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],
+    ),
     "a8_error_workspace_bytes": (C.c_size_t, []),
     "a8_error_stats": (
         C.c_int,

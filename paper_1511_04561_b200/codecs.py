@@ -218,6 +218,9 @@ class QuantizedTensor:
         self.scale_tensor = scale_tensor
         self._meta = meta  # int32[2] = [status, scale bits] written by the encoder
         self._checked = meta is None
+        self.block_size: Optional[int] = None  # per-block scales (encode_buffer(block_size=...))
+        self.block_scales: Optional[torch.Tensor] = None
+        self._block_status: Optional[torch.Tensor] = None
 
     def _host_levels(self):
         if self.levels_tensor is not None and self._levels is None:
@@ -252,6 +255,8 @@ class QuantizedTensor:
 
     @property
     def scale(self) -> float:
+        if self.block_size is not None:
+            raise UsageError("this tensor has one scale per block: use block_scales")
         if self._scale is None:
             self._finish()
         return self._scale
@@ -264,6 +269,12 @@ class QuantizedTensor:
     def _finish(self) -> None:
         """Sync on the encoder's status word; raise InputError for NaN/Inf
         input exactly where the reference does (codecs.py:251-252)."""
+        if self._block_status is not None:
+            st = int(self._block_status.cpu()[0])
+            self._block_status = None
+            if st & N.A8_STATUS_NONFINITE:
+                raise InputError("cannot encode non-finite values (NaN or Inf present)")
+            return
         if self._checked and self._scale is not None:
             return
         if self._meta is not None:
@@ -359,14 +370,26 @@ def _stream(dev: torch.device) -> int:
 # codec entry points
 
 
-def encode_buffer(x, codebook: Codebook, *, device=None, sync: bool = True) -> QuantizedTensor:
+BLOCK_SIZES = (1024, 2048, 4096)
+
+
+def encode_buffer(x, codebook: Codebook, *, device=None, sync: bool = True,
+                  block_size: Optional[int] = None) -> QuantizedTensor:
     """Quantise ``x`` to the nearest codebook values (codecs.py:244-269).
 
     Ties go to the smaller magnitude; the sign bit is set only on non-zero
     values; non-finite input raises ``InputError``.  With ``sync=False`` the
     call is fully asynchronous and the check happens when ``scale`` is read.
+
+    ``block_size`` (1024, 2048 or 4096; absmax specs only) selects per-block
+    scales: every block of that many consecutive elements is encoded exactly
+    as ``encode_buffer`` would encode it alone (its own absmax).  The scales
+    are ``q.block_scales``.  Not a reference feature (the north star's
+    optional per-block max-abs); single pass on the GPU.
     """
     spec = codebook.spec
+    if block_size is not None:
+        return _encode_blocked(x, codebook, device, sync, int(block_size))
     if _is_f64(x):  # the reference computes float64 input in float64 (codecs.py:254)
         return _encode_f64(x, codebook, device, sync)
     t, shape = as_device_f32(x, device)
@@ -389,6 +412,35 @@ def encode_buffer(x, codebook: Codebook, *, device=None, sync: bool = True) -> Q
                                 ws.numel(), None, meta.data_ptr(), stream))
     q = QuantizedTensor(codes, shape, spec, scale_tensor=meta[1:].view(torch.float32), meta=meta)
     q._keepalive = t  # input must outlive the asynchronous kernel
+    if sync:
+        q._finish()
+    return q
+
+
+def _encode_blocked(x, codebook: Codebook, device, sync: bool, block: int) -> QuantizedTensor:
+    spec = codebook.spec
+    if spec.normalization is not NormKind.ABSMAX:
+        raise ConfigError(f"per-block scales need absmax normalization, not {spec.normalization.value!r}")
+    if block not in BLOCK_SIZES:
+        raise ConfigError(f"block_size must be one of {BLOCK_SIZES}, got {block}")
+    t, shape = as_device_f32(x, device)
+    t = t.reshape(-1)
+    dev = t.device
+    n = t.numel()
+    nblk = -(-n // block)
+    book, _ = codebook.device_tables(dev)
+    with torch.cuda.device(dev):
+        stream = _stream(dev)
+        codes = torch.empty(max(n, 4), dtype=torch.uint8, device=dev)[:n]
+        scales = torch.empty(max(nblk, 1), dtype=torch.float32, device=dev)[:nblk]
+        status = torch.empty(1, dtype=torch.int32, device=dev)
+        N.check(N.lib.a8_encode_blocked(t.data_ptr(), n, block, book.data_ptr(), codes.data_ptr(),
+                                        scales.data_ptr(), status.data_ptr(), stream))
+    q = QuantizedTensor(codes, shape, spec, 1.0, scale_tensor=None)
+    q.block_size = block
+    q.block_scales = scales
+    q._block_status = status
+    q._keepalive = t
     if sync:
         q._finish()
     return q
@@ -459,6 +511,14 @@ def decode_buffer(q: QuantizedTensor, codebook: Codebook, *, device=None, out=No
     if n == 0:
         return out
     book, _ = codebook.device_tables(dev)
+    if q.block_size is not None:
+        with torch.cuda.device(dev):
+            if codes.data_ptr() % 4:
+                codes = codes.clone()
+            sc = q.block_scales.to(dev).contiguous()
+            N.check(N.lib.a8_decode_blocked(codes.data_ptr(), n, q.block_size, sc.data_ptr(), book.data_ptr(),
+                                            out.data_ptr(), _stream(dev)))
+        return out
     with torch.cuda.device(dev):
         stream = _stream(dev)
         scale_t = q.device_scale(dev)

@@ -1,0 +1,203 @@
+// Per-block max-abs codec (the north star's "optional per-block max-abs"):
+// every block of B consecutive elements (B = 1024, 2048 or 4096) gets its own
+// absmax scale, computed exactly as the reference computes a tensor's
+// (codecs.py:232-241), and is encoded with the reference decision
+// (codecs.py:254-268) -- i.e. the result equals encode_buffer applied to
+// each block separately.  Not a reference feature: it has its own oracle
+// (oracle.encode_blocked) and tests.
+//
+// Because a block fits in one CTA's registers, the encode is a single pass:
+// 4 B read + 1 B written per element (+4 B per block), no cross-CTA
+// dependency, no second read of the data.  Per block: a CTA loads B floats
+// (float4 per thread), reduces the max (warp shuffles + shared memory), 127
+// threads evaluate the decision thresholds for that scale (threshold(), the
+// reference's float64 decision), and every thread encodes its elements by a
+// branch-free 7-step search over the thresholds (the paper's method).  The
+// decode is table[c] * s_block (one RN multiply, codecs.py:281).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+
+#include "a8_core.cuh"
+#include "approx8_b200.h"
+
+namespace a8 {
+int fail(int code, const char* msg);
+}  // namespace a8
+
+using namespace a8;
+
+namespace {
+
+constexpr int kThreads = 256;
+
+
+template <int V>  // float4 groups per thread: B = 1024 * V
+__global__ void __launch_bounds__(kThreads, 4) blocked_encode_kernel(const float* __restrict__ x, int64_t n,
+                                                                 const a8_book_t* book, uint8_t* codes,
+                                                                 float* scales, unsigned int* status) {
+    constexpr int B = kThreads * 4 * V;
+    __shared__ double sV[128];
+    __shared__ uint32_t sT[128];
+    __shared__ uint8_t sCanon[128];
+    __shared__ unsigned int sRed[kThreads / 32];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    if (tid < 128) {
+        sV[tid] = book->values[tid];
+        sCanon[tid] = book->codes[tid];
+    }
+    const int D = book->ndistinct;
+    const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    const int64_t nblk = (n + B - 1) / B;
+    unsigned int bad = 0;
+    for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        const int64_t base = blk * B;
+        const int cnt = (int)min((int64_t)B, n - base);
+        const bool full = cnt == B && aligned;
+        uint4 v[V];
+        unsigned int mx = 0;  // bits * 2 (drops the sign)
+        if (full) {
+#pragma unroll
+            for (int q = 0; q < V; ++q) {
+                v[q] = __ldcs(reinterpret_cast<const uint4*>(x + base) + q * kThreads + tid);
+                mx = __vimax3_u32(mx, v[q].x * 2u, v[q].y * 2u);
+                mx = __vimax3_u32(mx, v[q].z * 2u, v[q].w * 2u);
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < V; ++q) {
+                const int e = (q * kThreads + tid) * 4;
+                uint32_t b[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) b[k] = e + k < cnt ? __float_as_uint(x[base + e + k]) : 0u;
+                v[q] = make_uint4(b[0], b[1], b[2], b[3]);
+                mx = __vimax3_u32(mx, b[0] * 2u, b[1] * 2u);
+                mx = __vimax3_u32(mx, b[2] * 2u, b[3] * 2u);
+            }
+        }
+        mx = __reduce_max_sync(0xffffffffu, mx);
+        __syncthreads();  // the previous block's sT / sRed are no longer read
+        if (lane == 0) sRed[w] = mx;
+        __syncthreads();
+        unsigned int amax = 0;
+#pragma unroll
+        for (int i = 0; i < kThreads / 32; ++i) amax = max(amax, sRed[i]);
+        amax >>= 1;
+        const float scale = amax == 0u ? 1.0f : __uint_as_float(amax);  // codecs.py:237-241
+        if (amax >= kInfBits) bad = 1u;
+        if (tid < 128) {
+            uint32_t t = kInfBits;
+            if (scale_ok(scale) && tid + 1 < D) t = threshold((double)scale, sV[tid], sV[tid + 1]);
+            sT[tid] = t;
+        }
+        if (tid == 0) scales[blk] = scale;
+        __syncthreads();
+        if (full) {
+            uint32_t* out = reinterpret_cast<uint32_t*>(codes + base);
+#pragma unroll
+            for (int q = 0; q < V; ++q) {
+                const uint32_t c0 = encode_search(v[q].x, sT, sCanon), c1 = encode_search(v[q].y, sT, sCanon);
+                const uint32_t c2 = encode_search(v[q].z, sT, sCanon), c3 = encode_search(v[q].w, sT, sCanon);
+                __stcs(out + q * kThreads + tid, c0 | (c1 << 8) | (c2 << 16) | (c3 << 24));
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < V; ++q) {
+                const int e = (q * kThreads + tid) * 4;
+                const uint32_t b[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (e + k < cnt) codes[base + e + k] = (uint8_t)encode_search(b[k], sT, sCanon);
+            }
+        }
+    }
+    if (__syncthreads_or(bad) && tid == 0) atomicOr(status, A8_STATUS_NONFINITE);
+}
+
+template <int V>
+__global__ void __launch_bounds__(kThreads) blocked_decode_kernel(const uint8_t* __restrict__ codes, int64_t n,
+                                                                 const float* __restrict__ scales,
+                                                                 const a8_book_t* book, float* __restrict__ out) {
+    constexpr int B = kThreads * 4 * V;
+    __shared__ float sTab[256];
+    sTab[threadIdx.x] = book->table[threadIdx.x];
+    __syncthreads();
+    const int tid = threadIdx.x;
+    const bool aligned = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+    const int64_t nblk = (n + B - 1) / B;
+    for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        const int64_t base = blk * B;
+        const int cnt = (int)min((int64_t)B, n - base);
+        const float s = __ldg(scales + blk);
+        if (cnt == B && aligned) {
+            uint32_t wd[V];
+#pragma unroll
+            for (int q = 0; q < V; ++q) wd[q] = __ldcs(reinterpret_cast<const uint32_t*>(codes + base) + q * kThreads + tid);
+#pragma unroll
+            for (int q = 0; q < V; ++q) {
+                const float4 d = make_float4(__fmul_rn(sTab[wd[q] & 255u], s), __fmul_rn(sTab[(wd[q] >> 8) & 255u], s),
+                                             __fmul_rn(sTab[(wd[q] >> 16) & 255u], s), __fmul_rn(sTab[wd[q] >> 24], s));
+                __stcs(reinterpret_cast<float4*>(out + base) + q * kThreads + tid, d);  // codecs.py:281
+            }
+        } else {
+            for (int i = tid; i < cnt; i += kThreads) out[base + i] = __fmul_rn(sTab[codes[base + i]], s);
+        }
+    }
+}
+
+int grid_for(int64_t nblk, int per_sm) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return (int)std::max<int64_t>(1, std::min<int64_t>(nblk, (int64_t)std::max(sms, 1) * per_sm));
+}
+
+}  // namespace
+
+extern "C" int a8_encode_blocked(const float* x, int64_t n, int64_t block, const void* book_dev, uint8_t* codes,
+                                 float* scales, uint32_t* status_out, void* stream) {
+    if (n < 0 || (n > 0 && (!x || !codes || !scales)) || !book_dev || !status_out)
+        return fail(A8_ERR_USAGE, "a8_encode_blocked: bad argument");
+    if (block != 1024 && block != 2048 && block != 4096)
+        return fail(A8_ERR_USAGE, "a8_encode_blocked: block must be 1024, 2048 or 4096");
+    if (reinterpret_cast<uintptr_t>(codes) & 3) return fail(A8_ERR_USAGE, "a8_encode_blocked: codes must be 4-byte aligned");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaMemsetAsync(status_out, 0, sizeof(uint32_t), st);
+    const int64_t nblk = (n + block - 1) / block;
+    if (nblk > 0) {
+        const a8_book_t* book = static_cast<const a8_book_t*>(book_dev);
+        const int g = grid_for(nblk, 8);
+        unsigned int* stt = reinterpret_cast<unsigned int*>(status_out);
+        if (block == 1024)
+            blocked_encode_kernel<1><<<g, kThreads, 0, st>>>(x, n, book, codes, scales, stt);
+        else if (block == 2048)
+            blocked_encode_kernel<2><<<g, kThreads, 0, st>>>(x, n, book, codes, scales, stt);
+        else
+            blocked_encode_kernel<4><<<g, kThreads, 0, st>>>(x, n, book, codes, scales, stt);
+    }
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? A8_OK : fail(A8_ERR_CUDA, cudaGetErrorString(e));
+}
+
+extern "C" int a8_decode_blocked(const uint8_t* codes, int64_t n, int64_t block, const float* scales,
+                                 const void* book_dev, float* out, void* stream) {
+    if (n < 0 || (n > 0 && (!codes || !scales || !out)) || !book_dev) return fail(A8_ERR_USAGE, "a8_decode_blocked: bad argument");
+    if (block != 1024 && block != 2048 && block != 4096)
+        return fail(A8_ERR_USAGE, "a8_decode_blocked: block must be 1024, 2048 or 4096");
+    if (reinterpret_cast<uintptr_t>(codes) & 3) return fail(A8_ERR_USAGE, "a8_decode_blocked: codes must be 4-byte aligned");
+    const int64_t nblk = (n + block - 1) / block;
+    if (nblk > 0) {
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const a8_book_t* book = static_cast<const a8_book_t*>(book_dev);
+        const int g = grid_for(nblk, 8);
+        if (block == 1024)
+            blocked_decode_kernel<1><<<g, kThreads, 0, st>>>(codes, n, scales, book, out);
+        else if (block == 2048)
+            blocked_decode_kernel<2><<<g, kThreads, 0, st>>>(codes, n, scales, book, out);
+        else
+            blocked_decode_kernel<4><<<g, kThreads, 0, st>>>(codes, n, scales, book, out);
+    }
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? A8_OK : fail(A8_ERR_CUDA, cudaGetErrorString(e));
+}

@@ -1,0 +1,68 @@
+"""Per-block max-abs codec (north star "optional per-block max-abs"; not a
+reference feature).  Parity target: the reference's encode_buffer applied to
+each block alone (oracle.encode_blocked), bit for bit; decode is
+table[c] * s_block (codecs.py:281)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1511_04561_b200 as A
+from helpers import O
+
+
+def test_oracle_blocked_is_per_block_reference_encode():
+    x = O.sample_normal(10_000, 5)
+    codes, scales = O.encode_blocked(x, "dynamic-tree", 4096)
+    assert scales.shape == (3,)
+    for b in range(3):
+        c, s = O.encode(x[b * 4096:(b + 1) * 4096], "dynamic-tree", "absmax")
+        assert np.array_equal(codes[b * 4096:(b + 1) * 4096], c) and scales[b] == np.float32(s)
+    y = O.decode_blocked(codes, scales, "dynamic-tree", 4096)
+    assert y.dtype == np.float32 and y.size == x.size
+
+
+def test_blocked_symbols_exported():
+    from paper_1511_04561_b200 import _native as N
+
+    assert callable(N.lib.a8_encode_blocked) and callable(N.lib.a8_decode_blocked)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("block", [1024, 2048, 4096])
+@pytest.mark.parametrize("n", [1, 17, 1024, 4095, 4096, 4097, 100_003, 1 << 20])
+@pytest.mark.parametrize("kind", ["dynamic-tree", "linear"])
+def test_blocked_codes_and_decode_match_oracle(cuda, block, n, kind):
+    x = O.sample_normal(n, n + block, 0.0, 0.3)
+    x[::7] *= 1e-3  # blocks with very different ranges
+    x[5::11] = 0.0
+    cb = A.build_codebook(A.DataTypeSpec(kind, "absmax"))
+    q = A.encode_buffer(torch.from_numpy(x).to(cuda), cb, block_size=block)
+    want_c, want_s = O.encode_blocked(x, kind, block)
+    assert np.array_equal(q.codes.cpu().numpy(), want_c)
+    assert np.array_equal(q.block_scales.cpu().numpy(), want_s)
+    y = A.decode_buffer(q, cb).cpu().numpy().ravel()
+    assert y.tobytes() == O.decode_blocked(want_c, want_s, kind, block).tobytes()
+
+
+@pytest.mark.gpu
+def test_blocked_edge_cases(cuda):
+    cb = A.build_codebook(A.DataTypeSpec("dynamic-tree", "absmax"))
+    z = torch.zeros(5000, device=cuda)
+    q = A.encode_buffer(z, cb, block_size=4096)
+    assert q.block_scales.cpu().tolist() == [1.0, 1.0]  # all-zero block -> scale 1 (codecs.py:240)
+    assert int(q.codes.cpu().numpy().max()) == 0
+    e = A.encode_buffer(torch.zeros(0, device=cuda), cb, block_size=1024)
+    assert e.codes.numel() == 0 and e.block_scales.numel() == 0
+    with pytest.raises(A.UsageError):
+        _ = q.scale
+    x = torch.randn(9000, device=cuda)
+    x[8191] = float("inf")
+    with pytest.raises(A.InputError):
+        A.encode_buffer(x, cb, block_size=2048)
+    with pytest.raises(A.ConfigError):
+        A.encode_buffer(x, A.build_codebook(A.DataTypeSpec("mantissa", "decade", 1)), block_size=4096)
+    with pytest.raises(A.ConfigError):
+        A.encode_buffer(x, cb, block_size=3000)
