@@ -33,11 +33,19 @@ namespace {
 constexpr int kThreads = 256;
 
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+// Blocks are streamed global -> shared by the TMA bulk engine, two stages per
+// CTA: block k+1 is in flight while block k is reduced, its thresholds
+// evaluated and its codes written.  Full blocks only; the ragged last block
+// (and unaligned inputs) take plain loads.
 template <int V>  // float4 groups per thread: B = 1024 * V
 __global__ void __launch_bounds__(kThreads, 4) blocked_encode_kernel(const float* __restrict__ x, int64_t n,
-                                                                 const a8_book_t* book, uint8_t* codes,
-                                                                 float* scales, unsigned int* status) {
+                                                                    const a8_book_t* book, uint8_t* codes,
+                                                                    float* scales, unsigned int* status) {
     constexpr int B = kThreads * 4 * V;
+    extern __shared__ __align__(128) float sBuf[];  // [2][B]
+    __shared__ __align__(8) uint64_t sBar[2];
     __shared__ double sV[128];
     __shared__ uint32_t sT[128];
     __shared__ uint8_t sCanon[128];
@@ -50,17 +58,48 @@ __global__ void __launch_bounds__(kThreads, 4) blocked_encode_kernel(const float
     const int D = book->ndistinct;
     const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
     const int64_t nblk = (n + B - 1) / B;
+    const int64_t nfull = aligned ? n / B : 0;  // blocks taken by bulk copies
+    if (tid == 0) {
+        for (int i = 0; i < 2; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sBar[i])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int64_t blk, int st) {  // thread 0: bulk copy of a full block into stage st
+        const uint32_t bar = smem_u32(&sBar[st]);
+        asm volatile("{\n\t.reg .b64 s;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 s, [%0], %1;\n\t}" ::"r"(bar),
+                     "r"((uint32_t)(B * 4))
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(sBuf + st * B)),
+            "l"(x + blk * B), "r"((uint32_t)(B * 4)), "r"(bar)
+            : "memory");
+    };
     unsigned int bad = 0;
-    for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    int it = 0;
+    if (tid == 0 && blockIdx.x < nfull) issue(blockIdx.x, 0);
+    for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x, ++it) {
+        const int st = it & 1;
         const int64_t base = blk * B;
         const int cnt = (int)min((int64_t)B, n - base);
-        const bool full = cnt == B && aligned;
+        const bool full = blk < nfull;
+        // prefetch this CTA's next block into the other stage (its previous
+        // contents were consumed in iteration it-1, closed by a barrier)
+        if (tid == 0 && blk + gridDim.x < nfull) issue(blk + gridDim.x, st ^ 1);
         uint4 v[V];
         unsigned int mx = 0;  // bits * 2 (drops the sign)
         if (full) {
+            const uint32_t bar = smem_u32(&sBar[st]);
+            const uint32_t par = (uint32_t)(it >> 1) & 1u;
+            asm volatile(
+                "{\n\t.reg .pred p;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n\t}" ::"r"(
+                    bar),
+                "r"(par)
+                : "memory");
 #pragma unroll
             for (int q = 0; q < V; ++q) {
-                v[q] = __ldcs(reinterpret_cast<const uint4*>(x + base) + q * kThreads + tid);
+                v[q] = reinterpret_cast<const uint4*>(sBuf + st * B)[q * kThreads + tid];
                 mx = __vimax3_u32(mx, v[q].x * 2u, v[q].y * 2u);
                 mx = __vimax3_u32(mx, v[q].z * 2u, v[q].w * 2u);
             }
@@ -88,12 +127,12 @@ __global__ void __launch_bounds__(kThreads, 4) blocked_encode_kernel(const float
         if (amax >= kInfBits) bad = 1u;
         if (tid < 128) {
             uint32_t t = kInfBits;
-            if (scale_ok(scale) && tid + 1 < D) t = threshold((double)scale, sV[tid], sV[tid + 1]);
+            if (scale_ok(scale) && tid + 1 < D) t = threshold_fast((double)scale, sV[tid], sV[tid + 1]);
             sT[tid] = t;
         }
         if (tid == 0) scales[blk] = scale;
         __syncthreads();
-        if (full) {
+        if (cnt == B && aligned) {
             uint32_t* out = reinterpret_cast<uint32_t*>(codes + base);
 #pragma unroll
             for (int q = 0; q < V; ++q) {
@@ -170,11 +209,11 @@ extern "C" int a8_encode_blocked(const float* x, int64_t n, int64_t block, const
         const int g = grid_for(nblk, 8);
         unsigned int* stt = reinterpret_cast<unsigned int*>(status_out);
         if (block == 1024)
-            blocked_encode_kernel<1><<<g, kThreads, 0, st>>>(x, n, book, codes, scales, stt);
+            blocked_encode_kernel<1><<<g, kThreads, 2 * 1024 * sizeof(float), st>>>(x, n, book, codes, scales, stt);
         else if (block == 2048)
-            blocked_encode_kernel<2><<<g, kThreads, 0, st>>>(x, n, book, codes, scales, stt);
+            blocked_encode_kernel<2><<<g, kThreads, 2 * 2048 * sizeof(float), st>>>(x, n, book, codes, scales, stt);
         else
-            blocked_encode_kernel<4><<<g, kThreads, 0, st>>>(x, n, book, codes, scales, stt);
+            blocked_encode_kernel<4><<<g, kThreads, 2 * 4096 * sizeof(float), st>>>(x, n, book, codes, scales, stt);
     }
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? A8_OK : fail(A8_ERR_CUDA, cudaGetErrorString(e));

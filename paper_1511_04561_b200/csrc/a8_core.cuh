@@ -118,6 +118,21 @@ A8_HD uint32_t threshold(double s, double v_lo, double v_hi) {
     return hi;
 }
 
+// threshold() with one predicate evaluation.  g = RN32(m) is within half a
+// float32 ulp of the real midpoint; the float64 decision resolves the
+// neighbours g-1 (half an ulp or more below) and g+1 (above) correctly
+// because its own rounding error is ~2^-29 of a float32 ulp.  Hence
+// T is g or g+1 and pred(g) tells which.  Near the ends of the float32
+// range (g < 8 or g within 8 of Inf) the walk + bisection is used.
+// tests/cpp/threshold_window.cpp checks it against threshold() over
+// millions of normal, tiny and huge scales for all four codebooks.
+A8_HD uint32_t threshold_fast(double s, double v_lo, double v_hi) {
+    const double m = 0.5 * (v_lo + v_hi) * s;
+    const uint32_t g = m < 3.4028234663852886e38 ? f32_bits((float)m) : kInfBits;
+    if (g < 8u || g >= kInfBits - 8u) return threshold(s, v_lo, v_hi);
+    return picks_upper(g, s, v_lo, v_hi) ? g : g + 1u;
+}
+
 A8_HD bool scale_ok(float s) {
     const uint32_t b = f32_bits(s);
     return b != 0u && b < kInfBits;  // positive, finite, non-zero

@@ -530,7 +530,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                 if (ctid < 128) {
                     uint32_t t = kInfBits;
                     if (scale_ok(scale) && ctid + 1 < p.book->ndistinct)
-                        t = threshold((double)scale, sV[ctid], sV[ctid + 1]);
+                        t = threshold_fast((double)scale, sV[ctid], sV[ctid + 1]);
                     sT[ctid] = t;
                 }
                 if (amax >= kInfBits && ctid == 0) atomicOr(&p.head->status, A8_STATUS_NONFINITE);
@@ -585,7 +585,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                     const float scale = amax == 0u ? 1.0f : __uint_as_float(amax);
                     uint32_t t = kInfBits;
                     if (ctid < 128) {
-                        if (scale_ok(scale) && ctid + 1 < p.book->ndistinct) t = threshold((double)scale, sV[ctid], sV[ctid + 1]);
+                        if (scale_ok(scale) && ctid + 1 < p.book->ndistinct) t = threshold_fast((double)scale, sV[ctid], sV[ctid + 1]);
                         sT[ctid] = t;
                     }
                     const int nf = nbar_popc(kBarC, kConsumers, ctid < 127 && t < kInfBits);

@@ -221,6 +221,6 @@ def test_parallel_threshold_window(tmp_path):
                     str(root / "tests" / "cpp" / "threshold_window.cpp"),
                     str(root / "paper_1511_04561_b200" / "csrc" / "a8_codebook.cpp"), "-o", str(exe)], check=True)
     out = subprocess.run([str(exe), "1500"], capture_output=True, text=True)
-    total, bad, fallback = (int(v) for v in out.stdout.split())
-    assert out.returncode == 0 and bad == 0, out.stdout
-    assert total > 700_000 and fallback < total // 100
+    total, bad, fallback, bad_fast = (int(v) for v in out.stdout.split())
+    assert out.returncode == 0 and bad == 0 and bad_fast == 0, out.stdout
+    assert total > 700_000 and fallback < total // 50

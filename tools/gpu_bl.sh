@@ -1,8 +1,5 @@
-for v in base bl6 bl8; do
-  if [ $v = base ]; then lib=paper_1511_04561_b200/_lib/libapprox8_b200.so; else lib=paper_1511_04561_b200/_lib_var/$v/libapprox8_b200.so; fi
-  A8_LIB=$lib python tools/prof_blocked.py | python -c "
-import sys,json
-for l in sys.stdin:
-    r=json.loads(l)
-    if r['log2'] in (26,30): print('$v', r['log2'], r['block'], round(r['encode_us'],1), round(r['encode_GBps']))"
-done
+timeout 900 python -m pytest tests/test_blocked.py -m gpu -x -q 2>&1 | tail -1
+python tools/prof_blocked.py > gpurun_out/blocked.jsonl; python -c "
+import json
+for l in open('gpurun_out/blocked.jsonl'):
+    r=json.loads(l); print(r['log2'], r['block'], round(r['encode_us'],1), round(r['encode_GBps']), round(r['decode_us'],1), round(r['decode_GBps']))"
