@@ -340,6 +340,19 @@ def run_b200(args, nranks, rank, local_rank):
                 "algo": os.environ.get("NCCL_ALGO", "default"), "speedup_8bit": value / (nranks * 4.0 * n / (nms * 1e-3) / 1e9)}
         del flat
 
+    # NVLink roofline of the exchange: bytes each rank must
+    # receive over NVLink per step / the measured peer-copy bandwidth
+    # (770 GB/s per direction, B200_PROFILING.md), against the step time
+    nvlink = None
+    if nranks > 1:
+        if args.mode == "allgather":
+            ingress = (nranks - 1) * (n + 4 * len(ALEXNET))
+        else:  # two_round: an all-to-all of 8-bit shards, then an all-gather of them
+            ingress = 2 * (nranks - 1) * n / nranks
+        bound_ms = ingress / 770e9 * 1e3
+        nvlink = {"ingress_bytes_per_rank": ingress, "peer_GBps": 770.0, "bound_ms": bound_ms,
+                  "frac": bound_ms / ms, "fp32_ring_allreduce_ingress_bytes": 2 * (nranks - 1) / nranks * 4.0 * n}
+
     # e2e: host buffers through the public API, copies inside the timed region.
     # Every step copies its gradients host->device (pinned), exchanges them
     # and copies the averaged result device->host.  Steps are software
@@ -442,6 +455,7 @@ def run_b200(args, nranks, rank, local_rank):
             "e2e": e2e, "clocks": clk.summary(), "gpu_launches": int(sum(launches.values())),
             "gpu_launches_per_step": {k: v / args.steps for k, v in launches.items()},
             "nccl_fp32_allreduce": nccl,
+            "nvlink_roofline": nvlink,
         }
         print(json.dumps(line), flush=True)
 
