@@ -597,11 +597,16 @@ class LocalExchange:
 
 
 class DDPHookState:
-    def __init__(self, spec: DataTypeSpec, group=None, mode: str = "allgather"):
-        self.exchange = GradientExchange(spec, group, mode, "avg")
+    """State of ``a8_comm_hook``: one ``GradientExchange`` (op="avg") shared by
+    the buckets of a ``DistributedDataParallel`` model.  ``codec`` / ``comm``
+    as for ``GradientExchange`` (tests inject CPU stand-ins)."""
+
+    def __init__(self, spec: DataTypeSpec, group=None, mode: str = "allgather", codec: Optional[SegmentCodec] = None,
+                 comm=None, check: str = "deferred"):
+        self.exchange = GradientExchange(spec, group, mode, "avg", check=check, codec=codec, comm=comm)
 
 
-def a8_comm_hook(state: DDPHookState, bucket) -> torch.futures.Future:
+def a8_comm_hook(state, bucket):
     """``DistributedDataParallel.register_comm_hook(state, a8_comm_hook)``:
     the bucket's per-parameter gradient views are exchanged 8-bit with one
     scale per parameter (the reference's per-tensor seam, mlp.py:367-369)."""
@@ -610,3 +615,9 @@ def a8_comm_hook(state: DDPHookState, bucket) -> torch.futures.Future:
     fut: torch.futures.Future = torch.futures.Future()
     fut.set_result(bucket.buffer())
     return fut
+
+
+# DDP checks the hook's annotations by identity (not as strings, which is what
+# `from __future__ import annotations` would leave here)
+a8_comm_hook.__annotations__ = {"state": DDPHookState, "bucket": dist.GradBucket,
+                                "return": torch.futures.Future[torch.Tensor]}

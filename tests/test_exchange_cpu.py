@@ -166,3 +166,61 @@ def test_model_parallel_fc_orchestration(nranks):
     for r in range(nranks):
         assert np.array_equal(res[r][0], y_want)
         assert np.array_equal(res[r][1], dx_want)
+
+
+# ---------------------------------------------------------------------------
+# the DDP comm hook with a real DistributedDataParallel model (gloo, 2 ranks)
+
+
+def _ddp_model():
+    torch.manual_seed(0)
+    return torch.nn.Sequential(torch.nn.Linear(20, 30), torch.nn.ReLU(), torch.nn.Linear(30, 5))
+
+
+def _ddp_inputs(rank):
+    g = torch.Generator().manual_seed(100 + rank)
+    return torch.randn(8, 20, generator=g), torch.randn(8, 5, generator=g)
+
+
+def _local_grads(rank):
+    m = _ddp_model()
+    x, y = _ddp_inputs(rank)
+    torch.nn.functional.mse_loss(m(x), y).backward()
+    return [p.grad.numpy().copy() for p in m.parameters()]
+
+
+def _ddp_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        spec = SPECS[0]
+        model = torch.nn.parallel.DistributedDataParallel(_ddp_model())
+        model.register_comm_hook(A.DDPHookState(spec, codec=NumpyCodec(spec), check="sync"), A.a8_comm_hook)
+        x, y = _ddp_inputs(rank)
+        torch.nn.functional.mse_loss(model(x), y).backward()
+        per_rank = [_local_grads(r) for r in range(world)]
+        ok = True
+        for i, p in enumerate(model.parameters()):
+            want = O.exchange_allgather([[per_rank[r][i]] for r in range(world)], spec.kind.value,
+                                        spec.normalization.value, spec.decades, "avg")[0]
+            ok &= bool(np.array_equal(p.grad.numpy(), want))
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ddp_comm_hook_gloo_world_size_2():
+    """register_comm_hook(DDPHookState, a8_comm_hook) on a real DDP model:
+    every parameter's gradient is the 8-bit all-gather average of the ranks'
+    local gradients (per-parameter scales), bit-exact against the oracle."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ddp_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    results = dict(q.get(timeout=5) for _ in range(2))
+    assert results == {0: True, 1: True}

@@ -127,3 +127,53 @@ def test_dp_training_parity_config2(cuda):
         diffs.append(100.0 * (e8 - e32))
         assert e32 < 0.2, e32  # the task is learnable in 3 epochs
     assert all(abs(d) < 1.0 for d in diffs), diffs
+
+
+def _ddp_nccl_worker(port, q):
+    import os
+
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    try:
+        spec = A.DataTypeSpec("dynamic-tree", "absmax")
+        torch.manual_seed(0)
+        model = torch.nn.Sequential(torch.nn.Linear(64, 128), torch.nn.ReLU(), torch.nn.Linear(128, 10)).to(dev)
+        ref = torch.nn.Sequential(torch.nn.Linear(64, 128), torch.nn.ReLU(), torch.nn.Linear(128, 10)).to(dev)
+        ref.load_state_dict(model.state_dict())
+        ddp = torch.nn.parallel.DistributedDataParallel(model, device_ids=[0])
+        ddp.register_comm_hook(A.DDPHookState(spec, check="sync"), A.a8_comm_hook)
+        x = torch.randn(32, 64, device=dev)
+        y = torch.randn(32, 10, device=dev)
+        torch.nn.functional.mse_loss(ddp(x), y).backward()
+        torch.nn.functional.mse_loss(ref(x), y).backward()
+        ok = True
+        for p, r in zip(model.parameters(), ref.parameters()):
+            want = O.roundtrip(r.grad.cpu().numpy(), "dynamic-tree", "absmax")  # N = 1: exchange == round trip
+            ok &= p.grad.cpu().numpy().tobytes() == want.tobytes()
+        q.put(ok)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ddp_comm_hook_nccl_single_rank(cuda):
+    """The DDP hook on the GPU with NCCL: a real DistributedDataParallel
+    bucket goes through the sm_100a codec; at one rank every parameter's
+    gradient equals the reference round trip of its local gradient."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_ddp_nccl_worker, args=(port, q))
+    p.start()
+    p.join(timeout=300)
+    assert q.get(timeout=5) is True
