@@ -248,3 +248,15 @@ def test_make_quantizer_records_fused_stats(cuda):
     got = stats.summary()["backward"][0]
     assert got[0] == pytest.approx(a / x64.size, rel=REL, abs=0.0)
     assert got[1] == pytest.approx(100.0 * r / nz, rel=REL, abs=0.0)
+
+
+@pytest.mark.gpu
+def test_cli_bench_error_matches_reference_csv(cuda, tmp_path):
+    """`python -m paper_1511_04561_b200.errorbench` mirrors the reference CLI's
+    bench-error (cli.py:119-125): same CSV text for the same seed and count."""
+    out = tmp_path / "suite.csv"
+    assert EB.main(["--n", "20000", "--seed", "5", "--out", str(out)]) == 0
+    assert out.read_text() == G["suite_seed5"]["csv"]
+    tab = tmp_path / "suite.txt"
+    assert EB.main(["--n", "20000", "--seed", "5", "--table", "--out", str(tab)]) == 0
+    assert tab.read_text().splitlines()[0].startswith("distribution")

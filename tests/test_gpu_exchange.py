@@ -223,3 +223,14 @@ def test_deferred_checks_every_call(cuda):
         ex.synchronize()
     ex(good, out=outs)
     ex.synchronize()  # clean again
+
+
+def test_functional_exchange_world_size_one(cuda):
+    """exchange(tensors, spec): the one-shot form (check="sync")."""
+    spec = A.DataTypeSpec("linear", "absmax")
+    gs = grads(0, SMALL, seed=21)
+    ts = [torch.from_numpy(g).to(cuda) for g in gs]
+    out = A.exchange(ts, spec)
+    assert out is not None
+    for t, g in zip(ts, gs):
+        assert t.cpu().numpy().tobytes() == O.roundtrip(g, "linear", "absmax").tobytes()
