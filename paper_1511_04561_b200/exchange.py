@@ -471,6 +471,11 @@ class GradientExchange:
         status1 = self._buffer("status1", 4, dev)
         self.codec.decode(pouts, poffs, [p.tensor for p in mine], self.cb, recv, 0, L, L, B, 0, B,
                           nranks, 1 if self.op == "avg" else 0, plan.status_slot, 1, status1)
+        # round-2 blocks: chunk_elems of gathered data per block, as for allgather
+        K2 = 1 if nranks == 1 else int(min(self.max_chunks, max(1, -(-L // max(16, self.chunk_elems // nranks)))))
+        if K2 > 1:
+            self._two_round_pipelined_r2(outs, plan, nranks, rank, dev, mine, pouts, poffs, status1, K2)
+            return
         # round 2: re-encode my shard, one scale per piece, into my gather slot
         gathered = self._buffer("gather2", nranks * B, dev)
         slot = rank * B
@@ -491,6 +496,58 @@ class GradientExchange:
         status = self._status_word(dev)
         self.codec.decode(fouts, foffs, fidx, self.cb, gathered, 0, L, L, B, sbs, 0, 1, 0,
                           plan.status_slot, nranks, status)
+        self._collect_status(status)
+
+
+    def _two_round_pipelined_r2(self, outs, plan: Plan, nranks, rank, dev, mine, pouts, poffs, status1, K2):
+        """Round 2 of two_round with the all-gather split into K2 blocks: block
+        k holds chunk k (Ck elements) of every rank's shard, laid out
+        [r0 codes | r0 scales+status | r1 ...].  One re-encode launch writes
+        all K2 blocks of my shard (per-piece scales, as for K2 = 1), then
+        block k is all-gathered in place while block k-1 is decoded.  The
+        pieces and scales are those of the unpipelined round 2, so the result
+        does not depend on K2."""
+        L = plan.shard
+        Ck = round16(-(-L // K2))
+        K2 = -(-L // Ck)
+        P = Ck + plan.gap  # one rank's part of a block
+        BS = nranks * P
+        gathered = self._buffer("gather2p", K2 * BS, dev)
+        slot = rank * P
+        status_off = slot + Ck + 4 * plan.status_slot
+        if mine:
+            self.codec.encode(pouts, poffs, [p.idx for p in mine], self.cb, gathered, slot, slot + Ck, Ck, BS,
+                              BS // 4, K2, status_off, status_in=status1)
+        else:
+            for k in range(K2):
+                gathered[k * BS + status_off:k * BS + status_off + 4].copy_(status1)
+        start = getattr(self.comm, "all_gather_async", None)
+        handles = []
+        for k in range(K2):
+            blk = gathered[k * BS:(k + 1) * BS]
+            if start is not None:
+                handles.append(start(blk, blk[slot:slot + P]))
+            else:
+                self.comm.all_gather(blk, blk[slot:slot + P])
+                handles.append(None)
+        # pieces of every rank's shard, cut at chunk boundaries
+        sub: list = [[] for _ in range(K2)]
+        for p in plan.pieces:
+            o0 = p.flat - p.shard * L  # piece start inside its shard
+            a = o0
+            while a < o0 + p.n:
+                k = a // Ck
+                b = min(o0 + p.n, (k + 1) * Ck)
+                view = outs[p.tensor].view(-1)[p.start + (a - o0):p.start + (b - o0)]
+                sub[k].append((view, p.shard * Ck + (a - k * Ck), p.idx))
+                a = b
+        status = self._status_word(dev)
+        for k in range(K2):
+            if handles[k] is not None:
+                handles[k].wait()
+            self.codec.decode([v for v, f, i in sub[k]], [f for v, f, i in sub[k]], [i for v, f, i in sub[k]],
+                              self.cb, gathered, k * BS, k * BS + Ck, Ck, P, P // 4, 0, 1, 0,
+                              plan.status_slot, nranks, status if k == K2 - 1 else None)
         self._collect_status(status)
 
 

@@ -224,3 +224,23 @@ def test_ddp_comm_hook_gloo_world_size_2():
         p.join(timeout=300)
     results = dict(q.get(timeout=5) for _ in range(2))
     assert results == {0: True, 1: True}
+
+
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_pipelined_two_round_orchestration(nranks):
+    """Round-2 all-gather in K > 1 blocks (test codec, CPU): bit-exact with the
+    unchunked two_round oracle."""
+    spec = SPECS[0]
+
+    def body(rank, comm):
+        ex = A.GradientExchange(spec, mode="two_round", op="avg", check="sync", codec=NumpyCodec(spec), comm=comm,
+                                chunk_elems=256)
+        ts = [torch.from_numpy(g) for g in grads_for(rank)]
+        ex(ts)
+        return [t.numpy().copy() for t in ts]
+
+    res = run_virtual_ranks(nranks, body)
+    want = expected(nranks, spec, "two_round", "avg")
+    for r in range(nranks):
+        for a, b in zip(res[r], want):
+            assert np.array_equal(a, b), r

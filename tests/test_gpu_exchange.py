@@ -234,3 +234,24 @@ def test_functional_exchange_world_size_one(cuda):
     assert out is not None
     for t, g in zip(ts, gs):
         assert t.cpu().numpy().tobytes() == O.roundtrip(g, "linear", "absmax").tobytes()
+
+
+@pytest.mark.parametrize("nranks", [2, 3, 8])
+@pytest.mark.parametrize("chunk", [4096, 50000])
+def test_pipelined_two_round_chunks(nranks, chunk, cuda):
+    """two_round with the round-2 all-gather split into K > 1 blocks: same
+    pieces and scales as K = 1, so bit-exact against the unchunked oracle."""
+    spec = A.DataTypeSpec("dynamic-tree", "absmax")
+
+    def body(rank, comm):
+        ex = A.GradientExchange(spec, mode="two_round", check="sync", comm=comm, chunk_elems=chunk)
+        ts = [torch.from_numpy(g).to(cuda) for g in grads(rank, SMALL + ALEXNET[:2], 9)]
+        ex(ts)
+        torch.cuda.synchronize()
+        return [t.cpu().numpy() for t in ts]
+
+    res = run_virtual_ranks(nranks, body)
+    want = O.exchange_two_round([grads(r, SMALL + ALEXNET[:2], 9) for r in range(nranks)], "dynamic-tree", "absmax")
+    for r in range(nranks):
+        for a, b in zip(res[r], want):
+            assert a.tobytes() == b.tobytes(), (r, nranks, chunk)
