@@ -1028,18 +1028,20 @@ __global__ void __launch_bounds__(kRThreads, 1) resident_encode_kernel(const __g
 constexpr int kDecGroups = A8_DEC_GROUPS;
 constexpr int kDecChunkD = kDecThreads * kDecGroups * 4;  // 4096 elements
 
-// 4 copies: 1-4 copies measured equal; 8 and 32 (lane-private) were slower
-// (the larger shared-memory carveout costs more than the conflicts save).
-__host__ __device__ __forceinline__ int dec_rep_shift(int) { return 2; }
+
 
 // 4 CTAs/SM (64 registers).  Measured: 2 CTAs (96 registers, the default
 // when min-blocks is 1) 30% slower, 5-8 CTAs (48-32 registers) slower at 2^30.
 __global__ void __launch_bounds__(kDecThreads, 4) decode_kernel(const __grid_constant__ DecParams p) {
-    extern __shared__ float sTab[];  // [nranks][256][rep]
+    // One UNSCALED decode table, one copy per lane ([256][32]: lane j reads
+    // column j, so table lookups never conflict on a bank), built once per
+    // CTA; the per-rank scale is applied in registers: fl(table[c] * s_r) is
+    // exactly the pre-scaled entry of codecs.py:281.  No per-segment table
+    // rebuild, and the table size does not grow with the rank count.
+    extern __shared__ float sTab[];  // [256][32]
+    __shared__ float sScale[kMaxRanks];
     const int tid = threadIdx.x;
-    const int rsh = dec_rep_shift(p.nranks);
-    const int rep = tid & ((1 << rsh) - 1);
-    const int tstride = 256 << rsh;  // floats per rank table
+    const int lane = tid & 31;
     const DecSegD* segs = p.segs_dev ? p.segs_dev : p.segs;
     const int R = p.nranks;
     const int64_t L = p.lay.block_len;
@@ -1049,6 +1051,15 @@ __global__ void __launch_bounds__(kDecThreads, 4) decode_kernel(const __grid_con
     int cur = -1;
     int64_t cbase = 0;
     const uint8_t* src = nullptr;  // codes of rank 0 for this segment, flat-indexed
+
+    {
+        static_assert(kDecThreads == 256, "one code per thread");
+        const float v = p.book->table[tid];
+        float4* d = reinterpret_cast<float4*>(sTab + tid * 32);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) d[q] = make_float4(v, v, v, v);
+    }
+    const float* tl = sTab + lane;  // this lane's column: entry c at tl[c * 32]
 
     if (p.status_out && blockIdx.x == 0) {
         __shared__ unsigned int sSt;
@@ -1076,22 +1087,18 @@ __global__ void __launch_bounds__(kDecThreads, 4) decode_kernel(const __grid_con
         }
         return lo;
     };
+    auto dec = [&](uint32_t code, float s) { return __fmul_rn(tl[code * 32u], s); };  // codecs.py:281
 
     for (int64_t c = blockIdx.x; c < p.total; c += gridDim.x) {
         const int lo = seg_of(c);
         const DecSegD sg = segs[lo];
         if (lo != cur) {
-            __syncthreads();
+            __syncthreads();  // (also orders the table build before the first lookups)
             const int64_t j = sg.flat_off / L;
-            for (int i = tid; i < R * 256; i += kDecThreads) {
-                const int r = i >> 8, code = i & 255;
-                const float* sc = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.lay.scales) +
-                                                                 (int64_t)r * p.lay.rank_stride) +
-                                  j * p.lay.scale_block_stride + sg.scale_idx;
-                const float v = __fmul_rn(p.book->table[code], __ldcg(sc));  // codecs.py:281
-                float* d = sTab + r * tstride + (code << rsh);
-                for (int q = 0; q < (1 << rsh); ++q) d[q] = v;
-            }
+            if (tid < R)
+                sScale[tid] = __ldcg(reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.lay.scales) +
+                                                                    (int64_t)tid * p.lay.rank_stride) +
+                                     j * p.lay.scale_block_stride + sg.scale_idx);
             __syncthreads();
             cur = lo;
             cbase = sg.cstart;
@@ -1107,26 +1114,38 @@ __global__ void __launch_bounds__(kDecThreads, 4) decode_kernel(const __grid_con
                 uint32_t w[kDecGroups];
 #pragma unroll
                 for (int q = 0; q < kDecGroups; ++q) w[q] = ld_stream_u32(src + f0 + q * (kDecThreads * 4) + tid * 4);
+                const float s0 = sScale[0];
 #pragma unroll
                 for (int q = 0; q < kDecGroups; ++q) {
-                    acc[q][0] = sTab[((w[q] & 255u) << rsh) + rep];
-                    acc[q][1] = sTab[(((w[q] >> 8) & 255u) << rsh) + rep];
-                    acc[q][2] = sTab[(((w[q] >> 16) & 255u) << rsh) + rep];
-                    acc[q][3] = sTab[((w[q] >> 24) << rsh) + rep];
+                    acc[q][0] = dec(w[q] & 255u, s0);
+                    acc[q][1] = dec((w[q] >> 8) & 255u, s0);
+                    acc[q][2] = dec((w[q] >> 16) & 255u, s0);
+                    acc[q][3] = dec(w[q] >> 24, s0);
                 }
             }
+            // rank r+1's code words are loaded before rank r's are decoded
+            uint32_t wn[kDecGroups];
+            if (R > 1) {
+                const uint8_t* s1 = src + p.lay.rank_stride + f0 + tid * 4;
+#pragma unroll
+                for (int q = 0; q < kDecGroups; ++q) wn[q] = ld_stream_u32(s1 + q * (kDecThreads * 4));
+            }
             for (int r = 1; r < R; ++r) {
-                const uint8_t* sr = src + (int64_t)r * p.lay.rank_stride + f0 + tid * 4;
-                const float* T = sTab + r * tstride;
+                const float sc = sScale[r];
                 uint32_t w[kDecGroups];
 #pragma unroll
-                for (int q = 0; q < kDecGroups; ++q) w[q] = ld_stream_u32(sr + q * (kDecThreads * 4));
+                for (int q = 0; q < kDecGroups; ++q) w[q] = wn[q];
+                if (r + 1 < R) {
+                    const uint8_t* sn = src + (int64_t)(r + 1) * p.lay.rank_stride + f0 + tid * 4;
+#pragma unroll
+                    for (int q = 0; q < kDecGroups; ++q) wn[q] = ld_stream_u32(sn + q * (kDecThreads * 4));
+                }
 #pragma unroll
                 for (int q = 0; q < kDecGroups; ++q) {
-                    acc[q][0] = __fadd_rn(acc[q][0], T[((w[q] & 255u) << rsh) + rep]);
-                    acc[q][1] = __fadd_rn(acc[q][1], T[(((w[q] >> 8) & 255u) << rsh) + rep]);
-                    acc[q][2] = __fadd_rn(acc[q][2], T[(((w[q] >> 16) & 255u) << rsh) + rep]);
-                    acc[q][3] = __fadd_rn(acc[q][3], T[((w[q] >> 24) << rsh) + rep]);
+                    acc[q][0] = __fadd_rn(acc[q][0], dec(w[q] & 255u, sc));
+                    acc[q][1] = __fadd_rn(acc[q][1], dec((w[q] >> 8) & 255u, sc));
+                    acc[q][2] = __fadd_rn(acc[q][2], dec((w[q] >> 16) & 255u, sc));
+                    acc[q][3] = __fadd_rn(acc[q][3], dec(w[q] >> 24, sc));
                 }
             }
 #pragma unroll
@@ -1151,9 +1170,9 @@ __global__ void __launch_bounds__(kDecThreads, 4) decode_kernel(const __grid_con
             }
         } else {
             for (int64_t i = tid; i < cnt; i += kDecThreads) {
-                float a = sTab[((uint32_t)src[f0 + i] << rsh) + rep];
+                float a = dec(src[f0 + i], sScale[0]);
                 for (int r = 1; r < R; ++r)
-                    a = __fadd_rn(a, sTab[r * tstride + ((uint32_t)src[(int64_t)r * p.lay.rank_stride + f0 + i] << rsh) + rep]);
+                    a = __fadd_rn(a, dec(src[(int64_t)r * p.lay.rank_stride + f0 + i], sScale[r]));
                 if (p.op == 1 && R > 1) a = pow2 ? __fmul_rn(a, invN) : __fdiv_rn(a, (float)R);
                 sg.out[base + i] = a;
             }
@@ -1161,7 +1180,7 @@ __global__ void __launch_bounds__(kDecThreads, 4) decode_kernel(const __grid_con
     }
 }
 
-static size_t dec_smem(int nranks) { return (size_t)nranks * (256u << dec_rep_shift(nranks)) * sizeof(float); }
+static size_t dec_smem(int) { return 256u * 32u * sizeof(float); }  // lane-private table copies
 
 // ---------------------------------------------------------------------------
 // host launchers
