@@ -1039,7 +1039,7 @@ __global__ void __launch_bounds__(kDecThreads, 4) decode_kernel(const __grid_con
     // exactly the pre-scaled entry of codecs.py:281.  No per-segment table
     // rebuild, and the table size does not grow with the rank count.
     extern __shared__ float sTab[];  // [256][32]
-    __shared__ float sScale[kMaxRanks];
+    __shared__ float sScale[kInlineSegs * kMaxRanks];  // [segment][rank] (inline plans), else [rank]
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const DecSegD* segs = p.segs_dev ? p.segs_dev : p.segs;
@@ -1060,6 +1060,19 @@ __global__ void __launch_bounds__(kDecThreads, 4) decode_kernel(const __grid_con
         for (int q = 0; q < 8; ++q) d[q] = make_float4(v, v, v, v);
     }
     const float* tl = sTab + lane;  // this lane's column: entry c at tl[c * 32]
+    // inline plans: every (segment, rank) scale is loaded once, up front, in
+    // parallel (one round trip instead of one per segment switch)
+    const bool preload = p.nseg <= kInlineSegs;
+    if (preload) {
+        for (int i = tid; i < R * p.nseg; i += kDecThreads) {
+            const int sgi = i / R, r = i % R;
+            const DecSegD& d = segs[sgi];
+            sScale[i] = __ldcg(reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.lay.scales) +
+                                                              (int64_t)r * p.lay.rank_stride) +
+                               (d.flat_off / L) * p.lay.scale_block_stride + d.scale_idx);
+        }
+    }
+    const float* scl = sScale;  // the current segment's per-rank scales
 
     if (p.status_out && blockIdx.x == 0) {
         __shared__ unsigned int sSt;
@@ -1093,13 +1106,18 @@ __global__ void __launch_bounds__(kDecThreads, 4) decode_kernel(const __grid_con
         const int lo = seg_of(c);
         const DecSegD sg = segs[lo];
         if (lo != cur) {
-            __syncthreads();  // (also orders the table build before the first lookups)
             const int64_t j = sg.flat_off / L;
-            if (tid < R)
-                sScale[tid] = __ldcg(reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.lay.scales) +
-                                                                    (int64_t)tid * p.lay.rank_stride) +
-                                     j * p.lay.scale_block_stride + sg.scale_idx);
-            __syncthreads();
+            if (preload) {
+                if (cur < 0) __syncthreads();  // table + scales complete before the first lookups
+                scl = sScale + lo * R;
+            } else {
+                __syncthreads();  // (also orders the table build before the first lookups)
+                if (tid < R)
+                    sScale[tid] = __ldcg(reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.lay.scales) +
+                                                                        (int64_t)tid * p.lay.rank_stride) +
+                                         j * p.lay.scale_block_stride + sg.scale_idx);
+                __syncthreads();
+            }
             cur = lo;
             cbase = sg.cstart;
             src = p.lay.codes + j * gap;
@@ -1114,7 +1132,7 @@ __global__ void __launch_bounds__(kDecThreads, 4) decode_kernel(const __grid_con
                 uint32_t w[kDecGroups];
 #pragma unroll
                 for (int q = 0; q < kDecGroups; ++q) w[q] = ld_stream_u32(src + f0 + q * (kDecThreads * 4) + tid * 4);
-                const float s0 = sScale[0];
+                const float s0 = scl[0];
 #pragma unroll
                 for (int q = 0; q < kDecGroups; ++q) {
                     acc[q][0] = dec(w[q] & 255u, s0);
@@ -1131,7 +1149,7 @@ __global__ void __launch_bounds__(kDecThreads, 4) decode_kernel(const __grid_con
                 for (int q = 0; q < kDecGroups; ++q) wn[q] = ld_stream_u32(s1 + q * (kDecThreads * 4));
             }
             for (int r = 1; r < R; ++r) {
-                const float sc = sScale[r];
+                const float sc = scl[r];
                 uint32_t w[kDecGroups];
 #pragma unroll
                 for (int q = 0; q < kDecGroups; ++q) w[q] = wn[q];
@@ -1170,9 +1188,9 @@ __global__ void __launch_bounds__(kDecThreads, 4) decode_kernel(const __grid_con
             }
         } else {
             for (int64_t i = tid; i < cnt; i += kDecThreads) {
-                float a = dec(src[f0 + i], sScale[0]);
+                float a = dec(src[f0 + i], scl[0]);
                 for (int r = 1; r < R; ++r)
-                    a = __fadd_rn(a, dec(src[(int64_t)r * p.lay.rank_stride + f0 + i], sScale[r]));
+                    a = __fadd_rn(a, dec(src[(int64_t)r * p.lay.rank_stride + f0 + i], scl[r]));
                 if (p.op == 1 && R > 1) a = pow2 ? __fmul_rn(a, invN) : __fdiv_rn(a, (float)R);
                 sg.out[base + i] = a;
             }

@@ -1,9 +1,14 @@
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -1 > gpurun_out/pt.txt
 for v in base head; do
   if [ $v = base ]; then lib=$PWD/paper_1511_04561_b200/_lib/libapprox8_b200.so; else lib=$PWD/paper_1511_04561_b200/_lib_var/$v/libapprox8_b200.so; fi
-  (cd tools && A8_LIB=$lib python prof_decode_reduce.py | sed "s/^/$v /")
-  for c in alexnet big; do A8_LIB=$lib timeout 300 python tools/prof_codec.py --case $c | python -c "
+  (cd tools && A8_LIB=$lib python prof_decode_reduce.py | python -c "
 import sys,json
 for l in sys.stdin:
-    r=json.loads(l); print('$v', r['case'], 'enc', round(r['encode']['ms']*1e3,1), 'us dec', round(r['decode']['ms']*1e3,1))"; done
+    r=json.loads(l); print('$v N', r['nranks'], round(r['decode_reduce_us'],1))")
+  A8_LIB=$lib python tools/sweep_config4.py --max-log2 22 | python -c "
+import sys,json
+for l in sys.stdin:
+    r=json.loads(l)
+    if r['spec']=='dynamic-tree/absmax': print('$v', r['log2'], 'dec', round(r['decode_us'],1))"
 done
+cat gpurun_out/pt.txt
