@@ -163,6 +163,15 @@ int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_dev, int norm
               size_t workspace_bytes, const uint32_t* status_in, uint32_t* status_out,
               void* stream);
 
+/* roundtrip (codecs.py:285-288) fused: decode(encode(x)) for nseg float32
+ * tensors in one launch, written to outs[i] (same length as segs[i]); the
+ * codes are never stored.  scales_out[scale_idx] receives each scale,
+ * status_out (device uint32) the A8_STATUS_* bits.  Only for calls that fit
+ * in the GPU's shared memory (<= 32 tensors, ~7.5M elements); otherwise it
+ * returns A8_ERR_USAGE and the caller uses a8_encode + a8_decode.        */
+int a8_roundtrip(const a8_enc_seg_t* segs, float* const* outs, int nseg, const void* book_dev, int norm,
+                 const void* static_lut_dev, float* scales_out, uint32_t* status_out, void* workspace,
+                 size_t workspace_bytes, void* stream);
 /* encode_buffer for float64 input, bit-exact with the reference's float64
  * arithmetic (codecs.py:254-268): absmax over the float64 values rounded to
  * float32, y = |x|/s in float64, searchsorted + clip + tie rule per element.

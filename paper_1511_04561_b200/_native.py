@@ -120,6 +120,11 @@ SIGNATURES = {
          C.c_size_t, C.c_void_p],
     ),
     "a8_onebit_decode": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "a8_roundtrip": (
+        C.c_int,
+        [C.POINTER(EncSeg), C.POINTER(C.c_void_p), C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+         C.c_void_p, C.c_size_t, C.c_void_p],
+    ),
     "a8_encode_blocked": (
         C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],
     ),

@@ -530,9 +530,48 @@ def decode_buffer(q: QuantizedTensor, codebook: Codebook, *, device=None, out=No
     return out
 
 
+def _roundtrip_fused(t: torch.Tensor, codebook: Codebook) -> Optional[torch.Tensor]:
+    """decode(encode(t)) in one kernel (a8_roundtrip) when the call fits in
+    the GPU's shared memory; None otherwise.  t: contiguous float32 CUDA."""
+    dev = t.device
+    n = t.numel()
+    if n == 0 or n > RESIDENT_MAX_ELEMS:
+        return None
+    book, lut = codebook.device_tables(dev)
+    out = torch.empty_like(t)
+    with torch.cuda.device(dev):
+        stream = _stream(dev)
+        meta = torch.empty(2, dtype=torch.int32, device=dev)  # [status, scale]
+        seg = N.EncSeg(t.data_ptr(), n, 0, 0, 0)
+        outs = (C.c_void_p * 1)(out.data_ptr())
+        ws = workspace(dev, stream, 1)
+        rc = N.lib.a8_roundtrip(C.byref(seg), outs, 1, book.data_ptr(), codebook.spec.norm_code,
+                                None if lut is None else lut.data_ptr(), meta.data_ptr() + 4, meta.data_ptr(),
+                                ws.data_ptr(), ws.numel(), stream)
+    if rc == N.A8_ERR_USAGE:
+        return None
+    N.check(rc)
+    if int(meta[0].cpu()) & N.A8_STATUS_NONFINITE:  # codecs.py:251-252
+        raise InputError("cannot encode non-finite values (NaN or Inf present)")
+    return out
+
+
+# largest single call the fused round trip takes (148 SMs x 51196 elements)
+RESIDENT_MAX_ELEMS = 148 * 51196
+
+
 def roundtrip(x, spec: DataTypeSpec, *, device=None):
-    """encode + decode in one step (codecs.py:285-288).  NumPy in -> NumPy out."""
+    """encode + decode in one step (codecs.py:285-288).  NumPy in -> NumPy out.
+
+    float32 data that fits in the GPU's shared memory takes one fused kernel
+    (the codes are never stored); anything else runs encode then decode."""
     cb = build_codebook(spec)
+    if not _is_f64(x):
+        t, shape = as_device_f32(x, device)
+        y = _roundtrip_fused(t.reshape(-1), cb)
+        if y is not None:
+            y = y.reshape(shape)
+            return y if isinstance(x, torch.Tensor) else y.cpu().numpy()
     q = encode_buffer(x, cb, device=device, sync=False)
     y = decode_buffer(q, cb)
     q._finish()

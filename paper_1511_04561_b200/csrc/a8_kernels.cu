@@ -811,10 +811,11 @@ constexpr int kRCap = (int)(kRDynSmem / sizeof(float));  // floats per CTA
 
 struct RSeg {
     const float* x;
+    float* out;  // fused round trip: decoded values (codecs.py:285-288), or null
     int64_t n;
     int64_t flat_off;
     int32_t scale_idx;
-    int32_t aligned;  // x is 16-byte aligned
+    int32_t aligned;  // x (and out) 16-byte aligned
     int32_t cta0;     // first CTA of the segment; its CTAs are [cta0, next segment's cta0)
     int32_t pad;
 };
@@ -828,39 +829,50 @@ struct RParams {
     const unsigned int* status_in;
     unsigned int* status_out;
     int nseg;
-    int pad;
+    int write_codes;  // 0: fused round trip only (no codes in memory)
     RSeg segs[kInlineSegs + 1];  // segs[nseg].cta0 = grid
 };
 
 // Encode elements [lo, hi) of segment g from shared memory (dst[i]) with the
 // table in sE (valid) or the thresholds in sT; codes through the layout.
+// With g.out set, the decoded values fl(table[c] * scale) (sDec) are written
+// too: the fused round trip of codecs.py:285-288.
 __device__ void resident_encode_piece(const RParams& p, const RSeg& g, const float* dst, int64_t lo, int64_t hi,
                                       int64_t a0, int64_t a1, int valid, int32_t kb, uint32_t len, const uint32_t* sE,
-                                      const uint32_t* sT, const uint8_t* sCanon, int tid) {
+                                      const uint32_t* sT, const uint8_t* sCanon, const float* sDec, int tid) {
     const int64_t L = p.lay.block_len;
     const int64_t gap = p.lay.block_stride - p.lay.block_len;
+    const bool wc = p.write_codes != 0;
+    float* const out = g.out;
     if (hi > lo) {
         const int64_t f_lo = g.flat_off + lo, f_hi = g.flat_off + hi - 1;
         const int32_t kmax = kb + (int32_t)len - 1;
-        if (valid && (f_lo / L) == (f_hi / L)) {
-            uint8_t* cb = p.lay.codes + (f_lo / L) * gap + g.flat_off;  // code of element i at cb[i]
-            const uint32_t eb = smem_addr(sE) - (uint32_t)kb * 4u;
-            for (int64_t i = a0 + 4 * (int64_t)tid; i < a1; i += 4 * kRThreads) {
-                const uint4 v = *reinterpret_cast<const uint4*>(dst + i);
-                *reinterpret_cast<uint32_t*>(cb + i) = encode4_lut(v, eb, kb, kmax);
-            }
-            if (tid < a0 - lo) cb[lo + tid] = (uint8_t)encode_lut(__float_as_uint(dst[lo + tid]), sE, kb, (int32_t)len - 1);
-            if (tid < hi - a1) cb[a1 + tid] = (uint8_t)encode_lut(__float_as_uint(dst[a1 + tid]), sE, kb, (int32_t)len - 1);
-        } else {
-            for (int64_t i = lo + tid; i < hi; i += kRThreads) {
-                const uint32_t b = __float_as_uint(dst[i]);
-                const uint32_t cc = valid ? encode_lut(b, sE, kb, (int32_t)len - 1) : encode_search(b, sT, sCanon);
+        auto one = [&](int64_t i) {  // element i alone
+            const uint32_t b = __float_as_uint(dst[i]);
+            const uint32_t cc = valid ? encode_lut(b, sE, kb, (int32_t)len - 1) : encode_search(b, sT, sCanon);
+            if (wc) {
                 const int64_t f = g.flat_off + i;
                 p.lay.codes[f + (f / L) * gap] = (uint8_t)cc;
             }
+            if (out) out[i] = sDec[cc & 255u];
+        };
+        if (valid && (f_lo / L) == (f_hi / L)) {
+            uint8_t* cb = wc ? p.lay.codes + (f_lo / L) * gap + g.flat_off : nullptr;  // code of element i at cb[i]
+            const uint32_t eb = smem_addr(sE) - (uint32_t)kb * 4u;
+            for (int64_t i = a0 + 4 * (int64_t)tid; i < a1; i += 4 * kRThreads) {
+                const uint4 v = *reinterpret_cast<const uint4*>(dst + i);
+                const uint32_t w = encode4_lut(v, eb, kb, kmax);
+                if (wc) *reinterpret_cast<uint32_t*>(cb + i) = w;
+                if (out)
+                    *reinterpret_cast<float4*>(out + i) =
+                        make_float4(sDec[w & 255u], sDec[(w >> 8) & 255u], sDec[(w >> 16) & 255u], sDec[w >> 24]);
+            }
+            if (tid < a0 - lo) one(lo + tid);
+            if (tid < hi - a1) one(a1 + tid);
+        } else {
+            for (int64_t i = lo + tid; i < hi; i += kRThreads) one(i);
         }
     }
-
 }
 
 // Phase 4: the last CTA out publishes the status and re-zeroes the workspace.
@@ -898,6 +910,7 @@ __global__ void __launch_bounds__(kRThreads, 1) resident_encode_kernel(const __g
     __shared__ unsigned int sWarp[kRThreads / 32];
     __shared__ int sHdr[4];
     __shared__ unsigned int sAmax;
+    __shared__ float sDec[256];  // fused round trip: fl(table[c] * scale)
     __shared__ __align__(8) uint64_t sBar;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
 
@@ -964,12 +977,15 @@ __global__ void __launch_bounds__(kRThreads, 1) resident_encode_kernel(const __g
         load_lut_smem(p.static_lut, sE, sT, sCanon, p.book, hdr, tid, kRThreads);
         __syncthreads();
         const float scale = p.static_lut->scale;
+        if (g.out && tid < 256) sDec[tid] = __fmul_rn(p.book->table[tid], scale);  // codecs.py:281
+        __syncthreads();
         if (q == 0 && tid < p.lay.scale_reps) p.lay.scales[tid * p.lay.scale_block_stride + g.scale_idx] = scale;
         if (blockIdx.x == 0)
             for (int e = 0; e < p.nseg; ++e)
                 if (p.segs[e].n == 0 && tid < p.lay.scale_reps)
                     p.lay.scales[tid * p.lay.scale_block_stride + p.segs[e].scale_idx] = scale;
-        resident_encode_piece(p, g, dst, lo, hi, a0, a1, hdr[0], hdr[1], (uint32_t)hdr[2] + 1u, sE, sT, sCanon, tid);
+        resident_encode_piece(p, g, dst, lo, hi, a0, a1, hdr[0], hdr[1], (uint32_t)hdr[2] + 1u, sE, sT, sCanon, sDec,
+                              tid);
         resident_finish(p, tid);
         return;
     }
@@ -993,6 +1009,7 @@ __global__ void __launch_bounds__(kRThreads, 1) resident_encode_kernel(const __g
     const unsigned int amax = sAmax;
     const float scale = amax == 0u ? 1.0f : __uint_as_float(amax);
     threshold_parallel(scale, p.book, sT, tid);
+    if (g.out && tid < 256) sDec[tid] = __fmul_rn(p.book->table[tid], scale);  // codecs.py:281
     __syncthreads();  // sT[i] is written by thread 4i; the count below reads sT[tid]
     const int F = __syncthreads_count(tid < 127 && sT[tid] < kInfBits);
     int32_t kb;
@@ -1011,7 +1028,7 @@ __global__ void __launch_bounds__(kRThreads, 1) resident_encode_kernel(const __g
             if (p.segs[e].n == 0 && tid < p.lay.scale_reps)
                 p.lay.scales[tid * p.lay.scale_block_stride + p.segs[e].scale_idx] = 1.0f;
     }
-    resident_encode_piece(p, g, dst, lo, hi, a0, a1, valid, kb, len, sE, sT, sCanon, tid);
+    resident_encode_piece(p, g, dst, lo, hi, a0, a1, valid, kb, len, sE, sT, sCanon, sDec, tid);
     resident_finish(p, tid);
 }
 
@@ -1451,7 +1468,8 @@ static bool resident_enabled() {
 // CTA holds one piece of one segment and builds one table.
 static int encode_resident(const a8_enc_seg_t* segs, int nseg, const void* book_dev, const void* static_lut_dev,
                            const a8_layout_t& layout, void* workspace, const uint32_t* status_in,
-                           uint32_t* status_out, const DevInfo& di, cudaStream_t st, bool* done) {
+                           uint32_t* status_out, const DevInfo& di, cudaStream_t st, bool* done,
+                           float* const* outs = nullptr) {
     *done = false;
     if (!resident_enabled() || di.res_occ < 1 || nseg > kInlineSegs) return A8_OK;
     const int64_t per = kRCap - 4;  // elements per CTA (+ up to 3 of alignment offset)
@@ -1481,13 +1499,16 @@ static int encode_resident(const a8_enc_seg_t* segs, int nseg, const void* book_
     p.status_in = status_in;
     p.status_out = status_out;
     p.nseg = nseg;
+    p.write_codes = outs ? 0 : 1;
     int64_t grid = 0;
     for (int i = 0; i < nseg; ++i) {
         p.segs[i].x = segs[i].x;
+        p.segs[i].out = outs ? outs[i] : nullptr;
         p.segs[i].n = segs[i].n;
         p.segs[i].flat_off = segs[i].flat_off;
         p.segs[i].scale_idx = segs[i].scale_idx;
-        p.segs[i].aligned = (reinterpret_cast<uintptr_t>(segs[i].x) % 16) == 0;
+        p.segs[i].aligned = (reinterpret_cast<uintptr_t>(segs[i].x) % 16) == 0 &&
+                            (!outs || (reinterpret_cast<uintptr_t>(outs[i]) % 16) == 0);
         p.segs[i].cta0 = (int32_t)grid;
         grid += c[i];
     }
@@ -1505,6 +1526,34 @@ static int encode_resident(const a8_enc_seg_t* segs, int nseg, const void* book_
     cudaLaunchKernelEx(&cfg, resident_encode_kernel, p);
     *done = true;
     return cuda_check("a8_encode (resident)");
+}
+
+extern "C" int a8_roundtrip(const a8_enc_seg_t* segs, float* const* outs, int nseg, const void* book_dev, int norm,
+                            const void* static_lut_dev, float* scales_out, uint32_t* status_out, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+    if (nseg <= 0 || !segs || !outs || !book_dev || !scales_out || !status_out || !workspace)
+        return fail(A8_ERR_USAGE, "a8_roundtrip: bad argument");
+    if (norm != A8_NORM_ABSMAX && !static_lut_dev) return fail(A8_ERR_USAGE, "a8_roundtrip: fixed-scale spec needs a static table");
+    for (int i = 0; i < nseg; ++i) {
+        if (segs[i].n < 0 || (segs[i].n > 0 && (!segs[i].x || !outs[i]))) return fail(A8_ERR_USAGE, "a8_roundtrip: bad segment");
+        if (segs[i].flat_off % 16 || segs[i].flat_off < 0) return fail(A8_ERR_USAGE, "a8_roundtrip: flat_off must be a multiple of 16");
+    }
+    if (ws_capacity(workspace_bytes) < nseg) return fail(A8_ERR_USAGE, "a8_roundtrip: workspace too small");
+    int device = 0;
+    cudaGetDevice(&device);
+    DevInfo di;
+    if (int rc = dev_info(device, &di)) return rc;
+    a8_layout_t lay;
+    memset(&lay, 0, sizeof(lay));
+    lay.scales = scales_out;
+    lay.block_len = (int64_t)1 << 40;  // one block: no code layout (codes are not written)
+    lay.block_stride = lay.block_len;
+    lay.scale_reps = 1;
+    bool done = false;
+    const int rc = encode_resident(segs, nseg, book_dev, norm == A8_NORM_ABSMAX ? nullptr : static_lut_dev, lay, workspace,
+                                   nullptr, status_out, di, static_cast<cudaStream_t>(stream), &done, outs);
+    if (rc) return rc;
+    return done ? A8_OK : fail(A8_ERR_USAGE, "a8_roundtrip: call does not fit the fused path (use a8_encode + a8_decode)");
 }
 
 extern "C" int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_dev, int norm,

@@ -126,6 +126,16 @@ def make_quantizer(spec: DataTypeSpec, stats: Optional[HookStats] = None, site: 
     cb = build_codebook(spec)
 
     def quantize(x: torch.Tensor, layer: int) -> torch.Tensor:
+        if x.dtype != torch.float64:  # float32 (or narrower): fused round trip when it fits
+            from .codecs import _roundtrip_fused, as_device_f32
+
+            t, shape = as_device_f32(x)
+            t = t.reshape(-1)
+            y = _roundtrip_fused(t, cb)
+            if y is not None:
+                if stats is not None:
+                    stats.record(site, layer, t, y)
+                return y.reshape(shape).to(x.dtype)
         q = encode_buffer(x, cb, sync=False)
         y = decode_buffer(q, cb)
         if stats is not None:

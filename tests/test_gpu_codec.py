@@ -238,3 +238,32 @@ def test_non_finite_in_large_call_ticket_kernel(spec, bad, cuda):
     x[5_000_003] = 0.0
     q = A.encode_buffer(x, cb)
     assert q.scale > 0
+
+
+@pytest.mark.parametrize("spec", [ALL_SPECS[1], ALL_SPECS[3], ALL_SPECS[5], ALL_SPECS[6]], ids=tag)
+@pytest.mark.parametrize("n", [1, 5, 4096, 100_003, 2_000_000, 8_000_000])
+def test_roundtrip_fused_and_fallback_match_oracle(spec, n, cuda):
+    """roundtrip(): one fused kernel (a8_roundtrip) up to the resident
+    capacity, encode + decode beyond it (8M) -- both equal the reference
+    round trip bit for bit; NumPy in -> NumPy out, torch in -> torch out."""
+    rng = np.random.default_rng(n)
+    x = (rng.normal(0, 0.05, size=n)).astype(np.float32)
+    x[::9] = 0.0
+    want = O.roundtrip(x, *spec)
+    got = A.roundtrip(x, S(spec), device=cuda)
+    assert isinstance(got, np.ndarray) and got.tobytes() == want.tobytes()
+    gt = A.roundtrip(torch.from_numpy(x).to(cuda), S(spec))
+    assert isinstance(gt, torch.Tensor) and gt.cpu().numpy().tobytes() == want.tobytes()
+
+
+def test_roundtrip_fused_non_finite_and_shapes(cuda):
+    spec = A.DataTypeSpec("dynamic-tree", "absmax")
+    x = torch.randn(3, 5, 7, device=cuda)
+    y = A.roundtrip(x, spec)
+    assert y.shape == x.shape
+    assert y.cpu().numpy().tobytes() == O.roundtrip(x.cpu().numpy(), "dynamic-tree", "absmax").tobytes()
+    x[1, 2, 3] = float("nan")
+    with pytest.raises(A.InputError):
+        A.roundtrip(x, spec)
+    y2 = A.roundtrip(torch.randn(100, device=cuda), spec)  # clean afterwards
+    assert torch.isfinite(y2).all()
