@@ -1,12 +1,11 @@
-"""Time the GPU error bench (one GPU) against the reference algorithm on the host.
+"""Time the GPU error bench (one GPU).
 
-    python tools/errorbench_timing.py [--n 25000000] [--cpu-n 1000000]
+    python tools/errorbench_timing.py [--n 25000000]
 
 Per suite cell: the sample is drawn on the host (not timed) and copied to the
 device; the timed region is measure_error's device work (encode + fused
-error sums, CUDA events, median of 5) on the resident input.  The CPU line
-times the oracle restatement of errorbench.measure_error on --cpu-n samples
-(1 core, NumPy).  Prints JSON lines.
+error sums, CUDA events, median of 5) on the resident input.  Prints JSON
+lines and the table.
 """
 
 from __future__ import annotations
@@ -14,7 +13,6 @@ from __future__ import annotations
 import argparse
 import json
 import sys
-import time
 from pathlib import Path
 
 import numpy as np
@@ -30,7 +28,6 @@ from paper_1511_04561_b200 import errorbench as EB  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=25_000_000)
-    ap.add_argument("--cpu-n", type=int, default=1_000_000)
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     cells = []
@@ -61,16 +58,6 @@ def main():
                           "mean_abs_error": r.mean_abs_error, "mean_rel_error_pct": r.mean_rel_error_pct}), flush=True)
     print(json.dumps({"suite_gpu_ms": tot, "n": a.n, "cells": len(cells)}), flush=True)
     sys.stdout.write(EB.format_table(reports))
-    try:
-        from oracle import approx8_oracle as O
-    except ImportError:
-        return
-    x = O.sample_normal(a.cpu_n, 4)
-    t0 = time.perf_counter()
-    O.measure_error(x, "dynamic-tree", "absmax")
-    dt = time.perf_counter() - t0
-    print(json.dumps({"cpu_reference_algorithm": "oracle measure_error (NumPy, 1 core)", "n": a.cpu_n, "s": dt,
-                      "s_per_25M_extrapolated": dt * 25_000_000 / a.cpu_n}), flush=True)
 
 
 if __name__ == "__main__":
