@@ -235,12 +235,12 @@ size_t a8_error_workspace_bytes(void);
 int a8_error_stats(const void* x, int x_is_f64, int64_t n, const uint8_t* codes, const float* scale_dev,
                    const void* book_dev, const float* after, double* out_dev, int accumulate, void* workspace,
                    size_t workspace_bytes, void* stream);
-/* Diagnostics: globaltimer trace of the last a8_encode on `workspace`
- * (synchronous device->host copy).  out[0..3] = kernel start ns, end ns,
- * total CTA time spent waiting for segment tables (ns), number of waits;
- * out[4 + 4k .. 7 + 4k] = table build start, thresholds done, table filled,
- * table published, for the k-th segment in scheduling order (ascending
- * size).  Needs 4 + 4*nseg entries.                                        */
+/* Diagnostics: globaltimer trace of the last ticket-kernel a8_encode on
+ * `workspace` (synchronous device->host copy).  out[0..3] = kernel start
+ * ns, end ns, total CTA time spent waiting for a segment's max to be final
+ * (ns), number of such waits; out[4 + 4k .. 7 + 4k] are reserved (zero: the
+ * per-segment tables are built by the CTAs that use them).  Needs
+ * 4 + 4*nseg entries.                                                      */
 int a8_encode_trace(const void* workspace, int nseg, uint64_t* out);
 
 /* Number of SMs and the persistent grid sizes the kernels use on `device`. */
