@@ -63,16 +63,31 @@ __global__ void __launch_bounds__(kThreads) onebit_stats(const void* g, int f64,
     double sp = 0.0, sn = 0.0;
     unsigned long long cp = 0, cn = 0;
     unsigned int bad = 0;
-    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads) {
-        const double gi = load_g(g, f64, i);
-        if (!isfinite(gi)) bad = 1;
-        const double c = __dadd_rn(gi, res[i]);
-        if (c >= 0.0) {
-            sp = __dadd_rn(sp, c);
-            ++cp;
-        } else {
-            sn = __dadd_rn(sn, c);
-            ++cn;
+    // the same per-thread element order (i, i+S, i+2S, ...) as a plain
+    // grid-stride loop -- so the sums are bit-identical to it -- with the
+    // loads of 4 elements issued before any of them is accumulated
+    constexpr int U = 4;
+    const int64_t S = (int64_t)gridDim.x * kThreads;
+    for (int64_t i0 = (int64_t)blockIdx.x * kThreads + threadIdx.x; i0 < n; i0 += U * S) {
+        double gv[U], rv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = i0 + u * S;
+            gv[u] = i < n ? load_g(g, f64, i) : 0.0;
+            rv[u] = i < n ? res[i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (i0 + u * S >= n) break;
+            if (!isfinite(gv[u])) bad = 1;
+            const double c = __dadd_rn(gv[u], rv[u]);
+            if (c >= 0.0) {
+                sp = __dadd_rn(sp, c);
+                ++cp;
+            } else {
+                sn = __dadd_rn(sn, c);
+                ++cn;
+            }
         }
     }
     const double SP = block_sum(sp, rd);
@@ -116,35 +131,75 @@ __global__ void __launch_bounds__(kThreads) onebit_apply(const void* g, int f64,
     }
     __syncthreads();
     const double pl = (double)sLv[0], nl = (double)sLv[1];
+    // warp chunks of 1024 consecutive elements: in step k the lanes take
+    // elements 32k + lane (coalesced loads and stores of g and the residual),
+    // the ballot gives those 32 sign bits, and lane k keeps them; at the end
+    // every lane stores its 4 bytes (128 coalesced bytes of bits per warp)
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (kThreads / 32);
     const int64_t nbytes = (n + 7) / 8;
-    for (int64_t b = (int64_t)blockIdx.x * kThreads + threadIdx.x; b < nbytes; b += (int64_t)gridDim.x * kThreads) {
-        uint32_t byte = 0;
+    for (int64_t wc = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); wc * 1024 < n; wc += warps) {
+        const int64_t base = wc * 1024;
+        uint32_t mine = 0;
+        constexpr int U = 8;  // steps whose loads are issued together
+        for (int k0 = 0; k0 < 32; k0 += U) {
+            double gv[U], rv[U];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int64_t i = b * 8 + k;
-            if (i < n) {
-                const double c = __dadd_rn(load_g(g, f64, i), res[i]);
-                const bool pos = c >= 0.0;
-                res[i] = __dsub_rn(c, pos ? pl : nl);
-                byte |= (uint32_t)pos << (7 - k);  // np.packbits: first element in the MSB
+            for (int u = 0; u < U; ++u) {
+                const int64_t i = base + 32 * (k0 + u) + lane;
+                gv[u] = i < n ? load_g(g, f64, i) : 0.0;
+                rv[u] = i < n ? res[i] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t i = base + 32 * (k0 + u) + lane;
+                const double c = __dadd_rn(gv[u], rv[u]);
+                const bool pos = i < n && c >= 0.0;
+                if (i < n) res[i] = __dsub_rn(c, pos ? pl : nl);
+                const uint32_t bal = __ballot_sync(0xffffffffu, pos);
+                if (lane == k0 + u) mine = bal;
             }
         }
-        bits[b] = (uint8_t)byte;
+        // np.packbits order: element 8j + t is bit 7 - t of byte j
+        const uint32_t w = __byte_perm(__brev(mine), 0, 0x0123);
+        const int64_t b0 = base / 8 + 4 * lane;
+        if (b0 + 4 <= nbytes && (reinterpret_cast<uintptr_t>(bits) & 3) == 0) {
+            *reinterpret_cast<uint32_t*>(bits + b0) = w;
+        } else {
+            for (int t = 0; t < 4; ++t)
+                if (b0 + t < nbytes) bits[b0 + t] = (uint8_t)(w >> (8 * t));
+        }
     }
 }
 
 __global__ void __launch_bounds__(kThreads) onebit_decode_k(const uint8_t* bits, int64_t n, const float* levels,
                                                              float* out) {
     const float pl = levels[0], nl = levels[1];
-    const int64_t nbytes = (n + 7) / 8;
-    for (int64_t b = (int64_t)blockIdx.x * kThreads + threadIdx.x; b < nbytes; b += (int64_t)gridDim.x * kThreads) {
-        const uint32_t byte = bits[b];
+    // lane l of a warp writes float4 number l of each 128-element group: its
+    // 4 elements are one nibble (high nibble first, np.packbits order)
+    const int64_t nq = n / 4;  // full float4 groups
+    const bool vec = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+    const int64_t S = (int64_t)gridDim.x * kThreads;
+    if (vec) {
+        constexpr int U = 8;  // float4 groups per thread per step, loads first
+        for (int64_t q0 = (int64_t)blockIdx.x * kThreads + threadIdx.x; q0 < nq; q0 += U * S) {
+            uint32_t nib[U];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int64_t i = b * 8 + k;
-            if (i < n) out[i] = (byte >> (7 - k)) & 1u ? pl : nl;
+            for (int u = 0; u < U; ++u) {
+                const int64_t q = q0 + u * S;
+                nib[u] = q < nq ? (__ldg(bits + (q >> 1)) >> ((q & 1) ? 0 : 4)) & 15u : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t q = q0 + u * S;
+                if (q < nq)
+                    __stcs(reinterpret_cast<float4*>(out) + q, make_float4(nib[u] & 8u ? pl : nl, nib[u] & 4u ? pl : nl,
+                                                                         nib[u] & 2u ? pl : nl, nib[u] & 1u ? pl : nl));
+            }
         }
     }
+    for (int64_t i = (vec ? nq * 4 : 0) + (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += S)
+        out[i] = (bits[i >> 3] >> (7 - (i & 7))) & 1u ? pl : nl;
 }
 
 int grid_for(int64_t n) {
