@@ -1769,8 +1769,21 @@ __global__ void __launch_bounds__(256) f64_absmax_kernel(const __grid_constant__
         const int64_t base = (c - sg.cstart) * kF64Chunk;
         const int64_t cnt = min((int64_t)kF64Chunk, sg.n - base);
         unsigned long long m = 0;
-        for (int64_t i = threadIdx.x; i < cnt; i += 256)
-            m = max(m, (unsigned long long)__double_as_longlong(sg.x[base + i]) & 0x7fffffffffffffffull);
+        const double* xs = sg.x + base;
+        if (cnt == kF64Chunk && (reinterpret_cast<uintptr_t>(xs) & 15) == 0) {
+            // 8 double2 loads per thread, all in flight before the max
+            double2 v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = __ldcs(reinterpret_cast<const double2*>(xs) + q * 256 + threadIdx.x);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                m = max(m, (unsigned long long)__double_as_longlong(v[q].x) & 0x7fffffffffffffffull);
+                m = max(m, (unsigned long long)__double_as_longlong(v[q].y) & 0x7fffffffffffffffull);
+            }
+        } else {
+            for (int64_t i = threadIdx.x; i < cnt; i += 256)
+                m = max(m, (unsigned long long)__double_as_longlong(xs[i]) & 0x7fffffffffffffffull);
+        }
         for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
         if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
         __syncthreads();
@@ -1783,9 +1796,50 @@ __global__ void __launch_bounds__(256) f64_absmax_kernel(const __grid_constant__
     }
 }
 
+// The reference decision for float64 |x| (bits a) at scale s: picks the upper
+// value of the pair (v_lo, v_hi) (codecs.py:260-265).
+__device__ __forceinline__ bool picks_upper64(unsigned long long a, double s, double v_lo, double v_hi) {
+    const double y = __ddiv_rn(__longlong_as_double((long long)a), s);
+    return !(__dsub_rn(y, v_lo) <= __dsub_rn(v_hi, y));
+}
+
+// T64: the smallest float64 bit pattern (of |x|) whose decision resolves
+// upward.  The decision is monotone in |x|, so the code of x is
+// #{i : T64_i <= bits(|x|)}.  Walk from the rounded midpoint, then bisect.
+__device__ unsigned long long threshold64(double s, double v_lo, double v_hi) {
+    constexpr unsigned long long kInf64 = 0x7ff0000000000000ull;
+    const double m = 0.5 * (v_lo + v_hi) * s;
+    const unsigned long long g = (unsigned long long)__double_as_longlong(m);
+    unsigned long long lo = 0ull, hi = kInf64;  // pred(lo) false (pred(0) is), pred(hi) true
+    if (g > 0ull && g < kInf64) {
+        if (picks_upper64(g, s, v_lo, v_hi)) {
+            hi = g;
+            for (int k = 0; k < 8 && hi > 0ull; ++k) {
+                if (!picks_upper64(hi - 1ull, s, v_lo, v_hi)) return hi;
+                --hi;
+            }
+        } else {
+            lo = g;
+            for (int k = 0; k < 8 && lo + 1ull < kInf64; ++k) {
+                if (picks_upper64(lo + 1ull, s, v_lo, v_hi)) return lo + 1ull;
+                ++lo;
+            }
+        }
+    }
+    while (hi - lo > 1ull) {
+        const unsigned long long mid = lo + ((hi - lo) >> 1);
+        if (picks_upper64(mid, s, v_lo, v_hi))
+            hi = mid;
+        else
+            lo = mid;
+    }
+    return hi;
+}
+
 __global__ void __launch_bounds__(256) f64_encode_kernel(const __grid_constant__ F64Params p) {
     __shared__ double sV[128];
     __shared__ uint8_t sC[128];
+    __shared__ unsigned long long sT64[128];  // thresholds of the current segment's scale
     __shared__ int sFinal;
     const int tid = threadIdx.x;
     const int D = p.book->ndistinct;
@@ -1797,34 +1851,65 @@ __global__ void __launch_bounds__(256) f64_encode_kernel(const __grid_constant__
     unsigned int bad = 0;
     const int64_t L = p.lay.block_len;
     const int64_t gap = p.lay.block_stride - p.lay.block_len;
+    int cur = -1;
+    float sf = p.fixed_scale;
     for (int64_t c = blockIdx.x; c < p.total; c += gridDim.x) {
         const int s = f64_seg_of(p, c);
         const F64Seg& sg = p.segs[s];
-        float sf = p.fixed_scale;
-        if (p.absmax) {
-            const unsigned long long mb = __ldcg(reinterpret_cast<const unsigned long long*>(&p.ctl[s].amax));
-            if (mb >= 0x7ff0000000000000ull) bad = 1;
-            const double peak = __longlong_as_double((long long)mb);
-            sf = peak > 0.0 ? __double2float_rn(peak) : 1.0f;  // codecs.py:234-241
+        if (s != cur) {  // thresholds of this segment's scale, once per CTA and segment
+            sf = p.fixed_scale;
+            if (p.absmax) {
+                const unsigned long long mb = __ldcg(reinterpret_cast<const unsigned long long*>(&p.ctl[s].amax));
+                if (mb >= 0x7ff0000000000000ull) bad = 1;
+                const double peak = __longlong_as_double((long long)mb);
+                sf = peak > 0.0 ? __double2float_rn(peak) : 1.0f;  // codecs.py:234-241
+            }
+            __syncthreads();  // the previous segment's thresholds are no longer read
+            if (tid < 128) {
+                unsigned long long t = 0x7ff0000000000000ull;
+                if (scale_ok(sf) && tid + 1 < D) t = threshold64((double)sf, sV[tid], sV[tid + 1]);
+                sT64[tid] = t;
+            }
+            __syncthreads();
+            cur = s;
         }
-        const double sd = (double)sf;
         const int64_t base = (c - sg.cstart) * kF64Chunk;
         const int64_t cnt = min((int64_t)kF64Chunk, sg.n - base);
         if (base == 0 && tid < p.lay.scale_reps) p.lay.scales[tid * p.lay.scale_block_stride + sg.scale_idx] = sf;
-        for (int64_t i = tid; i < cnt; i += 256) {
-            const double xv = sg.x[base + i];
+        auto code_of = [&](double xv) -> uint32_t {
             if (!isfinite(xv)) bad = 1;
-            const double y = __ddiv_rn(fabs(xv), sd);
-            int lo = 0;  // #{values < y} = searchsorted left
+            const unsigned long long a = (unsigned long long)__double_as_longlong(xv) & 0x7fffffffffffffffull;
+            int pick = 0;  // #{i : T64_i <= |x|} = the reference's pick (codecs.py:262-266)
 #pragma unroll
             for (int step = 64; step; step >>= 1)
-                if (sV[lo + step - 1] < y) lo += step;
-            const int idx = min(max(lo, 1), D - 1);
-            const int pick = (__dsub_rn(y, sV[idx - 1]) <= __dsub_rn(sV[idx], y)) ? idx - 1 : idx;
+                if (sT64[pick + step - 1] <= a) pick += step;
             uint32_t code = sC[pick];
             if (xv < 0.0 && pick != 0) code |= 0x80u;  // codecs.py:267-268
-            const int64_t f = sg.flat_off + base + i;
-            p.lay.codes[f + (f / L) * gap] = (uint8_t)code;
+            return code;
+        };
+        const double* xs = sg.x + base;
+        const int64_t f0 = sg.flat_off + base;
+        if (cnt == kF64Chunk && (reinterpret_cast<uintptr_t>(xs) & 15) == 0) {
+            // 8 consecutive elements per thread and group (4 double2 loads,
+            // one 8-byte store of codes; a group never straddles a block)
+#pragma unroll
+            for (int grp = 0; grp < 2; ++grp) {
+                const int e0 = grp * 2048 + tid * 8;
+                double2 v[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) v[q] = __ldcs(reinterpret_cast<const double2*>(xs + e0) + q);
+                unsigned long long w = 0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    w |= ((unsigned long long)code_of(v[q].x) << (16 * q)) | ((unsigned long long)code_of(v[q].y) << (16 * q + 8));
+                const int64_t f = f0 + e0;
+                *reinterpret_cast<unsigned long long*>(p.lay.codes + f + (f / L) * gap) = w;
+            }
+        } else {
+            for (int64_t i = tid; i < cnt; i += 256) {
+                const int64_t f = f0 + i;
+                p.lay.codes[f + (f / L) * gap] = (uint8_t)code_of(xs[i]);
+            }
         }
     }
     if (__syncthreads_or(bad) && tid == 0) atomicOr(&p.head->status, A8_STATUS_NONFINITE);
