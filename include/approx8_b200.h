@@ -193,6 +193,18 @@ int a8_decode(const a8_dec_seg_t* segs, int nseg, const void* book_dev, a8_layou
               int nranks, int op, int status_idx, int status_blocks, uint32_t* status_out,
               void* workspace, size_t workspace_bytes, void* stream);
 
+/* a8_decode with rank local_rank's term taken from its own float32 input:
+ * out = sum_r t_r, t_r = locals[i][k] for r == local_rank, else
+ * table[c_r] * s_r (same order, rounding and op as a8_decode).  The paper's
+ * "8-bit for incoming GPUs, 32-bit for the local GPU" (PAPER.md:194,
+ * SURVEY 8(e)); the reference has no multi-GPU path, so there is no
+ * reference function it replaces.  locals[i] holds segs[i].n floats and may
+ * be segs[i].out itself (in place).                                        */
+int a8_decode_local(const a8_dec_seg_t* segs, const float* const* locals, int local_rank, int nseg,
+                    const void* book_dev, a8_layout_t layout, int nranks, int op, int status_idx,
+                    int status_blocks, uint32_t* status_out, void* workspace, size_t workspace_bytes,
+                    void* stream);
+
 /* 1-bit error-feedback quantizer: onebit_quantize (codecs.py:306-339).
  *   g          n gradients, float32 (g_is_f64 = 0) or float64 (1)
  *   residual   n float64, updated in place: corrected - reconstruction

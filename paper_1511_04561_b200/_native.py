@@ -112,6 +112,11 @@ SIGNATURES = {
         [C.POINTER(DecSeg), C.c_int, C.c_void_p, Layout, C.c_int, C.c_int, C.c_int, C.c_int,
          C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p],
     ),
+    "a8_decode_local": (
+        C.c_int,
+        [C.POINTER(DecSeg), C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_void_p, Layout, C.c_int, C.c_int, C.c_int,
+         C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p],
+    ),
     "a8_encode_trace": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_uint64)]),
     "a8_onebit_workspace_bytes": (C.c_size_t, []),
     "a8_onebit_quantize": (

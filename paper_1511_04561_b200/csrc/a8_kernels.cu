@@ -82,6 +82,7 @@ struct DecSegD {
     int32_t scale_idx;
     int32_t aligned;
     int64_t cstart;  // first chunk id of this segment
+    const float* local;  // local-gradient variant: this rank's float32 input for the piece
 };
 
 struct WsHead {
@@ -144,6 +145,7 @@ struct DecParams {
     int status_blocks;
     unsigned int* status_out;
     int64_t total;
+    int local_rank;  // >= 0: rank whose term is the local float32 input (decode_kernel<true>)
     DecSegD segs[kInlineSegs];
 };
 
@@ -1049,6 +1051,12 @@ constexpr int kDecChunkD = kDecThreads * kDecGroups * 4;  // 4096 elements
 
 // 4 CTAs/SM (64 registers).  Measured: 2 CTAs (96 registers, the default
 // when min-blocks is 1) 30% slower, 5-8 CTAs (48-32 registers) slower at 2^30.
+//
+// kLocal: the paper's "8-bit for incoming GPUs, 32-bit for the local GPU"
+// (SURVEY 8(e)): rank p.local_rank's term is its own float32 input, read
+// from seg.local (which may alias seg.out: each thread reads its elements
+// before it stores them), instead of the decoded codes.
+template <bool kLocal>
 __global__ void __launch_bounds__(kDecThreads, 4) decode_kernel(const __grid_constant__ DecParams p) {
     // One UNSCALED decode table, one copy per lane ([256][32]: lane j reads
     // column j, so table lookups never conflict on a bank), built once per
@@ -1150,12 +1158,23 @@ __global__ void __launch_bounds__(kDecThreads, 4) decode_kernel(const __grid_con
 #pragma unroll
                 for (int q = 0; q < kDecGroups; ++q) w[q] = ld_stream_u32(src + f0 + q * (kDecThreads * 4) + tid * 4);
                 const float s0 = scl[0];
+                if (kLocal && p.local_rank == 0) {
 #pragma unroll
-                for (int q = 0; q < kDecGroups; ++q) {
-                    acc[q][0] = dec(w[q] & 255u, s0);
-                    acc[q][1] = dec((w[q] >> 8) & 255u, s0);
-                    acc[q][2] = dec((w[q] >> 16) & 255u, s0);
-                    acc[q][3] = dec(w[q] >> 24, s0);
+                    for (int q = 0; q < kDecGroups; ++q) {
+                        const float4 v = __ldcs(reinterpret_cast<const float4*>(sg.local + base + q * (kDecThreads * 4) + tid * 4));
+                        acc[q][0] = v.x;
+                        acc[q][1] = v.y;
+                        acc[q][2] = v.z;
+                        acc[q][3] = v.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < kDecGroups; ++q) {
+                        acc[q][0] = dec(w[q] & 255u, s0);
+                        acc[q][1] = dec((w[q] >> 8) & 255u, s0);
+                        acc[q][2] = dec((w[q] >> 16) & 255u, s0);
+                        acc[q][3] = dec(w[q] >> 24, s0);
+                    }
                 }
             }
             // rank r+1's code words are loaded before rank r's are decoded
@@ -1174,6 +1193,17 @@ __global__ void __launch_bounds__(kDecThreads, 4) decode_kernel(const __grid_con
                     const uint8_t* sn = src + (int64_t)(r + 1) * p.lay.rank_stride + f0 + tid * 4;
 #pragma unroll
                     for (int q = 0; q < kDecGroups; ++q) wn[q] = ld_stream_u32(sn + q * (kDecThreads * 4));
+                }
+                if (kLocal && r == p.local_rank) {
+#pragma unroll
+                    for (int q = 0; q < kDecGroups; ++q) {
+                        const float4 v = __ldcs(reinterpret_cast<const float4*>(sg.local + base + q * (kDecThreads * 4) + tid * 4));
+                        acc[q][0] = __fadd_rn(acc[q][0], v.x);
+                        acc[q][1] = __fadd_rn(acc[q][1], v.y);
+                        acc[q][2] = __fadd_rn(acc[q][2], v.z);
+                        acc[q][3] = __fadd_rn(acc[q][3], v.w);
+                    }
+                    continue;
                 }
 #pragma unroll
                 for (int q = 0; q < kDecGroups; ++q) {
@@ -1205,9 +1235,12 @@ __global__ void __launch_bounds__(kDecThreads, 4) decode_kernel(const __grid_con
             }
         } else {
             for (int64_t i = tid; i < cnt; i += kDecThreads) {
-                float a = dec(src[f0 + i], scl[0]);
-                for (int r = 1; r < R; ++r)
-                    a = __fadd_rn(a, dec(src[(int64_t)r * p.lay.rank_stride + f0 + i], scl[r]));
+                auto term = [&](int r) {
+                    return (kLocal && r == p.local_rank) ? sg.local[base + i]
+                                                         : dec(src[(int64_t)r * p.lay.rank_stride + f0 + i], scl[r]);
+                };
+                float a = term(0);
+                for (int r = 1; r < R; ++r) a = __fadd_rn(a, term(r));
                 if (p.op == 1 && R > 1) a = pow2 ? __fmul_rn(a, invN) : __fdiv_rn(a, (float)R);
                 sg.out[base + i] = a;
             }
@@ -1240,13 +1273,16 @@ static int dev_info(int device, DevInfo* out) {
         if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
         e = cudaFuncSetAttribute(encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEncDynSmem);
         if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
-        e = cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        e = cudaFuncSetAttribute(decode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)dec_smem(kMaxRanks));
+        if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
+        e = cudaFuncSetAttribute(decode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)dec_smem(kMaxRanks));
         if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.enc_occ, encode_kernel, kEncThreads, kEncDynSmem);
         if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
         const size_t dsm = dec_smem(1);
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.dec_occ, decode_kernel, kDecThreads, dsm);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.dec_occ, decode_kernel<false>, kDecThreads, dsm);
         if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
         e = cudaFuncSetAttribute(resident_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRDynSmem);
         if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
@@ -1651,9 +1687,10 @@ extern "C" int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_de
     return cuda_check("a8_encode");
 }
 
-extern "C" int a8_decode(const a8_dec_seg_t* segs, int nseg, const void* book_dev, a8_layout_t layout,
-                         int nranks, int op, int status_idx, int status_blocks, uint32_t* status_out,
-                         void* workspace, size_t workspace_bytes, void* stream) {
+static int decode_impl(const a8_dec_seg_t* segs, const float* const* locals, int local_rank, int nseg,
+                       const void* book_dev, a8_layout_t layout, int nranks, int op, int status_idx,
+                       int status_blocks, uint32_t* status_out, void* workspace, size_t workspace_bytes,
+                       void* stream) {
     if (nseg <= 0 && !status_out) return A8_OK;
     if (nseg < 0) return fail(A8_ERR_USAGE, "a8_decode: negative segment count");
     if (status_out && (status_idx < 0 || status_blocks < 1)) return fail(A8_ERR_USAGE, "a8_decode: bad status request");
@@ -1678,7 +1715,10 @@ extern "C" int a8_decode(const a8_dec_seg_t* segs, int nseg, const void* book_de
         d[i].n = s.n;
         d[i].flat_off = s.flat_off;
         d[i].scale_idx = s.scale_idx;
-        d[i].aligned = (reinterpret_cast<uintptr_t>(s.out) % 16) == 0;
+        d[i].local = locals ? locals[i] : nullptr;
+        if (locals && s.n > 0 && !d[i].local) return fail(A8_ERR_USAGE, "a8_decode_local: null local input");
+        d[i].aligned = (reinterpret_cast<uintptr_t>(s.out) % 16) == 0 &&
+                       (reinterpret_cast<uintptr_t>(d[i].local) % 16) == 0;
         d[i].cstart = chunks;
         chunks += (s.n + kDecChunkD - 1) / kDecChunkD;
     }
@@ -1694,12 +1734,19 @@ extern "C" int a8_decode(const a8_dec_seg_t* segs, int nseg, const void* book_de
     p.status_blocks = status_blocks;
     p.status_out = status_out;
     p.total = chunks;
+    p.local_rank = locals ? local_rank : -1;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    auto launch = [&](unsigned grid, size_t smem) {
+        if (locals)
+            decode_kernel<true><<<grid, kDecThreads, smem, st>>>(p);
+        else
+            decode_kernel<false><<<grid, kDecThreads, smem, st>>>(p);
+    };
     if (nseg <= kInlineSegs) {
         std::copy(d.begin(), d.begin() + nseg, p.segs);
         const size_t smem = dec_smem(nranks);
         const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)di.sms * di.dec_occ, chunks));
-        decode_kernel<<<(unsigned)grid, kDecThreads, smem, st>>>(p);
+        launch((unsigned)grid, smem);
     } else {
         const int cap = ws_capacity(workspace_bytes);
         if (cap < nseg) return fail(A8_ERR_USAGE, "a8_decode: workspace too small for the segment count");
@@ -1709,9 +1756,26 @@ extern "C" int a8_decode(const a8_dec_seg_t* segs, int nseg, const void* book_de
         p.segs_dev = reinterpret_cast<const DecSegD*>(plan);
         const size_t smem = dec_smem(nranks);
         const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)di.sms * di.dec_occ, chunks));
-        decode_kernel<<<(unsigned)grid, kDecThreads, smem, st>>>(p);
+        launch((unsigned)grid, smem);
     }
     return cuda_check("a8_decode");
+}
+
+extern "C" int a8_decode(const a8_dec_seg_t* segs, int nseg, const void* book_dev, a8_layout_t layout,
+                         int nranks, int op, int status_idx, int status_blocks, uint32_t* status_out,
+                         void* workspace, size_t workspace_bytes, void* stream) {
+    return decode_impl(segs, nullptr, -1, nseg, book_dev, layout, nranks, op, status_idx, status_blocks,
+                       status_out, workspace, workspace_bytes, stream);
+}
+
+extern "C" int a8_decode_local(const a8_dec_seg_t* segs, const float* const* locals, int local_rank, int nseg,
+                               const void* book_dev, a8_layout_t layout, int nranks, int op, int status_idx,
+                               int status_blocks, uint32_t* status_out, void* workspace, size_t workspace_bytes,
+                               void* stream) {
+    if (nseg > 0 && !locals) return fail(A8_ERR_USAGE, "a8_decode_local: null locals");
+    if (local_rank < 0 || local_rank >= nranks) return fail(A8_ERR_USAGE, "a8_decode_local: local_rank out of range");
+    return decode_impl(segs, locals, local_rank, nseg, book_dev, layout, nranks, op, status_idx, status_blocks,
+                       status_out, workspace, workspace_bytes, stream);
 }
 
 // ---------------------------------------------------------------------------

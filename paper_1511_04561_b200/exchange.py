@@ -64,7 +64,10 @@ class SegmentCodec:
     def decode(self, outs, flat_offs, scale_idx, cb: Codebook, buf: torch.Tensor, codes_off: int,
                scales_off: int, block_len: int, block_stride: int, scale_block_stride: int,
                rank_stride: int, nranks: int, op: int, status_idx: int = -1,
-               status_blocks: int = 0, status_out: Optional[torch.Tensor] = None) -> None:
+               status_blocks: int = 0, status_out: Optional[torch.Tensor] = None,
+               locals_: Optional[Sequence[torch.Tensor]] = None, local_rank: int = -1) -> None:
+        """``locals_``: rank ``local_rank``'s term of output i is locals_[i]
+        (float32, outs[i].numel() elements) instead of its decoded codes."""
         raise NotImplementedError
 
 
@@ -91,7 +94,7 @@ class CudaSegmentCodec(SegmentCodec):
 
     def decode(self, outs, flat_offs, scale_idx, cb, buf, codes_off, scales_off, block_len,
                block_stride, scale_block_stride, rank_stride, nranks, op, status_idx=-1,
-               status_blocks=0, status_out=None):
+               status_blocks=0, status_out=None, locals_=None, local_rank=-1):
         dev = buf.device
         book, _ = cb.device_tables(dev)
         n = len(outs)
@@ -103,9 +106,14 @@ class CudaSegmentCodec(SegmentCodec):
                        scale_block_stride, rank_stride, 1, 0)
         stream = torch.cuda.current_stream(dev).cuda_stream
         ws = workspace(dev, stream, max(n, 1))
-        N.check(N.lib.a8_decode(segs, n, book.data_ptr(), lay, nranks, op, status_idx,
-                                status_blocks, None if status_out is None else status_out.data_ptr(),
-                                ws.data_ptr(), ws.numel(), stream))
+        st = None if status_out is None else status_out.data_ptr()
+        if locals_ is None:
+            N.check(N.lib.a8_decode(segs, n, book.data_ptr(), lay, nranks, op, status_idx,
+                                    status_blocks, st, ws.data_ptr(), ws.numel(), stream))
+            return
+        lp = (C.c_void_p * max(n, 1))(*[t.data_ptr() for t in locals_])
+        N.check(N.lib.a8_decode_local(segs, lp, local_rank, n, book.data_ptr(), lay, nranks, op, status_idx,
+                                      status_blocks, st, ws.data_ptr(), ws.numel(), stream))
 
 
 # ---------------------------------------------------------------------------
@@ -222,18 +230,26 @@ class GradientExchange:
                single rank (N = 1); collectives run eagerly.  With deferred
                checks a non-finite status is reported at the next check of a
                later call (graph replays share one host status word).
+    ``local_fp32``  allgather only: each rank adds its own float32 gradient
+               instead of the decode of its own codes -- the paper's "8-bit
+               approximation for all incoming GPUs and 32-bit gradients for
+               the local GPU".  Ranks then hold different
+               (each slightly more accurate) averages.
     Every rank must call it with the same tensor shapes in the same order.
     """
 
     def __init__(self, spec: DataTypeSpec, group=None, mode: str = "allgather", op: str = "avg",
                  check: str = "deferred", codec: Optional[SegmentCodec] = None, comm=None,
-                 chunk_elems: int = 8 << 20, max_chunks: int = 8, graph: bool = False):
+                 chunk_elems: int = 8 << 20, max_chunks: int = 8, graph: bool = False,
+                 local_fp32: bool = False):
         if mode not in MODES:
             raise UsageError(f"mode must be one of {MODES}, got {mode!r}")
         if op not in OPS:
             raise UsageError(f"op must be one of {OPS}, got {op!r}")
         if check not in ("deferred", "sync", "none"):
             raise UsageError("check must be 'deferred', 'sync' or 'none'")
+        if local_fp32 and mode != "allgather":
+            raise UsageError("local_fp32 needs mode='allgather'")
         self.spec = spec
         self.cb = build_codebook(spec)
         self.group = group
@@ -254,6 +270,7 @@ class GradientExchange:
         self._graphs: dict = {}
         self._gstream = None
         self._capturing = None  # pinned host status word while capturing
+        self.local_fp32 = bool(local_fp32)
 
     # -- distributed context
     def _world(self):
@@ -429,9 +446,10 @@ class GradientExchange:
                           mine + C + 4 * plan.status_slot)
         status = self._status_word(dev)
         op = 1 if self.op == "avg" else 0
+        loc = self.local_fp32
         if nranks == 1:
             self.codec.decode(outs, plan.offs, idx, self.cb, gathered, 0, C, C, BS, BS // 4, P, 1, op,
-                              plan.status_slot, 1, status)
+                              plan.status_slot, 1, status, locals_=xs if loc else None, local_rank=0)
             self._collect_status(status)
             return
         start = getattr(self.comm, "all_gather_async", None)
@@ -447,9 +465,10 @@ class GradientExchange:
             if handles[j] is not None:
                 handles[j].wait()
             po = [outs[t].view(-1)[a:a + n] for (t, a, n, f) in pieces[j]]
+            pl = [xs[t].view(-1)[a:a + n] for (t, a, n, f) in pieces[j]] if loc else None
             self.codec.decode(po, [f for (t, a, n, f) in pieces[j]], [t for (t, a, n, f) in pieces[j]], self.cb,
                               gathered, 0, C, C, BS, BS // 4, P, nranks, op, plan.status_slot, 1,
-                              status if j == K - 1 else None)
+                              status if j == K - 1 else None, locals_=pl, local_rank=rank)
         self._collect_status(status)
 
     def _two_round(self, xs, outs, plan: Plan, nranks, rank, dev):

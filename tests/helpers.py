@@ -136,10 +136,10 @@ class NumpyCodec:
 
     def decode(self, outs, flat_offs, scale_idx, cb, buf, codes_off, scales_off, block_len,
                block_stride, scale_block_stride, rank_stride, nranks, op, status_idx=-1,
-               status_blocks=0, status_out=None):
+               status_blocks=0, status_out=None, locals_=None, local_rank=-1):
         mem = buf.numpy()
         table = O.book(self.kind).table
-        for o, f0, si in zip(outs, flat_offs, scale_idx):
+        for i, (o, f0, si) in enumerate(zip(outs, flat_offs, scale_idx)):
             n = o.numel()
             if n == 0:
                 continue
@@ -151,6 +151,8 @@ class NumpyCodec:
                 at = r * rank_stride + scales_off + 4 * (j * scale_block_stride + si)
                 s = np.frombuffer(mem[at:at + 4].tobytes(), np.float32)[0]
                 d = table[c] * np.float32(s)
+                if locals_ is not None and r == local_rank:
+                    d = locals_[i].reshape(-1).numpy().astype(np.float32)
                 acc = d.copy() if acc is None else (acc + d).astype(np.float32)
             if op == 1:
                 acc = (acc / np.float32(nranks)).astype(np.float32)

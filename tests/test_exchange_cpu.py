@@ -244,3 +244,33 @@ def test_pipelined_two_round_orchestration(nranks):
     for r in range(nranks):
         for a, b in zip(res[r], want):
             assert np.array_equal(a, b), r
+
+
+@pytest.mark.parametrize("nranks", [1, 2, 4])
+@pytest.mark.parametrize("chunk", [8 << 20, 256])
+def test_local_fp32_orchestration(nranks, chunk):
+    """local_fp32: each rank's own term is its float32
+    gradient; every other rank's is the round trip of its codes."""
+    spec = A.DataTypeSpec("dynamic-tree", "absmax")
+
+    def body(rank, comm):
+        ex = A.GradientExchange(spec, check="sync", codec=NumpyCodec(spec), comm=comm, local_fp32=True,
+                                chunk_elems=chunk)
+        ts = [torch.from_numpy(g) for g in grads_for(rank, seed=3)]
+        ex(ts)
+        return [t.numpy().copy() for t in ts]
+
+    res = run_virtual_ranks(nranks, body)
+    g = [grads_for(r, seed=3) for r in range(nranks)]
+    for r in range(nranks):
+        want = O.exchange_allgather_local(g, r, "dynamic-tree", "absmax")
+        for a, b in zip(res[r], want):
+            assert np.array_equal(a, b), (r, nranks)
+    if nranks == 1:
+        for a, b in zip(res[0], g[0]):
+            assert np.array_equal(a, b)  # N = 1: the gradient itself
+
+
+def test_local_fp32_needs_allgather():
+    with pytest.raises(A.UsageError):
+        A.GradientExchange(A.DataTypeSpec("linear", "absmax"), mode="two_round", local_fp32=True)

@@ -255,3 +255,47 @@ def test_pipelined_two_round_chunks(nranks, chunk, cuda):
     for r in range(nranks):
         for a, b in zip(res[r], want):
             assert a.tobytes() == b.tobytes(), (r, nranks, chunk)
+
+
+@pytest.mark.parametrize("nranks", [1, 2, 3, 8])
+@pytest.mark.parametrize("chunk", [8 << 20, 20000])
+def test_local_fp32_matches_oracle(nranks, chunk, cuda):
+    """local_fp32 through a8_decode_local, in place, bit-exact
+    against the per-rank oracle; ranks hold different results."""
+    spec = A.DataTypeSpec("dynamic-tree", "absmax")
+    sizes = SMALL + ALEXNET[:4]
+
+    def body(rank, comm):
+        ex = A.GradientExchange(spec, check="sync", comm=comm, local_fp32=True, chunk_elems=chunk)
+        ts = [torch.from_numpy(g).to(cuda) for g in grads(rank, sizes, 11)]
+        ex(ts)
+        torch.cuda.synchronize()
+        return [t.cpu().numpy() for t in ts]
+
+    res = run_virtual_ranks(nranks, body)
+    g = [grads(r, sizes, 11) for r in range(nranks)]
+    for r in range(nranks):
+        want = O.exchange_allgather_local(g, r, "dynamic-tree", "absmax")
+        for a, b in zip(res[r], want):
+            assert a.tobytes() == b.tobytes(), (r, nranks, chunk)
+
+
+def test_local_fp32_unaligned_pieces(cuda):
+    """Outputs and local inputs at offsets that are not 16-byte aligned take
+    the scalar path of the kernel."""
+    spec = A.DataTypeSpec("linear", "absmax")
+
+    def body(rank, comm):
+        base = torch.from_numpy(np.concatenate([np.zeros(1, np.float32)] + grads(rank, [(9001,), (4099,)], 12))).to(cuda)
+        ts = [base[1:9002], base[9002:]]
+        ex = A.GradientExchange(spec, check="sync", comm=comm, local_fp32=True)
+        ex(ts)
+        torch.cuda.synchronize()
+        return [t.cpu().numpy() for t in ts]
+
+    res = run_virtual_ranks(2, body)
+    g = [grads(r, [(9001,), (4099,)], 12) for r in range(2)]
+    for r in range(2):
+        want = O.exchange_allgather_local(g, r, "linear", "absmax")
+        for a, b in zip(res[r], want):
+            assert a.tobytes() == b.tobytes(), r
