@@ -268,4 +268,12 @@ A8_HD uint32_t encode_search(uint32_t b, const uint32_t* T128, const uint8_t* ca
     return c | ((c + 0x7fu) & (b >> 24) & 0x80u);
 }
 
+#ifdef __CUDACC__
+// Four elements by encode_search, packed little-endian into one word.
+__device__ __forceinline__ uint32_t encode4_search(uint4 v, const uint32_t* T128, const uint8_t* canon128) {
+    return encode_search(v.x, T128, canon128) | (encode_search(v.y, T128, canon128) << 8) |
+           (encode_search(v.z, T128, canon128) << 16) | (encode_search(v.w, T128, canon128) << 24);
+}
+#endif
+
 }  // namespace a8

@@ -810,6 +810,10 @@ __device__ void threshold_parallel(float scale, const a8_book_t* book, uint32_t*
 constexpr int kRThreads = 512;
 constexpr size_t kRDynSmem = 200u * 1024u;
 constexpr int kRCap = (int)(kRDynSmem / sizeof(float));  // floats per CTA
+#ifndef A8_RES_SEARCH_MAX
+#define A8_RES_SEARCH_MAX 4096
+#endif
+constexpr int64_t kRSearchMax = A8_RES_SEARCH_MAX;  // pieces up to this size skip the bucket table
 
 struct RSeg {
     const float* x;
@@ -858,12 +862,12 @@ __device__ void resident_encode_piece(const RParams& p, const RSeg& g, const flo
             }
             if (out) out[i] = sDec[cc & 255u];
         };
-        if (valid && (f_lo / L) == (f_hi / L)) {
+        if ((f_lo / L) == (f_hi / L)) {
             uint8_t* cb = wc ? p.lay.codes + (f_lo / L) * gap + g.flat_off : nullptr;  // code of element i at cb[i]
             const uint32_t eb = smem_addr(sE) - (uint32_t)kb * 4u;
             for (int64_t i = a0 + 4 * (int64_t)tid; i < a1; i += 4 * kRThreads) {
                 const uint4 v = *reinterpret_cast<const uint4*>(dst + i);
-                const uint32_t w = encode4_lut(v, eb, kb, kmax);
+                const uint32_t w = valid ? encode4_lut(v, eb, kb, kmax) : encode4_search(v, sT, sCanon);
                 if (wc) *reinterpret_cast<uint32_t*>(cb + i) = w;
                 if (out)
                     *reinterpret_cast<float4*>(out + i) =
@@ -1017,7 +1021,9 @@ __global__ void __launch_bounds__(kRThreads, 1) resident_encode_kernel(const __g
     int32_t kb;
     uint32_t len;
     lut_geometry(sT, (uint32_t)F, &kb, &len);
-    bool ok = len <= (uint32_t)kLutMax;
+    // small pieces search the 127 thresholds directly: filling the bucket
+    // table costs more than the extra shared-memory steps it saves
+    bool ok = len <= (uint32_t)kLutMax && hi - lo > kRSearchMax;
     if (ok && tid < kConsumers) ok = fill_lut_local(sT, (uint32_t)F, sCanon, kb, sE, sWarp, tid);
     const int valid = __syncthreads_and(ok);
     RES_STAMP(4);

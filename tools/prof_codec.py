@@ -103,6 +103,8 @@ def main():
         cases = [("alexnet", ALEXNET)]
     elif a.case == "mlpcodec":
         cases = [("mlp", [(784, 1200), (1200,), (1200, 1200), (1200,), (1200, 10), (10,)])]
+    elif a.case == "small":
+        cases = [("2^16", [(1 << 16,)]), ("c1_2^20", [(1 << 20,)]), ("2^22", [(1 << 22,)])]
     elif a.case == "single":
         cases = [("single_2^26", [(1 << 26,)])]
     elif a.case == "big":

@@ -16,7 +16,7 @@ for label in ("dynamic-tree/absmax", "mantissa/decade+2"):
     spec = A.parse_spec(label)
     cb = A.build_codebook(spec)
     book, lut = cb.device_tables(dev)
-    for n in (128 * 1200, 784 * 1200, 1200 * 1200, 1 << 22):
+    for n in (128 * 1200, 784 * 1200, 1 << 20, 1200 * 1200, 1 << 22):
         x = torch.randn(n, device=dev)
         out = torch.empty_like(x)
         codes = torch.empty(n, dtype=torch.uint8, device=dev)

@@ -9,7 +9,7 @@ import paper_1511_04561_b200 as A  # noqa
 from paper_1511_04561_b200 import _native as N  # noqa
 from prof_codec import run  # noqa
 dev = torch.device("cuda", 0)
-for name, sizes in (("mlp", [(784, 1200), (1200,), (1200, 1200), (1200,), (1200, 10), (10,)]), ("c5", [(128, 512)])):
+for name, sizes in (("mlp", [(784, 1200), (1200,), (1200, 1200), (1200,), (1200, 10), (10,)]), ("c5", [(128, 512)]), ("c1", [(1 << 20,)]), ("tiny", [(1024,)])):
     run(sizes, A.parse_spec("dynamic-tree/absmax"), 3, dev)
     torch.cuda.synchronize()
     lib = N.lib
