@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                 m.kind = kind;
                 {
                     const int64_t f0 = sg.flat_off + m.base;
-                    const int64_t j = f0 / L;
+                    const int64_t j = f0 < L ? 0 : f0 / L;  // one block (the common layout): no 64-bit divide
                     m.code_off = f0 + j * gap;
                     m.simple = m.bulk == kChunk && f0 + kChunk <= (j + 1) * L;
                 }
