@@ -345,8 +345,6 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
             const uint64_t drop = policy_evict_first();  // E reads: last use
             const int64_t L = p.lay.block_len;
             const int64_t gap = p.lay.block_stride - p.lay.block_len;
-            // tickets come in batches; the next batch is requested one batch
-            // ahead so the atomic's round trip never stalls the ring
             // tickets come in batches, requested two batches ahead so the
             // atomic's round trip (1-3 us under full HBM load) never stalls
             int64_t tb = (int64_t)atomicAdd(&p.head->ticket, kTicketBatch);
@@ -411,10 +409,6 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                     g_ticket_trace[t][4] = tr_free;
                 }
 #endif
-                // first E-chunk of a segment in this CTA: the segment's tagged
-                // thresholds ride along with the chunk (one more bulk copy), so
-                // the consumers usually find them in shared memory instead of
-                // paying an L2 round trip at the segment switch
                 sMeta[st] = m;
                 const uint32_t tx = (uint32_t)m.bulk * 4u;
                 if (tx > 0) {
