@@ -66,3 +66,36 @@ def test_blocked_edge_cases(cuda):
         A.encode_buffer(x, A.build_codebook(A.DataTypeSpec("mantissa", "decade", 1)), block_size=4096)
     with pytest.raises(A.ConfigError):
         A.encode_buffer(x, cb, block_size=3000)
+
+
+@pytest.mark.gpu
+def test_blocked_beyond_2_to_31_elements(cuda):
+    """Per-block codec at 2^31 + 4099 elements: x repeats a seeded 2^20
+    base (a whole number of blocks), so codes, block scales and decoded
+    values repeat the base's, which are checked against the oracle."""
+    P, reps, tail, block = 1 << 20, 2048, 4099, 4096
+    base_np = O.sample_normal(P, 33, 0.0, 0.3)
+    base_np[::7] *= 1e-3
+    cb = A.build_codebook(A.DataTypeSpec("dynamic-tree", "absmax"))
+    base = torch.from_numpy(base_np).to(cuda)
+    qb = A.encode_buffer(base, cb, block_size=block)
+    want_c, want_s = O.encode_blocked(base_np, "dynamic-tree", block)
+    assert np.array_equal(qb.codes.cpu().numpy(), want_c)
+    assert np.array_equal(qb.block_scales.cpu().numpy(), want_s)
+    x = torch.empty(P * reps + tail, device=cuda)
+    x[:P * reps].view(reps, P).copy_(base.expand(reps, P))
+    x[P * reps:] = base[:tail]
+    q = A.encode_buffer(x, cb, block_size=block)
+    nb = P // block
+    c, s = q.codes.view(-1), q.block_scales.view(-1)
+    assert bool((c[:P * reps].view(reps, P) == qb.codes.view(1, P)).all())
+    assert bool((s[:nb * reps].view(reps, nb) == qb.block_scales.view(1, nb)).all())
+    tq = A.encode_buffer(base[:tail].clone(), cb, block_size=block)  # the ragged tail's blocks
+    assert torch.equal(c[P * reps:], tq.codes.view(-1))
+    assert torch.equal(s[nb * reps:], tq.block_scales.view(-1))
+    del x
+    y = A.decode_buffer(q, cb).view(-1)
+    db = A.decode_buffer(qb, cb).view(-1)
+    assert bool((y[:P * reps].view(reps, P) == db.view(1, P)).all())
+    del y, q, c, s
+    torch.cuda.empty_cache()

@@ -267,3 +267,34 @@ def test_roundtrip_fused_non_finite_and_shapes(cuda):
         A.roundtrip(x, spec)
     y2 = A.roundtrip(torch.randn(100, device=cuda), spec)  # clean afterwards
     assert torch.isfinite(y2).all()
+
+
+@pytest.mark.parametrize("spec", [ALL_SPECS[1], ALL_SPECS[7]], ids=tag)
+def test_beyond_2_to_31_elements(spec, cuda):
+    """Maximum sizes: a buffer of 2^31 + 4099 elements (8.6 GB, 64-bit
+    indexing everywhere).  x repeats a seeded 2^20-element base (whose codes
+    are checked against the oracle) 2048 times plus a ragged tail, so the
+    scale is the base's and every period's codes and decoded values must
+    equal the base's."""
+    P, reps, tail = 1 << 20, 2048, 4099
+    base_np = O.sample_normal(P, 31, 0.0, 0.01)
+    ref, rs = O.encode(base_np, *spec)
+    cb = A.build_codebook(S(spec))
+    base = torch.from_numpy(base_np).to(cuda)
+    qb = A.encode_buffer(base, cb)
+    assert np.array_equal(qb.codes.cpu().numpy(), ref) and qb.scale == rs
+    db = A.decode_buffer(qb, cb)
+    x = torch.empty(P * reps + tail, device=cuda)
+    x[:P * reps].view(reps, P).copy_(base.expand(reps, P))
+    x[P * reps:] = base[:tail]
+    q = A.encode_buffer(x, cb)
+    assert q.scale == rs
+    c = q.codes.view(-1)
+    assert bool((c[:P * reps].view(reps, P) == qb.codes.view(1, P)).all())
+    assert torch.equal(c[P * reps:], qb.codes[:tail])
+    del x
+    y = A.decode_buffer(q, cb).view(-1)
+    assert bool((y[:P * reps].view(reps, P) == db.view(1, P)).all())
+    assert torch.equal(y[P * reps:], db[:tail])
+    del y, q, c
+    torch.cuda.empty_cache()
