@@ -198,7 +198,7 @@ def run_b200(args, nranks, rank, local_rank):
 
     import paper_1511_04561_b200 as A
 
-    dev = torch.device("cuda", local_rank)
+    dev = torch.device("cuda", local_rank % torch.cuda.device_count())
     torch.cuda.set_device(dev)
     spec = A.parse_spec(SPEC_LABEL)
     host = alexnet_grads(rank)
@@ -213,7 +213,10 @@ def run_b200(args, nranks, rank, local_rank):
 
     def barrier():
         if nranks > 1:
-            dist.barrier(device_ids=[local_rank])
+            if dist.get_backend() == "nccl":
+                dist.barrier(device_ids=[dev.index])
+            else:
+                dist.barrier()
 
     def max_over_ranks(v):
         if nranks == 1:
@@ -266,7 +269,7 @@ def run_b200(args, nranks, rank, local_rank):
             torch.cuda.synchronize()
 
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(dev.index) as clk:
         ex.codec = codec
         soak(0.6)
         ex.codec = TimedCodec()
@@ -489,8 +492,16 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        # A8_BENCH_BACKEND=gloo: plumbing check of the N > 1 path with every
+        # rank on one GPU (ranks wrap around the visible devices); numbers
+        # from such a run are not measurements
+        backend = os.environ.get("A8_BENCH_BACKEND", "nccl")
+        idx = local_rank % torch.cuda.device_count()
+        torch.cuda.set_device(idx)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", idx))
+        else:
+            dist.init_process_group(backend)
     try:
         run_b200(args, world, rank, local_rank)
     finally:
