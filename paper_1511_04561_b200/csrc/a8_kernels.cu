@@ -47,7 +47,7 @@ constexpr int kMaxRanks = 16;
 
 constexpr int kInlineSegs = 32;
 constexpr int kInlineBlks = 3 * kInlineSegs + 2;
-static int max_blocks(int nseg) { return 6 * nseg + 8; }
+static int max_blocks(int nseg) { return 7 * nseg + 8; }
 
 // ---------------------------------------------------------------------------
 // device-side plan / workspace
@@ -65,7 +65,14 @@ struct EncSegD {
 // Ticket kinds.  A: max-abs of a chunk; E: encode a chunk with the segment's
 // table; F: a whole single-chunk segment (max, thresholds and encode in one
 // CTA, no cross-CTA dependency); END: no more work.
-constexpr int kA = 0, kE = 1, kEnd = 2, kF = 3;
+// B ("build") tickets: the CTA that takes one waits for the segment's A
+// pass and builds + publishes its table ahead of the E pass.  The producer
+// treats a B ticket like any other (it streams the segment's chunk 0, which
+// the consumers ignore), so the per-ticket producer path is unchanged.
+constexpr int kA = 0, kE = 1, kB = 2, kF = 3, kEnd = 4;  // kEnd: stage metadata only
+#ifndef A8_BUILD_TICKETS
+#define A8_BUILD_TICKETS 1
+#endif
 
 // A contiguous run of tickets over one segment: chunks c0, c0+1, ... (A, F)
 // or c0, c0-1, ... (E).  c0k = c0 << 2 | kind.
@@ -273,7 +280,7 @@ __device__ unsigned long long g_flush_trace[32][512][4];  // per (seg, cta): flu
 
 constexpr unsigned int kTicketBatch = 4;  // tickets per atomic (two batches prefetched)
 constexpr int kSmemSegs = 64;
-constexpr int kSmemBlks = 6 * kSmemSegs + 8;  // max_blocks(kSmemSegs)
+constexpr int kSmemBlks = 6 * kSmemSegs + 8;  // larger plans are read from global memory
 
 // ---------------------------------------------------------------------------
 // K1+K2+K3: persistent encode.
@@ -537,7 +544,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                 lenm1 = 0;
                 cur = -1;  // sT now holds this segment's thresholds
             } else {
-            // ---------------- E: encode the chunk ----------------------------
+            // ---------------- E: encode the chunk (B: only build) -----------
             if (cur != m.seg && cur != -2) {
                 nbar_sync(kBarC, kConsumers);  // everyone is done with the old table
                 if (ctid == 0) {
@@ -564,12 +571,15 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                         mode = 2;
                     else if (r == 0u && atomicCAS(&p.ctl[m.seg].ready, 0u, 1u) == 0u)
                         mode = 3;
+                    if (m.kind == kB && mode != 3) mode = 0;  // B: someone else has it
                     sMode = mode;
                 }
                 nbar_sync(kBarC, kConsumers);
                 const unsigned int amax = (unsigned int)sHdr[3];
                 const int mode = sMode;
-                if (mode == 2) {
+                if (mode == 0) {
+                    // B ticket, table already claimed: nothing to do
+                } else if (mode == 2) {
                     load_lut_smem(p.luts + m.seg, sE, sT, sCanon, p.book, sHdr, ctid, kConsumers);
                     nbar_sync(kBarC, kConsumers);
                     tvalid = sHdr[0];
@@ -613,8 +623,15 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                         }
                     }
                 }
-                tamax = amax;
-                cur = m.seg;
+                if (mode != 0) {
+                    tamax = amax;
+                    cur = m.seg;
+                }
+                if (m.kind == kB) {  // (a B ticket always switches: it precedes the segment's E pass)
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_a(empty0 + 8u * st);
+                    continue;
+                }
             }
             if (cur != -2 && m.base == 0) {  // the CTA encoding chunk 0 publishes scale and status
                 const float scale = tamax == 0u ? 1.0f : __uint_as_float(tamax);
@@ -1382,6 +1399,11 @@ static void schedule(const std::vector<EncSegD>& d, bool absmax, int64_t wf, std
             r.c0 += now;
             r.cnt -= now;
             if (r.cnt == 0) {
+                // B ticket right after the A pass: its table is built and
+                // published while the fill distance runs
+                // (only when other work can fill the distance: a lone segment's
+                // E pass follows at once, measured 1.5% slower with a B ticket)
+                if (A8_BUILD_TICKETS && hold) emit(Run{r.s, kB, 0, 1});
                 pend.push_back(Pending{t + wf, r.s});
                 aq.pop_front();
             }

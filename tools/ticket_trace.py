@@ -29,7 +29,7 @@ from paper_1511_04561_b200 import _native as N  # noqa: E402
 import prof_codec  # noqa: E402
 from prof_codec import ALEXNET, run  # noqa: E402
 
-KIND = {0: "A", 1: "E", 2: "F", 3: "END"}
+KIND = {0: "A", 1: "E", 2: "B", 3: "F"}
 
 
 def main():
