@@ -1423,15 +1423,16 @@ static void schedule(const std::vector<EncSegD>& d, bool absmax, int64_t wf, std
     blks->push_back(EncBlk{t, -1, 0});  // sentinel: total tickets
 }
 
-// Fill distance in tickets: what 2 CTAs/SM hold reserved (ring + ticket
-// batches) plus a table build's worth of throughput.  A8_SCHED_FILL
-// overrides it (tuning).
+// Fill distance in tickets: what the CTAs hold reserved (ring + ticket
+// batches) plus enough throughput for the B ticket's wait and build to end
+// before the E pass is reached.  Measured (C3, with B tickets): 2880 -> 115.0
+// us, 6400 -> 113.0 us, flat up to 12000.  A8_SCHED_FILL overrides it.
 static int64_t fill_distance(int64_t ctas) {
     static const int64_t env = [] {
         const char* e = getenv("A8_SCHED_FILL");
         return e ? atoll(e) : -1ll;
     }();
-    return env >= 0 ? env : ctas * 8 + 512;
+    return env >= 0 ? env : ctas * 20 + 512;
 }
 
 }  // namespace a8
