@@ -876,13 +876,18 @@ __device__ void resident_encode_piece(const RParams& p, const RSeg& g, const flo
         if ((f_lo / L) == (f_hi / L)) {
             uint8_t* cb = wc ? p.lay.codes + (f_lo / L) * gap + g.flat_off : nullptr;  // code of element i at cb[i]
             const uint32_t eb = smem_addr(sE) - (uint32_t)kb * 4u;
-            for (int64_t i = a0 + 4 * (int64_t)tid; i < a1; i += 4 * kRThreads) {
-                const uint4 v = *reinterpret_cast<const uint4*>(dst + i);
-                const uint32_t w = valid ? encode4_lut(v, eb, kb, kmax) : encode4_search(v, sT, sCanon);
+            auto group = [&](int64_t i, uint32_t w) {
                 if (wc) *reinterpret_cast<uint32_t*>(cb + i) = w;
                 if (out)
                     *reinterpret_cast<float4*>(out + i) =
                         make_float4(sDec[w & 255u], sDec[(w >> 8) & 255u], sDec[(w >> 16) & 255u], sDec[w >> 24]);
+            };
+            if (valid) {  // separate loops: the table loop stays as tight as before the search mode
+                for (int64_t i = a0 + 4 * (int64_t)tid; i < a1; i += 4 * kRThreads)
+                    group(i, encode4_lut(*reinterpret_cast<const uint4*>(dst + i), eb, kb, kmax));
+            } else {
+                for (int64_t i = a0 + 4 * (int64_t)tid; i < a1; i += 4 * kRThreads)
+                    group(i, encode4_search(*reinterpret_cast<const uint4*>(dst + i), sT, sCanon));
             }
             if (tid < a0 - lo) one(lo + tid);
             if (tid < hi - a1) one(a1 + tid);
