@@ -278,7 +278,10 @@ __device__ unsigned long long g_ticket_trace[kTraceTickets][5];  // issue, done,
 __device__ unsigned long long g_flush_trace[32][512][4];  // per (seg, cta): flush start, atom back, amax back, chunks
 #endif
 
-constexpr unsigned int kTicketBatch = 4;  // tickets per atomic (two batches prefetched)
+#ifndef A8_TICKET_BATCH
+#define A8_TICKET_BATCH 2
+#endif
+constexpr unsigned int kTicketBatch = A8_TICKET_BATCH;  // tickets per atomic (two batches prefetched)
 constexpr int kSmemSegs = 64;
 constexpr int kSmemBlks = 6 * kSmemSegs + 8;  // larger plans are read from global memory
 
