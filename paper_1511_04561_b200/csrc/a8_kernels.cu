@@ -1387,7 +1387,11 @@ static void schedule(const std::vector<EncSegD>& d, bool absmax, int64_t wf, std
     auto emit_e = [&](int s) {
         Run e{s, kE, d[s].nE - 1, d[s].nE};
         if (hold && pool.s < 0) {  // first E pass: keep its cold head as filler
-            const int64_t h = std::min<int64_t>(e.cnt / 2, 2 * wf);
+            static const int pool_div = [] {  // A8_SCHED_POOL: held-back share 1/div (tuning)
+                const char* v = getenv("A8_SCHED_POOL");
+                return v ? std::max(1, atoi(v)) : 2;
+            }();
+            const int64_t h = std::min<int64_t>(e.cnt / pool_div, 2 * wf);
             pool = Run{s, kE, h - 1, h};
             e.cnt -= h;
         }
