@@ -400,9 +400,14 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                 m.kind = kind;
                 {
                     const int64_t f0 = sg.flat_off + m.base;
-                    const int64_t j = f0 < L ? 0 : f0 / L;  // one block (the common layout): no 64-bit divide
-                    m.code_off = f0 + j * gap;
-                    m.simple = m.bulk == kChunk && f0 + kChunk <= (j + 1) * L;
+                    if (f0 < L) {  // one block (the common layout): no 64-bit divide or multiply
+                        m.code_off = f0;
+                        m.simple = m.bulk == kChunk && f0 + kChunk <= L;
+                    } else {
+                        const int64_t j = f0 / L;
+                        m.code_off = f0 + j * gap;
+                        m.simple = m.bulk == kChunk && f0 + kChunk <= (j + 1) * L;
+                    }
                 }
                 {   // peek at this CTA's next ticket (tb + g after the advance above): an
                     // A run's partial max is published as soon as its last chunk is
