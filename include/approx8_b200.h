@@ -123,8 +123,14 @@ typedef struct a8_layout {
     int64_t scale_block_stride; /* floats between consecutive blocks' scales    */
     int64_t rank_stride;        /* bytes between ranks' copies (decode only)    */
     int32_t scale_reps;         /* encode: write the scale into blocks [0, reps) */
-    int32_t pad;
+    int32_t flags;              /* decode: A8_LAYOUT_* bits (0 = defaults)      */
 } a8_layout_t;
+
+/* a8_layout_t.flags (decode).  A8_LAYOUT_STATUS_COUNT: status_out counts
+ * non-finite calls -- *status_out += (status != 0) -- instead of being
+ * overwritten with the status bits, so a word shared by many launches (one
+ * CUDA graph replayed many times) never loses a report between host reads. */
+#define A8_LAYOUT_STATUS_COUNT 1
 
 int a8_abi_version(void);
 const char* a8_last_error(void);
@@ -188,7 +194,8 @@ int a8_encode_f64(const a8_enc_seg64_t* segs, int nseg, const void* book_dev, in
  *   nranks = 1 is exactly decode_buffer.
  *   status_idx >= 0: status_out = OR of the uint32 words at
  *   scales[r * rank_stride/4 + j * scale_block_stride + status_idx] for
- *   r < nranks, j < status_blocks (the encoders' replicated status words). */
+ *   r < nranks, j < status_blocks (the encoders' replicated status words);
+ *   with layout.flags & A8_LAYOUT_STATUS_COUNT it is incremented instead. */
 int a8_decode(const a8_dec_seg_t* segs, int nseg, const void* book_dev, a8_layout_t layout,
               int nranks, int op, int status_idx, int status_blocks, uint32_t* status_out,
               void* workspace, size_t workspace_bytes, void* stream);

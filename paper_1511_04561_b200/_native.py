@@ -17,6 +17,7 @@ _LIB_PATH = Path(os.environ.get("A8_LIB") or Path(__file__).resolve().parent / "
 
 A8_OK, A8_ERR_INPUT, A8_ERR_CONFIG, A8_ERR_USAGE, A8_ERR_CUDA = 0, 1, 2, 3, 4
 A8_STATUS_NONFINITE = 1
+A8_LAYOUT_STATUS_COUNT = 1
 KIND_CODE = {"dynamic-tree": 0, "static-tree": 1, "linear": 2, "mantissa": 3}
 NORM_CODE = {"none": 0, "absmax": 1, "decade": 2}
 LUT_MAX = 4096
@@ -85,7 +86,7 @@ class Layout(C.Structure):
         ("scale_block_stride", C.c_int64),
         ("rank_stride", C.c_int64),
         ("scale_reps", C.c_int32),
-        ("pad", C.c_int32),
+        ("flags", C.c_int32),
     ]
 
 

@@ -7,12 +7,18 @@ Same names, argument meaning and error behaviour as the reference codec API
 ``include/approx8_b200.h`` on the tensor's CUDA device.  There is no CPU
 fallback: without a CUDA device the compute calls raise.
 
-Differences a caller can see:
-  * ``QuantizedTensor.codes`` is a CUDA ``torch.uint8`` tensor (flat, C order);
+Host and device data:
+  * NumPy (or any non-torch) input behaves exactly like the reference:
+    ``encode_buffer`` returns a ``QuantizedTensor`` whose ``codes`` is a NumPy
+    ``uint8`` array (copied from the GPU on first access; the device copy is
+    kept for ``decode_buffer``), and ``decode_buffer`` / ``roundtrip`` /
+    ``onebit_decode`` return NumPy ``float32`` arrays; ``OneBitState`` keeps a
+    NumPy ``float64`` residual.  The reference's callers (mlp.py:171, 319,
+    tensorfile.py:74, cli.py:87-117) run unchanged on it.
+  * CUDA tensors stay on the device: ``codes`` is a CUDA ``torch.uint8``
+    tensor (flat, C order), decodes return CUDA ``torch.float32`` tensors and
     ``scale`` is a Python float fetched lazily (``scale_tensor`` stays on the
     device, so nothing syncs until it is read).
-  * ``decode_buffer``/``roundtrip`` return a CUDA ``torch.float32`` tensor,
-    or a NumPy array when the input to ``roundtrip`` was a NumPy array.
   * float32 and float64 inputs are encoded exactly as the reference does
     (float64 input through a float64 kernel, codecs.py:254); other dtypes
     are converted to float32 first.
@@ -191,7 +197,10 @@ def build_codebook(spec: DataTypeSpec) -> Codebook:
 class QuantizedTensor:
     """Encoded buffer plus everything needed to decode it (codecs.py:207-229).
 
-    ``codes``  CUDA uint8, one byte per element, flat C order
+    ``codes``  uint8, one byte per element, flat C order: a CUDA tensor for
+               device input, a NumPy array for host input (materialised from
+               the device copy on first access; once exposed, the NumPy array
+               is what decodes read, so in-place edits are honoured)
     ``scale``  float32 normalisation scale as a Python float (lazy)
     """
 
@@ -208,6 +217,9 @@ class QuantizedTensor:
         scale_tensor: Optional[torch.Tensor] = None,
         meta: Optional[torch.Tensor] = None,
     ) -> None:
+        self._dev_codes: Optional[torch.Tensor] = None
+        self._np_codes: Optional[np.ndarray] = None
+        self._host = False
         self.codes = codes
         self.shape = tuple(int(d) for d in shape)
         self.spec = spec
@@ -221,6 +233,31 @@ class QuantizedTensor:
         self.block_size: Optional[int] = None  # per-block scales (encode_buffer(block_size=...))
         self.block_scales: Optional[torch.Tensor] = None
         self._block_status: Optional[torch.Tensor] = None
+
+    @property
+    def codes(self):
+        if self._np_codes is not None:
+            return self._np_codes
+        if self._host and self._dev_codes is not None:
+            self._np_codes = self._dev_codes.cpu().numpy()  # host caller: the reference's ndarray
+        return self._np_codes if self._host else self._dev_codes
+
+    @codes.setter
+    def codes(self, c) -> None:
+        if isinstance(c, torch.Tensor):
+            self._dev_codes, self._np_codes, self._host = c, None, False
+        else:
+            self._dev_codes, self._np_codes, self._host = None, np.asarray(c), True
+
+    def _set_device_result(self, codes: torch.Tensor, host: bool) -> "QuantizedTensor":
+        """Codes produced on the device for a host (NumPy) or device caller."""
+        self._dev_codes, self._np_codes, self._host = codes, None, bool(host)
+        return self
+
+    @property
+    def is_host(self) -> bool:
+        """True when the tensor came from (and decodes to) host NumPy data."""
+        return self._host
 
     def _host_levels(self):
         if self.levels_tensor is not None and self._levels is None:
@@ -288,7 +325,7 @@ class QuantizedTensor:
             self._scale = float(self.scale_tensor.float().cpu()[0])
 
     def device_codes(self, device: torch.device) -> torch.Tensor:
-        c = self.codes
+        c = self._np_codes if self._np_codes is not None else self._dev_codes
         if not isinstance(c, torch.Tensor):
             c = torch.from_numpy(np.ascontiguousarray(np.asarray(c, dtype=np.uint8).ravel()))
         c = c.to(device).reshape(-1)
@@ -304,6 +341,12 @@ class QuantizedTensor:
     def codes_numpy(self) -> np.ndarray:
         c = self.codes
         return c.cpu().numpy() if isinstance(c, torch.Tensor) else np.asarray(c, dtype=np.uint8)
+
+    @property
+    def codes_device(self) -> Optional[torch.Tensor]:
+        """The CUDA copy of the codes, if there is one (None for codes that
+        only exist on the host)."""
+        return self._dev_codes
 
     def __repr__(self) -> str:
         label = self.spec.label() if self.spec is not None else None
@@ -325,19 +368,32 @@ def _cuda_device(device) -> torch.device:
 
 _ws_lock = threading.Lock()
 _ws_cache: dict = {}
+# Minimum capacity: every call of <= 32 segments (all graph-capturable calls)
+# shares the first allocation, so a captured graph's workspace pointer stays
+# valid; a larger call reallocates and bumps the epoch (see workspace_epoch).
+WS_MIN_SEGS = 32
+_ws_epoch: dict = {}
 
 
 def workspace(device: torch.device, stream: int, nseg: int) -> torch.Tensor:
     """Zero-filled kernel scratch for (device, stream); the kernels leave it
     zeroed, so it is allocated once and grown on demand."""
-    need = N.workspace_bytes(nseg)
+    need = N.workspace_bytes(max(nseg, WS_MIN_SEGS))
     key = (device.index, stream)
     with _ws_lock:
         ws = _ws_cache.get(key)
         if ws is None or ws.numel() < need:
             ws = torch.zeros(need, dtype=torch.uint8, device=device)
             _ws_cache[key] = ws
+            _ws_epoch[key] = _ws_epoch.get(key, 0) + 1
     return ws
+
+
+def workspace_epoch(device: torch.device, stream: int) -> int:
+    """Bumped whenever ``workspace(device, stream, ...)`` reallocates: a CUDA
+    graph captured under an older epoch holds a freed workspace address."""
+    with _ws_lock:
+        return _ws_epoch.get((device.index, stream), 0)
 
 
 def as_device_f32(x, device=None) -> tuple[torch.Tensor, tuple]:
@@ -392,13 +448,15 @@ def encode_buffer(x, codebook: Codebook, *, device=None, sync: bool = True,
         return _encode_blocked(x, codebook, device, sync, int(block_size))
     if _is_f64(x):  # the reference computes float64 input in float64 (codecs.py:254)
         return _encode_f64(x, codebook, device, sync)
+    host = not isinstance(x, torch.Tensor)
     t, shape = as_device_f32(x, device)
     dev = t.device
     n = t.numel()
     if n == 0:  # codecs.py:257-258
         s = codebook.fixed_scale
         return QuantizedTensor(torch.empty(0, dtype=torch.uint8, device=dev), shape, spec,
-                               1.0 if s is None else s)
+                               1.0 if s is None else s)._set_device_result(
+                                   torch.empty(0, dtype=torch.uint8, device=dev), host)
     book, lut = codebook.device_tables(dev)
     with torch.cuda.device(dev):
         stream = _stream(dev)
@@ -411,6 +469,7 @@ def encode_buffer(x, codebook: Codebook, *, device=None, sync: bool = True,
                                 None if lut is None else lut.data_ptr(), lay, ws.data_ptr(),
                                 ws.numel(), None, meta.data_ptr(), stream))
     q = QuantizedTensor(codes, shape, spec, scale_tensor=meta[1:].view(torch.float32), meta=meta)
+    q._set_device_result(codes, host)
     q._keepalive = t  # input must outlive the asynchronous kernel
     if sync:
         q._finish()
@@ -423,6 +482,7 @@ def _encode_blocked(x, codebook: Codebook, device, sync: bool, block: int) -> Qu
         raise ConfigError(f"per-block scales need absmax normalization, not {spec.normalization.value!r}")
     if block not in BLOCK_SIZES:
         raise ConfigError(f"block_size must be one of {BLOCK_SIZES}, got {block}")
+    host = not isinstance(x, torch.Tensor)
     t, shape = as_device_f32(x, device)
     t = t.reshape(-1)
     dev = t.device
@@ -436,7 +496,7 @@ def _encode_blocked(x, codebook: Codebook, device, sync: bool, block: int) -> Qu
         status = torch.empty(1, dtype=torch.int32, device=dev)
         N.check(N.lib.a8_encode_blocked(t.data_ptr(), n, block, book.data_ptr(), codes.data_ptr(),
                                         scales.data_ptr(), status.data_ptr(), stream))
-    q = QuantizedTensor(codes, shape, spec, 1.0, scale_tensor=None)
+    q = QuantizedTensor(codes, shape, spec, 1.0, scale_tensor=None)._set_device_result(codes, host)
     q.block_size = block
     q.block_scales = scales
     q._block_status = status
@@ -456,6 +516,7 @@ def _encode_f64(x, codebook: Codebook, device, sync: bool) -> QuantizedTensor:
     """float64 input: the reference decision restated in float64 on the GPU
     (a8_encode_f64), bit-exact with codecs.py:254-268 for any float64 data."""
     spec = codebook.spec
+    host = not isinstance(x, torch.Tensor)
     if isinstance(x, torch.Tensor):
         dev = _cuda_device(x.device if x.is_cuda else device)
         shape = tuple(x.shape)
@@ -468,7 +529,8 @@ def _encode_f64(x, codebook: Codebook, device, sync: bool) -> QuantizedTensor:
     n = t.numel()
     if n == 0:
         s = codebook.fixed_scale
-        return QuantizedTensor(torch.empty(0, dtype=torch.uint8, device=dev), shape, spec, 1.0 if s is None else s)
+        e = torch.empty(0, dtype=torch.uint8, device=dev)
+        return QuantizedTensor(e, shape, spec, 1.0 if s is None else s)._set_device_result(e, host)
     book, _ = codebook.device_tables(dev)
     fixed = codebook.fixed_scale
     with torch.cuda.device(dev):
@@ -482,22 +544,34 @@ def _encode_f64(x, codebook: Codebook, device, sync: bool) -> QuantizedTensor:
                                     1.0 if fixed is None else fixed, lay, ws.data_ptr(), ws.numel(),
                                     None, meta.data_ptr(), stream))
     q = QuantizedTensor(codes, shape, spec, scale_tensor=meta[1:].view(torch.float32), meta=meta)
+    q._set_device_result(codes, host)
     q._keepalive = t
     if sync:
         q._finish()
     return q
 
 
-def decode_buffer(q: QuantizedTensor, codebook: Codebook, *, device=None, out=None) -> torch.Tensor:
-    """Map codes back to float32 values, undoing the scale (codecs.py:272-282)."""
+def decode_buffer(q: QuantizedTensor, codebook: Codebook, *, device=None, out=None):
+    """Map codes back to float32 values, undoing the scale (codecs.py:272-282).
+
+    Returns a CUDA float32 tensor, or a NumPy float32 array of ``q.shape``
+    when ``q`` holds host (NumPy) data, as the reference does."""
+    y = _decode_device(q, codebook, device, out)
+    if q.is_host and out is None:
+        return y.cpu().numpy()
+    return y
+
+
+def _decode_device(q: QuantizedTensor, codebook: Codebook, device, out) -> torch.Tensor:
     if q.nbits != 8:
         raise UsageError("decode_buffer handles 8-bit tensors; use onebit_decode")
     if q.spec != codebook.spec:
         raise UsageError(
             f"tensor was encoded as {q.spec and q.spec.label()}, codebook is {codebook.spec.label()}"
         )
-    if isinstance(q.codes, torch.Tensor) and q.codes.is_cuda:
-        dev = q.codes.device
+    dc = q.codes_device
+    if dc is not None and dc.is_cuda and q._np_codes is None:
+        dev = dc.device
     else:
         dev = _cuda_device(device)
     codes = q.device_codes(dev)
@@ -573,7 +647,7 @@ def roundtrip(x, spec: DataTypeSpec, *, device=None):
             y = y.reshape(shape)
             return y if isinstance(x, torch.Tensor) else y.cpu().numpy()
     q = encode_buffer(x, cb, device=device, sync=False)
-    y = decode_buffer(q, cb)
+    y = _decode_device(q, cb, device, None)
     q._finish()
     if isinstance(x, torch.Tensor):
         return y
@@ -586,75 +660,107 @@ def roundtrip(x, spec: DataTypeSpec, *, device=None):
 
 class OneBitState:
     """Residual carried between successive 1-bit quantizations of one tensor
-    (codecs.py:295-303); a float64 tensor on the device."""
+    (codecs.py:295-303).  ``residual`` is a NumPy float64 array for host
+    callers (the reference's type; ``onebit_quantize`` rebinds it to a new
+    array, as codecs.py:335 does) or a float64 CUDA tensor for a
+    device-resident state (updated in place, no host traffic)."""
 
     def __init__(self, residual) -> None:
         self.residual = residual
 
     @classmethod
     def zeros(cls, shape, device=None) -> "OneBitState":
-        dev = _cuda_device(device)
-        return cls(torch.zeros(tuple(shape) if not isinstance(shape, int) else (shape,), dtype=torch.float64,
-                               device=dev))
+        shp = (shape,) if isinstance(shape, int) else tuple(shape)
+        if device is None:
+            return cls(np.zeros(shp, dtype=np.float64))
+        return cls(torch.zeros(shp, dtype=torch.float64, device=_cuda_device(device)))
 
 
 _ob_ws: dict = {}
 
+_NONFINITE_MSG = "cannot encode non-finite values (NaN or Inf present)"
 
-def onebit_quantize(g, state: OneBitState, *, sync: bool = True) -> QuantizedTensor:
+
+def onebit_quantize(g, state: OneBitState, *, sync: bool = True, device=None) -> QuantizedTensor:
     """Quantize ``g + residual`` to one bit per element and update ``state``
     (codecs.py:306-339): each side of 0 is reconstructed as its own float32
-    mean and the residual keeps exactly what the receiver cannot see."""
+    mean and the residual keeps exactly what the receiver cannot see.
+
+    Non-finite input raises ``InputError`` and leaves the state untouched
+    (codecs.py:317-318).  A host state (NumPy residual) is always checked
+    before returning; a device state with ``sync=False`` is checked by
+    ``q._finish()``."""
     res = state.residual
-    if not isinstance(res, torch.Tensor) or not res.is_cuda or res.dtype != torch.float64:
-        state.residual = res = torch.as_tensor(np.asarray(res, dtype=np.float64)).to(_cuda_device(None))
+    host = not isinstance(res, torch.Tensor)
+    if host:
+        res_np = np.asarray(res, dtype=np.float64)
+        gdev = g.device if isinstance(g, torch.Tensor) and g.is_cuda else device
+        dev = _cuda_device(gdev)
+        res_shape = tuple(res_np.shape)
+    else:
+        if not res.is_cuda or res.dtype != torch.float64:
+            state.residual = res = res.to(device=_cuda_device(device if not res.is_cuda else res.device),
+                                          dtype=torch.float64)
+        dev = res.device
+        res_shape = tuple(res.shape)
     if isinstance(g, torch.Tensor):
         shape = tuple(g.shape)
-        t = g.to(res.device)
+        t = g.to(dev)
     else:
         arr = np.asarray(g)
         shape = tuple(arr.shape)
-        t = torch.from_numpy(np.ascontiguousarray(arr)).to(res.device)
-    if shape != tuple(res.shape):
-        raise UsageError(f"gradient shape {shape} does not match residual shape {tuple(res.shape)}")
-    if t.dtype not in (torch.float32, torch.float64):
+        t = torch.from_numpy(np.ascontiguousarray(arr)).to(dev)
+    if shape != res_shape:
+        raise UsageError(f"gradient shape {shape} does not match residual shape {res_shape}")
+    if t.dtype not in (torch.float32, torch.float64):  # float32 widens exactly; the rest as np.asarray(g, float64)
         t = t.to(torch.float64)
     t = t.contiguous()
-    res_c = res if res.is_contiguous() else res.contiguous()
+    if host:
+        res_c = torch.from_numpy(np.ascontiguousarray(res_np).copy()).to(dev)
+    else:
+        res_c = res if res.is_contiguous() else res.contiguous()
     n = t.numel()
-    dev = res.device
     bits = torch.empty((n + 7) // 8, dtype=torch.uint8, device=dev)
     lv = torch.zeros(2, dtype=torch.float32, device=dev)
     status = torch.zeros(1, dtype=torch.int32, device=dev)
+    ws = None
     if n:
         with torch.cuda.device(dev):
-            key = dev.index
-            ws = _ob_ws.get(key)
+            ws = _ob_ws.get(dev.index)
             if ws is None:
-                ws = _ob_ws[key] = torch.empty(N.lib.a8_onebit_workspace_bytes(), dtype=torch.uint8, device=dev)
+                ws = _ob_ws[dev.index] = torch.empty(N.lib.a8_onebit_workspace_bytes(), dtype=torch.uint8,
+                                                     device=dev)
             N.check(N.lib.a8_onebit_quantize(t.data_ptr(), 1 if t.dtype == torch.float64 else 0, res_c.data_ptr(),
                                              n, bits.data_ptr(), lv.data_ptr(), status.data_ptr(), ws.data_ptr(),
                                              ws.numel(), _stream(dev)))
-        if res_c is not res:
-            res.copy_(res_c)
+    if host:
+        if n and int(status.cpu()[0]) & N.A8_STATUS_NONFINITE:
+            raise InputError(_NONFINITE_MSG)
+        lvh = lv.cpu()
+        state.residual = res_c.cpu().numpy().reshape(res_shape)
+        return QuantizedTensor(bits.cpu().numpy(), shape, None, 1.0, nbits=1,
+                               pos_level=float(lvh[0]), neg_level=float(lvh[1]))
+    if res_c is not res:
+        res.copy_(res_c)
     q = QuantizedTensor(bits, shape, None, 1.0, nbits=1)
     q._levels = None
     q.levels_tensor = lv
-    q._keepalive = (t, ws if n else None)
-    if sync and n and int(status.cpu()[0]) & N.A8_STATUS_NONFINITE:
-        raise InputError("cannot encode non-finite values (NaN or Inf present)")
+    q._keepalive = (t, ws)
+    if n:
+        q._block_status = status
+    if sync:
+        q._finish()
     return q
 
 
-def onebit_decode(q: QuantizedTensor, *, device=None) -> torch.Tensor:
-    """Reconstruct the two-level float32 tensor (codecs.py:342-348)."""
+def onebit_decode(q: QuantizedTensor, *, device=None):
+    """Reconstruct the two-level float32 tensor (codecs.py:342-348): a CUDA
+    tensor, or a NumPy array when ``q`` holds host data."""
     if q.nbits != 1:
         raise UsageError("onebit_decode expects a 1-bit tensor")
-    codes = q.codes
-    dev = codes.device if isinstance(codes, torch.Tensor) and codes.is_cuda else _cuda_device(device)
-    if not isinstance(codes, torch.Tensor):
-        codes = torch.from_numpy(np.ascontiguousarray(np.asarray(codes, dtype=np.uint8))).to(dev)
-    codes = codes.to(dev).contiguous()
+    dc = q.codes_device
+    dev = dc.device if dc is not None and dc.is_cuda and q._np_codes is None else _cuda_device(device)
+    codes = q.device_codes(dev)
     n = q.count
     lv = q.levels_tensor if q.levels_tensor is not None else torch.tensor(
         [np.float32(q.pos_level), np.float32(q.neg_level)], dtype=torch.float32, device=dev)
@@ -662,4 +768,4 @@ def onebit_decode(q: QuantizedTensor, *, device=None) -> torch.Tensor:
     if n:
         with torch.cuda.device(dev):
             N.check(N.lib.a8_onebit_decode(codes.data_ptr(), n, lv.data_ptr(), out.data_ptr(), _stream(dev)))
-    return out
+    return out.cpu().numpy() if q.is_host else out

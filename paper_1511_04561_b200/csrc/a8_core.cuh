@@ -257,6 +257,60 @@ __device__ __forceinline__ uint32_t encode4_lut(uint4 v, uint32_t ebase, int32_t
 }
 #endif
 
+// ---------------------------------------------------------------------------
+// "Carry" bucket table, for codebooks whose canonical code of sorted value i
+// is i itself (dynamic-tree and linear: exactly the kinds that allow absmax,
+// codecs.py:89-94).  Entry of the bucket with key k:
+//     lo << 16  +  (bucket holds threshold T_lo ? 0x10000 - lo16(T_lo) : 0)
+// where lo = #thresholds below the bucket.  For an element with bits b in the
+// bucket, entry + (b & 0x8000ffff) has the code in byte 2 (lo, plus the carry
+// out of the low half iff lo16(b) >= lo16(T_lo), i.e. iff b >= T_lo) and the
+// sign bit of x alone in byte 3 (the sum stays below 2^23).  A bucket can
+// hold at most one threshold (else the table is invalid and the caller
+// searches the thresholds).  Keys below the table clamp to entry 0, which is
+// 0 (code 0, no threshold); absmax tables extend up to the key of the scale
+// itself, the largest |x| of the segment, so no upper clamp is needed.
+A8_HD uint32_t carry_entry(uint32_t lo, uint32_t count, uint32_t t_lo) {
+    return (lo << 16) + (count ? 0x10000u - (t_lo & 0xffffu) : 0u);
+}
+
+// Scalar form with both clamps (any key; slow paths and host checks).
+A8_HD uint32_t encode_carry(uint32_t b, const uint32_t* e, int32_t kbase, int32_t lenm1) {
+    int32_t j = (int32_t)((b & 0x7fffffffu) >> kKeyShift) - kbase;
+    j = j < 0 ? 0 : (j > lenm1 ? lenm1 : j);
+    const uint32_t c = ((e[j] + (b & 0xffffu)) >> 16) & 0xffu;
+    return c | ((c + 0x7fu) & (b >> 24) & 0x80u);
+}
+
+#if defined(__CUDACC__)
+// One element: the table sum (code in byte 2, sign in byte 3).  `ebase` is
+// the shared address of the table minus kbase entries, `emin` the table's
+// own address (signed max: ebase may wrap below zero).  5 instructions:
+// LOP3, IMAD.HI (key * 4 + ebase), VIMNMX, LDS, IADD3.
+__device__ __forceinline__ uint32_t carry_sum(uint32_t b, uint32_t ebase, int32_t emin) {
+    const uint32_t m = b & 0x7fff0000u;
+    const int32_t a = max((int32_t)(__umulhi(m, 1u << 18) + ebase), emin);
+    uint32_t e;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(a));
+    return e + b - m;
+}
+
+// Four table sums -> four final code bytes, little-endian: code | sign for
+// non-zero codes (codecs.py:267-268; c + 0x7f carries into bit 7 iff c != 0).
+__device__ __forceinline__ uint32_t pack4_carry(uint32_t s0, uint32_t s1, uint32_t s2, uint32_t s3) {
+    const uint32_t w01 = __byte_perm(s0, s1, 0x7632);  // c0 g0 c1 g1
+    const uint32_t w23 = __byte_perm(s2, s3, 0x7632);  // c2 g2 c3 g3
+    const uint32_t codes = __byte_perm(w01, w23, 0x6420);
+    const uint32_t signs = __byte_perm(w01, w23, 0x7531);
+    return codes | (signs & (codes + 0x7f7f7f7fu));
+}
+
+__device__ __forceinline__ uint32_t encode4_carry(uint4 v, uint32_t ebase, int32_t emin) {
+    return pack4_carry(carry_sum(v.x, ebase, emin), carry_sum(v.y, ebase, emin), carry_sum(v.z, ebase, emin),
+                       carry_sum(v.w, ebase, emin));
+}
+#endif
+
 // One element by binary search over the padded thresholds (paper's method).
 A8_HD uint32_t encode_search(uint32_t b, const uint32_t* T128, const uint8_t* canon128) {
     const uint32_t a = b & 0x7fffffffu;

@@ -187,7 +187,10 @@ __device__ __forceinline__ unsigned long long gtime();
 // count), then write the entries in place.  Entry-for-entry equal to
 // lut_entry(); returns false (for this thread) if one of its buckets holds
 // two distinct thresholds.  Needs len <= kLutMax = 16 * kConsumers.
+// Carry = true: the carry format of a8_core.cuh (carry_entry; monotone
+// codebooks), where a bucket may hold at most one threshold.
 static_assert(kLutMax == 16 * kConsumers, "one thread per 16 buckets");
+template <bool Carry = false>
 __device__ bool fill_lut_local(const uint32_t* T, uint32_t F, const uint8_t* canon, int32_t kbase, uint32_t* e,
                                unsigned int* sWarp, int ctid) {
     const int lane = ctid & 31, w = ctid >> 5;
@@ -224,10 +227,15 @@ __device__ bool fill_lut_local(const uint32_t* T, uint32_t F, const uint8_t* can
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
         const uint32_t hi = lo + c[i];
-        v[i] = (uint32_t)canon[lo] | ((uint32_t)canon[hi] << 8);
-        if (c[i]) {
-            v[i] |= (T[lo] & 0xffffu) << 16;
-            ok &= T[lo] == T[hi - 1];
+        if (Carry) {
+            v[i] = carry_entry(lo, c[i], c[i] ? T[lo] : 0u);
+            ok &= c[i] <= 1u;
+        } else {
+            v[i] = (uint32_t)canon[lo] | ((uint32_t)canon[hi] << 8);
+            if (c[i]) {
+                v[i] |= (T[lo] & 0xffffu) << 16;
+                ok &= T[lo] == T[hi - 1];
+            }
         }
         lo = hi;
     }
@@ -606,9 +614,11 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                     int32_t kb;
                     uint32_t len;
                     lut_geometry(sT, (uint32_t)nf, &kb, &len);
+                    // carry tables reach the key of the max itself: no upper clamp
+                    len = max((int32_t)len, (int32_t)(amax >> kKeyShift) - kb + 1);
                     tkbase = kb;
                     tlenm1 = (int)len - 1;
-                    const bool ok = len <= (uint32_t)kLutMax && fill_lut_local(sT, nf, sCanon, kb, sE, sRed, ctid);
+                    const bool ok = len <= (uint32_t)kLutMax && fill_lut_local<true>(sT, nf, sCanon, kb, sE, sRed, ctid);
                     tvalid = nbar_and(kBarC, kConsumers, ok);  // also: sE complete
                     if (mode == 3) {  // publish for the CTAs that come later
                         a8_lut_t* L = p.luts + m.seg;
@@ -659,10 +669,11 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                 const uint4* in = reinterpret_cast<const uint4*>(stage) + ctid;
                 const uint32_t eb = smem_addr(sE) - (uint32_t)kbase * 4u;  // indexed by the clamped key
                 const int32_t kmax = kbase + lenm1;
-                if (p.absmax) {
+                if (p.absmax) {  // carry table (a8_core.cuh), 5 instructions per element
+                    const int32_t emin = (int32_t)smem_addr(sE);
 #pragma unroll
                     for (int q = 0; q < kChunk / (kConsumers * 4); ++q)
-                        out[q * kConsumers] = encode4_lut(in[q * kConsumers], eb, kbase, kmax);
+                        out[q * kConsumers] = encode4_carry(in[q * kConsumers], eb, emin);
                 } else {
                     int32_t kacc = 0;  // max key: >= 0x7f80 iff some |x| is Inf/NaN
 #pragma unroll
@@ -686,7 +697,12 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                 if (i + 4 <= m.bulk) {
                     const uint4 v = *reinterpret_cast<const uint4*>(stage + i);
                     uint32_t c0, c1, c2, c3;
-                    if (valid) {
+                    if (valid && p.absmax) {
+                        c0 = encode_carry(v.x, sE, kbase, lenm1);
+                        c1 = encode_carry(v.y, sE, kbase, lenm1);
+                        c2 = encode_carry(v.z, sE, kbase, lenm1);
+                        c3 = encode_carry(v.w, sE, kbase, lenm1);
+                    } else if (valid) {
                         c0 = encode_lut(v.x, sE, kbase, lenm1);
                         c1 = encode_lut(v.y, sE, kbase, lenm1);
                         c2 = encode_lut(v.z, sE, kbase, lenm1);
@@ -703,7 +719,9 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                     const int e_end = min(i + 4, m.cnt);
                     for (int e = i; e < e_end; ++e) {
                         const uint32_t b = e < m.bulk ? __float_as_uint(stage[e]) : __float_as_uint(sg.x[m.base + e]);
-                        const uint32_t c = valid ? encode_lut(b, sE, kbase, lenm1) : encode_search(b, sT, sCanon);
+                        const uint32_t c = !valid ? encode_search(b, sT, sCanon)
+                                           : p.absmax ? encode_carry(b, sE, kbase, lenm1)
+                                                      : encode_lut(b, sE, kbase, lenm1);
                         big = max(big, b & 0x7fffffffu);
                         const int64_t fe = f0 + e;
                         const int64_t je = fe / L;
@@ -1141,7 +1159,14 @@ __global__ void __launch_bounds__(kDecThreads, 4) decode_kernel(const __grid_con
             atomicOr(&sSt, __ldcg(w));
         }
         __syncthreads();
-        if (tid == 0) *p.status_out = sSt;
+        if (tid == 0) {
+            if (p.lay.flags & A8_LAYOUT_STATUS_COUNT) {
+                volatile unsigned int* w = p.status_out;  // may be host-mapped: stream order makes this safe
+                if (sSt) *w = *w + 1u;
+            } else {
+                *p.status_out = sSt;
+            }
+        }
     }
 
     auto seg_of = [&](int64_t c) {

@@ -130,6 +130,9 @@ __global__ void __launch_bounds__(kThreads) onebit_apply(const void* g, int f64,
         }
     }
     __syncthreads();
+    // codecs.py:317-318 raises before touching the state: non-finite input
+    // leaves the residual (and the bits) as they were
+    if (B) return;
     const double pl = (double)sLv[0], nl = (double)sLv[1];
     // warp chunks of 1024 consecutive elements: in step k the lanes take
     // elements 32k + lane (coalesced loads and stores of g and the residual),

@@ -134,7 +134,7 @@ def measure_error(x, spec: DataTypeSpec, *, device=None) -> ErrorReport:
     xd = q._keepalive  # the flat device input the encoder read (float32, or float64 input as is)
     dev = xd.device
     out = torch.empty(3, dtype=torch.float64, device=dev)
-    error_sums(xd, out, codes=q.codes, scale=q.scale_tensor, codebook=cb)
+    error_sums(xd, out, codes=q.codes_device, scale=q.scale_tensor, codebook=cb)
     q._finish()  # non-finite input -> InputError, as roundtrip raises in the reference
     abs_sum, rel_sum, nnz = (float(v) for v in out.cpu())
     rel_pct = float(rel_sum / nnz * 100.0) if nnz else 0.0

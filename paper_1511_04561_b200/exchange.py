@@ -41,7 +41,7 @@ import torch
 import torch.distributed as dist
 
 from . import _native as N
-from .codecs import Codebook, DataTypeSpec, build_codebook, round16, workspace
+from .codecs import Codebook, DataTypeSpec, build_codebook, round16, workspace, workspace_epoch
 from .errors import InputError, UsageError
 
 MODES = ("allgather", "two_round")
@@ -65,9 +65,12 @@ class SegmentCodec:
                scales_off: int, block_len: int, block_stride: int, scale_block_stride: int,
                rank_stride: int, nranks: int, op: int, status_idx: int = -1,
                status_blocks: int = 0, status_out: Optional[torch.Tensor] = None,
-               locals_: Optional[Sequence[torch.Tensor]] = None, local_rank: int = -1) -> None:
+               locals_: Optional[Sequence[torch.Tensor]] = None, local_rank: int = -1,
+               status_count: bool = False) -> None:
         """``locals_``: rank ``local_rank``'s term of output i is locals_[i]
-        (float32, outs[i].numel() elements) instead of its decoded codes."""
+        (float32, outs[i].numel() elements) instead of its decoded codes.
+        ``status_count``: increment ``status_out`` when the status is non-zero
+        instead of overwriting it (A8_LAYOUT_STATUS_COUNT)."""
         raise NotImplementedError
 
 
@@ -94,7 +97,7 @@ class CudaSegmentCodec(SegmentCodec):
 
     def decode(self, outs, flat_offs, scale_idx, cb, buf, codes_off, scales_off, block_len,
                block_stride, scale_block_stride, rank_stride, nranks, op, status_idx=-1,
-               status_blocks=0, status_out=None, locals_=None, local_rank=-1):
+               status_blocks=0, status_out=None, locals_=None, local_rank=-1, status_count=False):
         dev = buf.device
         book, _ = cb.device_tables(dev)
         n = len(outs)
@@ -103,7 +106,7 @@ class CudaSegmentCodec(SegmentCodec):
             segs[i] = N.DecSeg(o.data_ptr(), o.numel(), off, si, 0)
         base = buf.data_ptr()
         lay = N.Layout(base + codes_off, base + scales_off, block_len, block_stride,
-                       scale_block_stride, rank_stride, 1, 0)
+                       scale_block_stride, rank_stride, 1, N.A8_LAYOUT_STATUS_COUNT if status_count else 0)
         stream = torch.cuda.current_stream(dev).cuda_stream
         ws = workspace(dev, stream, max(n, 1))
         st = None if status_out is None else status_out.data_ptr()
@@ -227,9 +230,11 @@ class GradientExchange:
     ``graph``  capture the step (encode, decode, status copy) in a CUDA graph
                per (shapes, input/output addresses) and replay it: one launch
                per step and no host work between the kernels.  Applies on a
-               single rank (N = 1); collectives run eagerly.  With deferred
-               checks a non-finite status is reported at the next check of a
-               later call (graph replays share one host status word).
+               single rank (N = 1); collectives run eagerly.  A graph's
+               replays share one host word that counts non-finite replays
+               (A8_LAYOUT_STATUS_COUNT), so with deferred checks no report is
+               lost: a bad replay raises at the check of that call or of an
+               earlier one still pending.
     ``local_fp32``  allgather only: each rank adds its own float32 gradient
                instead of the decode of its own codes -- the paper's "8-bit
                approximation for all incoming GPUs and 32-bit gradients for
@@ -260,7 +265,7 @@ class GradientExchange:
         self.comm = comm or TorchDistComm(group)
         self._plans: dict = {}
         self._bufs: dict = {}
-        self._pending = collections.deque()  # (event or None, host status word, call)
+        self._pending = collections.deque()  # (event or None, host status word, call, graph key or None)
         self._ring = None
         self._slot = 0
         self.calls = 0
@@ -270,6 +275,7 @@ class GradientExchange:
         self._graphs: dict = {}
         self._gstream = None
         self._capturing = None  # pinned host status word while capturing
+        self._seen: dict = {}  # graph key -> non-finite count already reported
         self.local_fp32 = bool(local_fp32)
 
     # -- distributed context
@@ -317,19 +323,25 @@ class GradientExchange:
         if word.device.type == "cpu" and torch.cuda.is_available() and word.is_pinned():
             ev = torch.cuda.Event()
             ev.record()
-        self._pending.append((ev, word.view(torch.int32), self.calls))
+        self._pending.append((ev, word.view(torch.int32), self.calls, None))
         if self.check == "sync":
             self.synchronize()
 
     def _check_one(self, block: bool) -> bool:
         """Check the oldest pending status; False if it is not ready (non-blocking)."""
-        ev, word, call = self._pending[0]
+        ev, word, call, gkey = self._pending[0]
         if ev is not None:
             if not block and not ev.query():
                 return False
             ev.synchronize()
         self._pending.popleft()
-        if int(word[0]) & N.A8_STATUS_NONFINITE:
+        if gkey is not None:  # a graph's word counts its non-finite replays
+            count = int(word[0])
+            bad = count > self._seen.get(gkey, 0)
+            self._seen[gkey] = count
+        else:
+            bad = bool(int(word[0]) & N.A8_STATUS_NONFINITE)
+        if bad:
             self._pending.clear()
             raise InputError(f"exchange call {call}: cannot encode non-finite values (NaN or Inf present)")
         return True
@@ -355,6 +367,14 @@ class GradientExchange:
             if t.dtype != torch.float32 or not t.is_contiguous() or t.device != dev:
                 raise UsageError("exchange needs contiguous float32 tensors on one device")
         outs = list(out) if out is not None else tensors
+        if out is not None:
+            if len(outs) != len(tensors):
+                raise UsageError(f"out holds {len(outs)} tensors, the call has {len(tensors)}")
+            for t, o in zip(tensors, outs):
+                if (o.dtype != torch.float32 or not o.is_contiguous() or o.device != dev
+                        or o.numel() != t.numel()):
+                    raise UsageError("each out tensor must be contiguous float32 on the inputs' device, "
+                                     "with as many elements as its input")
         nranks, rank = self._world()
         sizes = tuple(t.numel() for t in tensors)
         key = (sizes, nranks)
@@ -383,6 +403,10 @@ class GradientExchange:
                tuple(o.data_ptr() for o in outs))
         hit = self._graphs.get(key)
         cur = torch.cuda.current_stream(dev)
+        if hit is not None and hit[2] != workspace_epoch(dev, self._gstream.cuda_stream):
+            # the side stream's workspace was reallocated: the graph holds a freed address
+            self._graphs.clear()
+            hit = None
         if hit is None:
             if self._gstream is None:
                 self._gstream = torch.cuda.Stream(dev)
@@ -391,7 +415,7 @@ class GradientExchange:
             with torch.cuda.stream(s):
                 self._step(tensors, outs, plan, nranks, rank, dev)  # this call's result
             cur.wait_stream(s)
-            host = torch.zeros(4, dtype=torch.uint8, pin_memory=True)  # this graph's status word
+            host = torch.zeros(4, dtype=torch.uint8, pin_memory=True)  # this graph's non-finite count
             g = torch.cuda.CUDAGraph()
             self._capturing = host
             try:
@@ -399,14 +423,16 @@ class GradientExchange:
                     self._step(tensors, outs, plan, nranks, rank, dev)
             finally:
                 self._capturing = None
-            self._graphs[key] = (g, host)
+            gkey = object()
+            self._seen[gkey] = 0
+            self._graphs[key] = (g, host, workspace_epoch(dev, s.cuda_stream), gkey)
             return
-        g, host = hit
+        g, host, _, gkey = hit
         g.replay()
         if self.check != "none":
             ev = torch.cuda.Event()
             ev.record(cur)
-            self._pending.append((ev, host.view(torch.int32), self.calls))
+            self._pending.append((ev, host.view(torch.int32), self.calls, gkey))
             if self.check == "sync":
                 self.synchronize()
 
@@ -449,7 +475,8 @@ class GradientExchange:
         loc = self.local_fp32
         if nranks == 1:
             self.codec.decode(outs, plan.offs, idx, self.cb, gathered, 0, C, C, BS, BS // 4, P, 1, op,
-                              plan.status_slot, 1, status, locals_=xs if loc else None, local_rank=0)
+                              plan.status_slot, 1, status, locals_=xs if loc else None, local_rank=0,
+                              status_count=self._capturing is not None)
             self._collect_status(status)
             return
         start = getattr(self.comm, "all_gather_async", None)

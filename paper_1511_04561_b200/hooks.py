@@ -106,7 +106,7 @@ class HookStats:
         from .errorbench import error_sums
 
         b = self._flat(before)
-        error_sums(b, self._row(site, layer, b.numel(), b.device), codes=q.codes, scale=q.scale_tensor,
+        error_sums(b, self._row(site, layer, b.numel(), b.device), codes=q.device_codes(b.device), scale=q.device_scale(b.device),
                    codebook=codebook, accumulate=True)
 
     def summary(self) -> dict:
@@ -140,6 +140,7 @@ def make_quantizer(spec: DataTypeSpec, stats: Optional[HookStats] = None, site: 
         y = decode_buffer(q, cb)
         if stats is not None:
             stats.record_codes(site, layer, q._keepalive, q, cb)
+        q._finish()  # InputError for NaN/Inf, as encode_buffer raises in mlp.py:171
         return y.to(x.dtype)
 
     return quantize

@@ -136,7 +136,7 @@ class NumpyCodec:
 
     def decode(self, outs, flat_offs, scale_idx, cb, buf, codes_off, scales_off, block_len,
                block_stride, scale_block_stride, rank_stride, nranks, op, status_idx=-1,
-               status_blocks=0, status_out=None, locals_=None, local_rank=-1):
+               status_blocks=0, status_out=None, locals_=None, local_rank=-1, status_count=False):
         mem = buf.numpy()
         table = O.book(self.kind).table
         for i, (o, f0, si) in enumerate(zip(outs, flat_offs, scale_idx)):
@@ -163,7 +163,11 @@ class NumpyCodec:
                 for j in range(status_blocks):
                     at = r * rank_stride + scales_off + 4 * (j * scale_block_stride + status_idx)
                     st |= int(np.frombuffer(mem[at:at + 4].tobytes(), np.uint32)[0])
-            status_out.view(torch.int32)[0] = st
+            w = status_out.view(torch.int32)
+            if status_count:
+                w[0] = int(w[0]) + (1 if st else 0)
+            else:
+                w[0] = st
 
 
 # ---------------------------------------------------------------------------

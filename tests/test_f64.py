@@ -35,7 +35,8 @@ def test_gpu_float64_matches_reference(case, cuda):
     cb = A.build_codebook(A.DataTypeSpec(*spec))
     for inp in (x, torch.from_numpy(x).to(cuda)):
         q = A.encode_buffer(inp, cb)
-        assert np.array_equal(q.codes.cpu().numpy(), ref)
+        assert np.array_equal(q.codes_numpy(), ref)
+        assert isinstance(q.codes, np.ndarray) == isinstance(inp, np.ndarray)  # NumPy in -> NumPy codes
         assert q.scale == s
 
 
@@ -56,4 +57,4 @@ def test_gpu_float64_edge_cases(cuda):
     # multi-chunk absmax with the peak in the last chunk
     x = rng.normal(size=3 * 4096 + 11)
     x[-1] = 9.0
-    assert np.array_equal(A.encode_buffer(x, cb).codes.cpu().numpy(), O.encode(x, "dynamic-tree", "absmax")[0])
+    assert np.array_equal(A.encode_buffer(x, cb).codes, O.encode(x, "dynamic-tree", "absmax")[0])

@@ -298,3 +298,29 @@ def test_beyond_2_to_31_elements(spec, cuda):
     assert torch.equal(y[P * reps:], db[:tail])
     del y, q, c
     torch.cuda.empty_cache()
+
+
+def test_numpy_in_numpy_out(cuda):
+    """Drop-in types (codecs.py:207-282): NumPy input gives NumPy uint8 codes
+    and a NumPy float32 decode of the input's shape; the reference's callers
+    (mlp.py:171 .astype, tensorfile.py:74 codes.astype) work on them."""
+    x = O.sample_normal(3 * 4099, 4).reshape(3, 4099)
+    for spec in (("dynamic-tree", "absmax"), ("mantissa", "decade", 1)):
+        cb = A.build_codebook(A.DataTypeSpec(*spec))
+        q = A.encode_buffer(x, cb)
+        ref, s = O.encode(x.ravel(), *spec)
+        assert isinstance(q.codes, np.ndarray) and q.codes.dtype == np.uint8
+        assert np.array_equal(q.codes, ref) and q.scale == s
+        assert q.codes.astype(np.uint8).tobytes() == ref.tobytes()
+        y = A.decode_buffer(q, cb)
+        assert isinstance(y, np.ndarray) and y.dtype == np.float32 and y.shape == x.shape
+        assert y.tobytes() == O.decode(ref, s, spec[0]).reshape(x.shape).tobytes()
+        assert y.astype(np.float64).dtype == np.float64
+        # a QuantizedTensor built by a caller from NumPy parts (tensorfile.read_tensor)
+        q2 = A.QuantizedTensor(codes=ref.copy(), shape=x.shape, spec=cb.spec, scale=s)
+        assert A.decode_buffer(q2, cb).tobytes() == y.tobytes()
+        # edits to the exposed codes are what decodes read
+        q.codes[0] = cb.zero_code
+        assert A.decode_buffer(q, cb).ravel()[0] == 0.0
+    empty = A.encode_buffer(np.zeros((0, 4), np.float32), A.build_codebook(A.DataTypeSpec("linear", "absmax")))
+    assert isinstance(empty.codes, np.ndarray) and empty.codes.size == 0 and empty.scale == 1.0

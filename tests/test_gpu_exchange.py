@@ -192,6 +192,70 @@ def test_graph_mode_reports_non_finite(cuda):
     assert torch.isfinite(outs[1]).all()
 
 
+def test_graph_mode_deferred_reports_every_bad_replay(cuda):
+    """replays share one host word; with check='deferred' a bad
+    replay followed by a clean one before any check must still raise."""
+    spec = A.DataTypeSpec("dynamic-tree", "absmax")
+    ex = A.GradientExchange(spec, graph=True)  # check="deferred"
+    ts = [torch.randn(3000, device=cuda), torch.randn(77, device=cuda)]
+    outs = [torch.empty_like(t) for t in ts]
+    ex(ts, out=outs)
+    ex(ts, out=outs)
+    ex.synchronize()
+    ts[0][7] = float("nan")
+    ex(ts, out=outs)  # bad replay, not checked yet
+    ts[0][7] = 1.0
+    with pytest.raises(A.InputError):
+        ex(ts, out=outs)  # clean replay: overwrites nothing (the word counts); may see the bad one
+        ex.synchronize()
+    ex(ts, out=outs)
+    ex.synchronize()  # reported once, clean afterwards
+
+
+def test_graph_mode_survives_workspace_growth(cuda):
+    """a call with more tensors but no more bytes must not leave a
+    captured graph pointing at a freed workspace."""
+    spec = A.DataTypeSpec("dynamic-tree", "absmax")
+    ex = A.GradientExchange(spec, check="sync", graph=True)
+    few = [(20000,), (5000,)]
+    many = [(700,)] * 30
+    fi = [torch.from_numpy(g).to(cuda) for g in grads(0, few, seed=1)]
+    fo = [torch.empty_like(t) for t in fi]
+    mi = [torch.from_numpy(g).to(cuda) for g in grads(0, many, seed=2)]
+    mo = [torch.empty_like(t) for t in mi]
+    for _ in range(3):
+        ex(fi, out=fo)
+        ex(mi, out=mo)
+    # a 40-segment eager call on the side stream grows nothing the graphs use
+    big = [torch.from_numpy(g).to(cuda) for g in grads(0, [(300,)] * 40, seed=3)]
+    ex(big)
+    for _ in range(2):
+        ex(fi, out=fo)
+        ex(mi, out=mo)
+    for t, o in zip(fi + mi, fo + mo):
+        assert o.cpu().numpy().tobytes() == O.roundtrip(t.cpu().numpy(), "dynamic-tree", "absmax").tobytes()
+
+
+def test_exchange_validates_out(cuda):
+    spec = A.DataTypeSpec("dynamic-tree", "absmax")
+    ex = A.GradientExchange(spec, check="sync")
+    ts = [torch.randn(100, device=cuda)]
+    for bad in ([torch.empty(100, device=cuda, dtype=torch.float16)], [torch.empty(99, device=cuda)],
+                [torch.empty(200, device=cuda)[::2]], []):
+        with pytest.raises(A.UsageError):
+            ex(ts, out=bad)
+
+
+def test_make_quantizer_f64_non_finite_raises(cuda):
+    """the non-fused (float64) quantizer path raises InputError like mlp.py:171."""
+    qz = A.make_quantizer(A.DataTypeSpec("dynamic-tree", "absmax"))
+    x = torch.randn(64, 10, dtype=torch.float64, device=cuda)
+    qz(x, 0)
+    x[3, 4] = float("inf")
+    with pytest.raises(A.InputError):
+        qz(x, 0)
+
+
 def test_graph_mode_many_tensors_runs_eagerly(cuda):
     """> 32 tensors: the launch plan goes through device memory, no capture."""
     spec = A.DataTypeSpec("dynamic-tree", "absmax")

@@ -86,3 +86,40 @@ def test_large_tensor_bits_and_levels(cuda):
     assert q.pos_level == pl and q.neg_level == nl
     recon = np.where(pos, pl, nl)
     assert st.residual.cpu().numpy().tobytes() == (corrected - recon).tobytes()
+
+
+def test_non_finite_leaves_state_untouched(cuda):
+    """codecs.py:317-318 raises before touching the state."""
+    rng = np.random.default_rng(5)
+    st = A.OneBitState.zeros((5000,), device=cuda)
+    A.onebit_quantize(torch.from_numpy(rng.normal(size=5000)).to(cuda), st)
+    before = st.residual.clone()
+    bad = torch.from_numpy(rng.normal(size=5000)).to(cuda)
+    bad[4321] = float("inf")
+    with pytest.raises(A.InputError):
+        A.onebit_quantize(bad, st)
+    assert torch.equal(st.residual, before)
+    q = A.onebit_quantize(bad, st, sync=False)  # asynchronous: checked later
+    with pytest.raises(A.InputError):
+        q._finish()
+    assert torch.equal(st.residual, before)
+
+
+def test_host_state_numpy_in_numpy_out(cuda):
+    """Reference types for host callers (mlp.py:313-321): NumPy residual,
+    NumPy packbits codes, float levels, NumPy decode; chained goldens."""
+    g, _ = golden()
+    st = A.OneBitState.zeros((3000,))
+    assert isinstance(st.residual, np.ndarray)
+    for k in range(12):
+        q = A.onebit_quantize(g[f"onebit/{k}/g"], st)
+        assert isinstance(q.codes, np.ndarray) and np.array_equal(q.codes, g[f"onebit/{k}/bits"]), k
+        assert (q.pos_level, q.neg_level) == tuple(g[f"onebit/{k}/levels"]), k
+        assert isinstance(st.residual, np.ndarray)
+        assert st.residual.tobytes() == g[f"onebit/{k}/residual"].tobytes(), k
+        out = A.onebit_decode(q)
+        assert isinstance(out, np.ndarray) and out.tobytes() == g[f"onebit/{k}/decoded"].tobytes(), k
+    prev = st.residual.copy()
+    with pytest.raises(A.InputError):
+        A.onebit_quantize(np.full(3000, np.nan), st)
+    assert np.array_equal(st.residual, prev)

@@ -117,6 +117,65 @@ def test_host_decision_table_reproduces_reference(case):
         assert lut.valid == 1 and lut.len <= N.LUT_MAX, name
 
 
+def _carry_table(T, amax_bits):
+    """NumPy restatement of the device's carry-table build (a8_kernels.cu
+    fill_lut_local<true> + the absmax length extension, a8_core.cuh
+    carry_entry): returns (entries, kbase) or None when a bucket would hold
+    two thresholds (the kernel then searches the thresholds)."""
+    F = int(np.count_nonzero(T < 0x7F800000))
+    if F == 0:
+        kbase, length = 0, 1
+    else:
+        kbase = int(T[0] >> 16) - 1
+        length = int(T[F - 1] >> 16) - int(T[0] >> 16) + 3
+    length = max(length, int(amax_bits >> 16) - kbase + 1)
+    if length > N.LUT_MAX:
+        return None
+    keys = np.arange(length, dtype=np.int64) + kbase
+    tk = (T[:F] >> 16).astype(np.int64)
+    lo = np.searchsorted(tk, keys, side="left")
+    cnt = np.searchsorted(tk, keys, side="right") - lo
+    if cnt.max(initial=0) > 1:
+        return None
+    tl = np.where(cnt > 0, T[np.minimum(lo, 126)] & 0xFFFF, 0).astype(np.int64)
+    e = ((lo << 16) + np.where(cnt > 0, 0x10000 - tl, 0)).astype(np.uint32)
+    return e, kbase
+
+
+def _carry_encode(x, e, kbase):
+    """The device formula of carry_sum / pack4_carry, element-wise: index
+    max(key - kbase, 0) with NO upper clamp (it must stay in the table),
+    code = byte 2 of e + (b & 0x8000ffff), sign from byte 3."""
+    b = np.ascontiguousarray(x, np.float32).view(np.uint32).astype(np.uint64)
+    j = np.maximum(((b & 0x7FFF0000) >> 16).astype(np.int64) - kbase, 0)
+    assert j.max(initial=0) < e.size, "an element indexes past the table"
+    ssum = (e[j].astype(np.uint64) + (b & 0x8000FFFF)) & 0xFFFFFFFF
+    c = (ssum >> 16) & 0xFF
+    sign = (ssum >> 24) & 0xFF
+    assert np.all((sign == 0) | (sign == 0x80)) and np.all(c < 128)
+    return (c | (sign & ((c + 0x7F) & 0x80))).astype(np.uint8)
+
+
+@pytest.mark.parametrize("case", [c for c in golden_cases() if c[1][1] == "absmax"], ids=lambda c: c[0])
+def test_carry_table_reproduces_reference(case):
+    """The absmax encode kernel's carry table (monotone codebooks), restated
+    on the host with its exact integer arithmetic, gives the reference codes."""
+    name, spec, x, ref = case
+    assert spec[0] in ("dynamic-tree", "linear")
+    assert np.array_equal(O.book(spec[0]).codes, np.arange(128, dtype=np.uint8))  # canonical code == index
+    s = O.encode(x, *spec)[1]
+    cb = A.build_codebook(A.DataTypeSpec(spec[0]))
+    lut = N.Lut()
+    N.check(N.lib.a8_build_lut_host(C.byref(cb._book), s, C.byref(lut)))
+    T = np.frombuffer(bytes(lut.T), np.uint32)[:127]
+    amax = int(np.abs(np.asarray(x, np.float32)).view(np.uint32).max(initial=0)) if x.size else 0
+    built = _carry_table(T, amax)
+    if built is None:  # the kernel searches the thresholds instead
+        assert s < 1e-30, name
+        return
+    assert np.array_equal(_carry_encode(x, *built), ref), name
+
+
 def test_error_codes_map_to_reference_exceptions():
     with pytest.raises(A.ConfigError):
         N.check(N.lib.a8_codebook(9, C.byref(N.Book())))

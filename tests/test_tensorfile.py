@@ -78,5 +78,6 @@ def test_gpu_codes_written_as_reference_files(cuda):
     assert sha(np.frombuffer(TF.encode_file_bytes(q), np.uint8)) == meta["a8t1"]["c1_dynamic_absmax_sha"]
     # and a reference file decodes on the GPU to the reference values
     r = TF.decode_file_bytes(g["a8t1/codes/dynamic-tree/absmax"].tobytes())
-    y = A.decode_buffer(r, A.build_codebook(r.spec), device=cuda).cpu().numpy()
+    y = A.decode_buffer(r, A.build_codebook(r.spec), device=cuda)
+    assert isinstance(y, np.ndarray)  # host codes decode to NumPy, as in the reference
     assert y.tobytes() == O.roundtrip(x, "dynamic-tree", "absmax").tobytes()
