@@ -1,7 +1,7 @@
 """Benchmark of the 8-bit approximation hot path on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                    [--mode allgather|two_round] [--workload c3|c1|sweep]
+                    [--mode allgather|two_round] [--no-cpu] [--no-sweep] [--eager]
 
 Metric (BASELINE.json): "8-bit codec GB/s vs HBM peak; compressed grad
 exchange fp32-equiv GB/s @1/2/4/8 GPU".  One step = one compressed exchange
@@ -123,60 +123,99 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# reference arm / CPU baseline: the oracle port of approx8.codecs on host cores
+# reference arm / CPU baseline: the reference's own CPU implementation
 
 
-def cpu_reference_step(sample, nranks: int, threads: int):
-    """One step of the reference algorithm on a bounded sample: every rank's
-    tensors are encoded+decoded (codecs.py:244-288) and accumulated in rank
-    order (the composed exchange); tensors are spread over the threads."""
+def reference_codec():
+    """(roundtrip function, kind): the UNMODIFIED reference ``approx8`` from
+    baseline/_ref (tools/install_reference.sh) when it is importable there,
+    else the oracle port of its algorithm (oracle/approx8_oracle.py)."""
+    ref = ROOT / "baseline" / "_ref"
+    if (ref / "approx8" / "codecs.py").exists():
+        if str(ref) not in sys.path:
+            sys.path.insert(0, str(ref))
+        try:
+            from approx8 import DataTypeSpec, roundtrip  # noqa: F401
+
+            spec = DataTypeSpec("dynamic-tree", "absmax")
+            return (lambda x: roundtrip(x, spec)), "reference"
+        except Exception:  # noqa: BLE001  (fall back to the port)
+            pass
     from oracle import approx8_oracle as O
 
-    def work(i):
-        acc = None
-        for r in range(nranks):
-            d = O.roundtrip(sample[r][i], "dynamic-tree", "absmax")
-            acc = d if acc is None else acc + d
-        return acc / np.float32(nranks) if nranks > 1 else acc
+    return (lambda x: O.roundtrip(x, "dynamic-tree", "absmax")), "port"
 
+
+def cpu_reference_step(per_rank, nranks: int, threads: int, rt):
+    """One exchange step of the reference algorithm: every rank's tensors
+    round-trip through encode_buffer/decode_buffer (codecs.py:244-288) and
+    are averaged in rank order in float32 (the composed exchange oracle,
+    SURVEY 8(c)); tensors (and ranks) are spread over the host threads, the
+    largest first, as the reference's own thread model runs independent
+    buffers (errorbench.py:130-139, 172)."""
+    jobs = sorted(((r, i) for r in range(nranks) for i in range(len(per_rank[r]))),
+                  key=lambda ri: -per_rank[ri[0]][ri[1]].size)
+    out: dict = {}
     with cf.ThreadPoolExecutor(max_workers=threads) as pool:
-        list(pool.map(work, range(len(sample[0]))))
+        for (r, i), d in zip(jobs, pool.map(lambda ri: rt(per_rank[ri[0]][ri[1]]), jobs)):
+            out[(r, i)] = d
+    for i in range(len(per_rank[0])):
+        acc = out[(0, i)]
+        for r in range(1, nranks):
+            acc = acc + out[(r, i)]
+        if nranks > 1:
+            acc = acc / np.float32(nranks)
+    return out
 
 
-def cpu_sample(nranks: int, threads: int, elems: int):
-    """Bounded sample of the config-3 workload: `threads` independent
-    tensors of `elems/threads` elements per rank, N(0, sigma)."""
-    per = max(1, elems // threads)
-    out = []
-    for r in range(nranks):
-        rng = np.random.default_rng(1000 + 16 * r)
-        out.append([rng.normal(0.0, SIGMA, per).astype(np.float32) for _ in range(threads)])
-    return out, per * threads
+def single_core_rate(rt, elems: int = 1 << 22):
+    """Reference round-trip throughput of ONE host core (fp32 GB/s), on one
+    2^22-element tensor of the workload's distribution."""
+    x = np.random.default_rng(1000).normal(0.0, SIGMA, elems).astype(np.float32)
+    rt(x)
+    t0 = time.perf_counter()
+    rt(x)
+    return 4.0 * elems / (time.perf_counter() - t0) / 1e9
 
 
 def run_reference(args, nranks, rank):
+    """--impl reference: the reference's CPU implementation on the SAME
+    workload as the B200 arm (config 3: all 16 AlexNet tensors of every rank,
+    61,100,840 elements each), all host threads; rank 0 only."""
     if rank != 0:
         return
+    rt, kind = reference_codec()
     threads = os.cpu_count() or 1
-    sample, n = cpu_sample(nranks, threads, args.cpu_elems)
-    for _ in range(args.warmup):
-        cpu_reference_step(sample, nranks, threads)
+    per_rank = [alexnet_grads(r) for r in range(nranks)]
+    n = sum(g.size for g in per_rank[0])
+    warm = min(args.warmup, 1)  # each step is the full workload (seconds): one warm-up pass suffices
+    for _ in range(warm):
+        cpu_reference_step(per_rank, nranks, threads, rt)
+    steps = max(1, min(args.steps, int(os.environ.get("A8_REF_MAX_STEPS", "5"))))
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        cpu_reference_step(sample, nranks, threads)
-    dt = (time.perf_counter() - t0) / args.steps
+    for _ in range(steps):
+        cpu_reference_step(per_rank, nranks, threads, rt)
+    dt = (time.perf_counter() - t0) / steps
     value = nranks * 4.0 * n / dt / 1e9
+    one = single_core_rate(rt)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": nranks,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+        "steps": steps, "warmup": warm, "ms_per_step": dt * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": workload_config(args, nranks),
-        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port",
-                         "sample": f"{nranks} rank(s) x {threads} tensors x {n // threads} elems "
-                                   f"N(0,{SIGMA}) per step, reference algorithm (oracle port of "
-                                   f"approx8.codecs encode/decode + rank-ordered average)"},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": kind,
+                         "sample": f"the full workload every step: {nranks} rank(s) x 16 AlexNet tensors "
+                                   f"({n} elements per rank) N(0,{SIGMA}), "
+                                   + ("unmodified approx8 (baseline/_ref) roundtrip" if kind == "reference"
+                                      else "oracle port of approx8.codecs roundtrip")
+                                   + " per tensor + rank-ordered float32 average; tensors over the threads",
+                         "single_core": {"value": one, "unit": "GB/s", "cores": 1,
+                                         "sample": "one 2^22-element tensor, one round trip"},
+                         "lscpu_cpus": os.cpu_count()},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if args.steps != steps:
+        line["note"] = f"timed {steps} full-workload steps (A8_REF_MAX_STEPS) of the requested {args.steps}"
     print(json.dumps(line), flush=True)
 
 
@@ -186,6 +225,190 @@ def workload_config(args, nranks):
             "tensors": len(ALEXNET), "spec": SPEC_LABEL, "scale": "per-tensor absmax",
             "mode": args.mode if nranks > 1 else "roundtrip (N=1)", "op": "avg",
             "parallelism": f"dp{nranks}", "l2": "inputs 244 MB/rank > 126 MB L2, no flush"}
+
+
+# ---------------------------------------------------------------------------
+# N > 1: parity of the exchange this run measured, and the fp32 NCCL legs
+
+PARITY_SIZES = [(int(np.prod(s)) if np.prod(s) <= 40000 else 40000 + 37 * t,) for t, s in enumerate(ALEXNET)]
+
+
+def parity_small(A, dist, mode, nranks, rank, dev):
+    """The same GradientExchange path as the timed step (same mode, op, NCCL
+    collectives, pipelined chunk blocks) on reduced AlexNet-shaped tensors,
+    against the composed oracle (oracle/approx8_oracle.py),
+    bit for bit.  Every rank regenerates every rank's (seeded) inputs."""
+    from oracle import approx8_oracle as O
+
+    def grads(r):
+        out = []
+        for t, (n,) in enumerate(PARITY_SIZES):
+            rng = np.random.default_rng(1000 + 16 * r + t)
+            out.append(rng.normal(0.0, SIGMA, n).astype(np.float32))
+        return out
+
+    per = [grads(r) for r in range(nranks)]
+    want = (O.exchange_allgather(per, "dynamic-tree", "absmax", op="avg") if mode == "allgather"
+            else O.exchange_two_round(per, "dynamic-tree", "absmax", op="avg"))
+    ex = A.GradientExchange(A.parse_spec(SPEC_LABEL), mode=mode, op="avg", check="sync", chunk_elems=1 << 16)
+    mine = [__import__("torch").from_numpy(g).to(dev) for g in per[rank]]
+    ex(mine)
+    ok = all(m.cpu().numpy().tobytes() == w.astype(np.float32).tobytes() for m, w in zip(mine, want))
+    blocks = ex._chunking(ex._plans[(tuple(g.size for g in per[rank]), nranks)], nranks)[0] if mode == "allgather" else None
+    return ok, blocks
+
+
+def outputs_agree(dist, outs, nranks):
+    """sha256 of this rank's output bytes, compared across ranks (allgather
+    and two_round both leave identical averages on every rank)."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for o in outs:
+        h.update(o.cpu().numpy().tobytes())
+    digests = [None] * nranks
+    dist.all_gather_object(digests, h.hexdigest())
+    return len(set(digests)) == 1, digests[0][:16]
+
+
+def nccl_leg(dist, algo, n, steps, rank, nranks, local_rank):
+    """fp32 NCCL all-reduce of an n-float buffer, in child processes (one per
+    rank) with NCCL_ALGO=<algo> (or NCCL's default choice), since NCCL reads
+    its tuning environment once per process.  NCCL_DEBUG output is scanned
+    for the algorithm it chose."""
+    import socket
+
+    port = [0]
+    if rank == 0:
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port[0] = sk.getsockname()[1]
+    dist.broadcast_object_list(port, src=0)
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port[0]), RANK=str(rank),
+               WORLD_SIZE=str(nranks), LOCAL_RANK=str(local_rank), NCCL_DEBUG="INFO",
+               NCCL_DEBUG_SUBSYS="INIT,TUNING,COLL")
+    env.pop("NCCL_ALGO", None)
+    if algo != "default":
+        env["NCCL_ALGO"] = algo
+    res = subprocess.run([sys.executable, str(Path(__file__).resolve()), "--nccl-leg", str(n), "--steps", str(steps)],
+                         env=env, capture_output=True, text=True, timeout=600)
+    out = None
+    for line in res.stdout.splitlines():
+        if line.startswith("{"):
+            out = json.loads(line)
+    seen = sorted({ln.split("NCCL INFO", 1)[1].strip()[:120] for ln in (res.stdout + res.stderr).splitlines()
+                   if "NCCL INFO" in ln and any(k in ln for k in ("Algo", "NVLS", "algorithm"))})[:6]
+    if out is not None:
+        out["algo_requested"] = algo
+        out["nccl_debug_algo_lines"] = seen
+    elif rank == 0:
+        out = {"algo_requested": algo, "error": (res.stderr or "")[-300:]}
+    return out
+
+
+def nccl_leg_child(n, steps):
+    """--nccl-leg: the child side of nccl_leg (torchrun-style env)."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    idx = int(os.environ["LOCAL_RANK"]) % torch.cuda.device_count()
+    torch.cuda.set_device(idx)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", idx))
+    buf = torch.randn(n, device="cuda")
+    for _ in range(3):
+        dist.all_reduce(buf)
+    torch.cuda.synchronize()
+    dist.barrier(device_ids=[idx])
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record()
+    for _ in range(steps):
+        dist.all_reduce(buf)
+    a1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([a0.elapsed_time(a1) / steps], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        ms = float(t.item())
+        print(json.dumps({"value": world * 4.0 * n / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
+                          "busbw_GBps": 2 * (world - 1) / world * 4.0 * n / (ms * 1e-3) / 1e9}), flush=True)
+    dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# N = 1: the other BASELINE configs' codec numbers, measured in the same run
+
+
+def codec_sweep(A, torch, dev, clk_sampler_cls):
+    """Config 1 (2^20 round trip, 4 codebooks), config 4 at 2^28 and 2^30
+    (dynamic-tree/absmax and mantissa/decade+1) and the per-block absmax codec
+    at 2^30 (blocks of 4096 and 1024): encode / decode kernel time of one
+    public-API call each (captured in a CUDA graph, replayed between CUDA
+    events; L2 flushed before every replay), with its own clocks record.
+    Synthetic N(0, 1) inputs generated on the device."""
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    peak, _ = peaks()
+
+    def time_graph(fn, reps):
+        s = torch.cuda.Stream(dev)
+        s.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(s):
+            fn()  # allocations happen here, outside the capture
+        torch.cuda.current_stream(dev).wait_stream(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            fn()
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return float(np.median(ts))
+
+    def case(n, label, block=None):
+        spec = A.parse_spec(label)
+        cb = A.build_codebook(spec)
+        x = torch.randn(n, device=dev)
+        y = torch.empty_like(x)
+        box = {}
+
+        def enc():
+            box["q"] = A.encode_buffer(x, cb, sync=False, block_size=block)
+
+        def dec():
+            A.decode_buffer(box["q"], cb, out=y)
+
+        reps = 7 if n >= 1 << 28 else 15
+        te = time_graph(enc, reps)
+        box["q"]._finish()
+        td = time_graph(dec, reps)
+        r = {"n": n, "spec": label, "encode_ms": te, "decode_ms": td,
+             "encode_GBps": 5.0 * n / (te * 1e-3) / 1e9, "decode_GBps": 5.0 * n / (td * 1e-3) / 1e9,
+             "roundtrip_GBps": 10.0 * n / ((te + td) * 1e-3) / 1e9}
+        r["roundtrip_frac"] = r["roundtrip_GBps"] / peak
+        if block:
+            r["block"] = block
+        del x, y, box
+        return r
+
+    out = {}
+    with clk_sampler_cls(dev.index) as clk:
+        out["c1"] = [case(1 << 20, lab) for lab in ("dynamic-tree/absmax", "linear/absmax", "static-tree/decade+1",
+                                                    "mantissa/decade+1")]
+        out["c4"] = [case(1 << k, lab) for k in (28, 30) for lab in ("dynamic-tree/absmax", "mantissa/decade+1")]
+        out["blocked"] = [case(1 << 30, "dynamic-tree/absmax", b) for b in (4096, 1024)]
+    out["clocks"] = clk.summary()
+    out["how"] = ("one public-API encode_buffer / decode_buffer call per case, CUDA-graph replayed between events, "
+                  "median of 7-15, 256 MB L2 flush before each; GB/s at 5 B/elem each way, round trip 10 B/elem; "
+                  "frac against MEASURED_PEAKS hbm_gbs")
+    del flush
+    torch.cuda.empty_cache()
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -323,25 +546,30 @@ def run_b200(args, nranks, rank, local_rank):
                 "kernel_ms_per_step": kms,
                 "codec_roundtrip_GBps": (alg["encode"] + alg["decode"]) / ((kms["encode"] + kms["decode"]) * 1e-3) / 1e9}
 
-    # north-star comparison at N > 1: a 32-bit NCCL all-reduce of the same
-    # gradient bucket (one flat fp32 buffer), fp32-equivalent GB/s
+    # N > 1: parity of this exchange path on NCCL (reduced sizes vs the
+    # oracle, and every rank holding the same C3 result), then the 32-bit
+    # NCCL all-reduce of the same gradient (north-star comparison), with
+    # NCCL_ALGO=Ring and with NCCL's default choice
     nccl = None
+    parity = None
     if nranks > 1:
-        flat = torch.cat([g.reshape(-1) for g in grads])
-        for _ in range(3):
-            dist.all_reduce(flat)
-        torch.cuda.synchronize()
-        barrier()
-        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a0.record()
-        for _ in range(args.steps):
-            dist.all_reduce(flat)
-        a1.record()
-        torch.cuda.synchronize()
-        nms = max_over_ranks(a0.elapsed_time(a1) / args.steps)
-        nccl = {"value": nranks * 4.0 * n / (nms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": nms,
-                "algo": os.environ.get("NCCL_ALGO", "default"), "speedup_8bit": value / (nranks * 4.0 * n / (nms * 1e-3) / 1e9)}
-        del flat
+        ex.synchronize()
+        agree, digest = outputs_agree(dist, outs, nranks)
+        small_ok, blocks = parity_small(A, dist, args.mode, nranks, rank, dev)
+        flags = torch.tensor([int(small_ok)], device=dev)
+        dist.all_reduce(flags, op=dist.ReduceOp.MIN)
+        parity = {"ok": bool(agree and int(flags.item())), "ranks_agree_c3": agree, "c3_digest": digest,
+                  "oracle_reduced_sizes": bool(int(flags.item())), "reduced_sizes": [n0 for (n0,) in PARITY_SIZES],
+                  "how": "same GradientExchange path (mode, NCCL collectives, pipelined chunk blocks) on reduced "
+                         "AlexNet-shaped tensors vs the composed oracle, bit-exact on every rank; C3 outputs "
+                         "identical (sha256) on every rank"}
+        legs = {}
+        for algo in ("Ring", "default"):
+            legs[algo] = nccl_leg(dist, algo, n, args.steps, rank, nranks, local_rank)
+        nccl = {"legs": legs}
+        for algo, leg in legs.items():
+            if leg and "value" in leg:
+                leg["speedup_8bit"] = value / leg["value"]
 
     # NVLink roofline of the exchange: bytes each rank must
     # receive over NVLink per step / the measured peer-copy bandwidth
@@ -435,18 +663,23 @@ def run_b200(args, nranks, rank, local_rank):
 
     cpu = None
     if rank == 0 and nranks == 1 and not args.no_cpu:
+        # the reference's CPU implementation on this very workload (all 16
+        # tensors, one full step, all host threads), plus one core
+        rt, kind = reference_codec()
         threads = os.cpu_count() or 1
-        sample, sn = cpu_sample(1, threads, args.cpu_elems)
-        cpu_reference_step(sample, 1, threads)
         t0 = time.perf_counter()
-        reps = 0
-        while time.perf_counter() - t0 < args.cpu_seconds:
-            cpu_reference_step(sample, 1, threads)
-            reps += 1
-        dt = (time.perf_counter() - t0) / reps
-        cpu = {"value": 4.0 * sn / dt / 1e9, "unit": "GB/s", "cores": threads, "kind": "port",
-               "sample": f"{threads} tensors x {sn // threads} elems N(0,{SIGMA}), {reps} reps, "
-                         f"reference algorithm (oracle port of approx8.codecs round trip)"}
+        cpu_reference_step([host], 1, threads, rt)
+        dt = time.perf_counter() - t0
+        cpu = {"value": 4.0 * n / dt / 1e9, "unit": "GB/s", "cores": threads, "kind": kind,
+               "sample": f"one full step of this workload ({n} elements, 16 tensors over {threads} threads), "
+                         + ("unmodified approx8 roundtrip (baseline/_ref)" if kind == "reference"
+                            else "oracle port of approx8.codecs roundtrip"),
+               "single_core": {"value": single_core_rate(rt), "unit": "GB/s", "cores": 1,
+                               "sample": "one 2^22-element tensor, one round trip"}}
+
+    sweep = None
+    if rank == 0 and nranks == 1 and not args.no_sweep:
+        sweep = codec_sweep(A, torch, dev, ClockSampler)
 
     if rank == 0:
         line = {
@@ -459,6 +692,8 @@ def run_b200(args, nranks, rank, local_rank):
             "gpu_launches_per_step": {k: v / args.steps for k, v in launches.items()},
             "nccl_fp32_allreduce": nccl,
             "nvlink_roofline": nvlink,
+            "parity": parity,
+            "codec_sweep": sweep,
         }
         print(json.dumps(line), flush=True)
 
@@ -470,11 +705,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--mode", default="auto", choices=["auto", "allgather", "two_round"])
-    ap.add_argument("--cpu-elems", type=int, default=1 << 23)
-    ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the config-1/4/per-block codec sub-measurements")
+    ap.add_argument("--nccl-leg", type=int, default=0, help=argparse.SUPPRESS)  # child of nccl_leg()
     ap.add_argument("--eager", action="store_true", help="no CUDA graph for the N=1 step")
     args = ap.parse_args()
+    if args.nccl_leg:
+        nccl_leg_child(args.nccl_leg, args.steps)
+        return
     if args.warmup < 3:
         args.warmup = 3
 

@@ -39,7 +39,7 @@ constexpr int kEncThreads = kConsumers + 32;     // + one producer warp
 constexpr int kStages = A8_STAGES;               // bulk-copy ring depth per CTA
 constexpr int kChunk = 4096;                     // elements per stage (16 KB)
 constexpr int kBarC = 1;                         // named barrier of the consumer warps
-constexpr size_t kEncDynSmem = (size_t)kStages * kChunk * sizeof(float);
+constexpr size_t kEncDynSmem = (size_t)kStages * kChunk * sizeof(float) + 2 * sizeof(a8_lut_t);  // ring + 2 table slots
 
 // ---- decode geometry ---------------------------------------------------------
 constexpr int kDecThreads = 256;
@@ -109,8 +109,8 @@ static_assert(sizeof(WsHead) == 64, "workspace head");
 struct SegCtl {
     unsigned int amax;
     unsigned int a_done;
-    unsigned int ready;
-    unsigned int pad;
+    unsigned int ready;  // 8-byte aligned with len: the producer reads both in one acquire load
+    unsigned int len;    // published table length
     unsigned long long t_b0, t_b1;  // table build start / end (globaltimer ns), trace
     unsigned long long t_thr, t_fill;  // thresholds done / table filled, trace
 };
@@ -135,7 +135,7 @@ struct EncParams {
     int nseg;
     int nblk;
     int absmax;
-    int pad;
+    int code_hint;  // L2 policy of the code stores: 0 default, 1 evict_first, 2 evict_last (A8_CODE_HINT)
     int64_t total;
     EncSegD segs[kInlineSegs];
     EncBlk blks[kInlineBlks];
@@ -277,6 +277,10 @@ struct StageMeta {
     int32_t simple;    // full chunk inside one block of the code layout
     int32_t last;      // the producer's next ticket is not in this run: flush after this A-chunk
     int32_t tkt;       // A8_TICKET_TRACE builds: the ticket
+    int32_t tslot;     // E: table slot of this run (when the segment changes)
+    int32_t tpre;      // 1: the producer bulk-copied the published table into tslot; 2: consumers fill it
+    int32_t tpar;      // tpre 1: parity of that slot's fill barrier
+    int32_t pad;
 };
 
 #ifdef A8_TICKET_TRACE
@@ -309,13 +313,15 @@ constexpr int kSmemBlks = 6 * kSmemSegs + 8;  // larger plans are read from glob
 // recently read by the A pass (still in L2) is re-read first.
 
 __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_constant__ EncParams p) {
-    extern __shared__ __align__(128) float sStage[];  // [kStages][kChunk]
-    __shared__ __align__(16) uint32_t sE[kLutMax];
-    __shared__ uint32_t sT[128];
+    extern __shared__ __align__(128) float sStage[];  // [kStages][kChunk], then a8_lut_t[2] (table slots)
+    a8_lut_t* const sLut = reinterpret_cast<a8_lut_t*>(sStage + (size_t)kStages * kChunk);
+    __shared__ uint32_t sT[128];  // F tickets: thresholds of a single-chunk segment
     __shared__ uint8_t sCanon[128];
     __shared__ double sV[128];
     __shared__ __align__(8) uint64_t sFull[kStages];
     __shared__ __align__(8) uint64_t sEmpty[kStages];
+    __shared__ __align__(8) uint64_t sTFull[2];  // table slot s filled by the producer's bulk copy
+    __shared__ unsigned int sRel[2];             // warps that left table slot s (monotone count)
     __shared__ StageMeta sMeta[kStages];
     __shared__ int sHdr[4];
     __shared__ unsigned int sRed[kConsumerWarps];
@@ -344,6 +350,9 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
             mbar_init(&sFull[s], 1);
             mbar_init(&sEmpty[s], kConsumerWarps);
         }
+        mbar_init(&sTFull[0], 1);
+        mbar_init(&sTFull[1], 1);
+        sRel[0] = sRel[1] = 0u;
         mbar_fence_init();
     }
     if (tid == 0) atomicMax(&p.head->t_start_inv, ~gtime());
@@ -351,8 +360,8 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
         sV[tid - 32] = p.book->values[tid - 32];
         sCanon[tid - 32] = p.book->codes[tid - 32];
     }
-    if (!p.absmax && tid >= 32)  // fixed scale: one table for every segment
-        load_lut_smem(p.static_lut, sE, sT, sCanon, p.book, sHdr, tid - 32, kConsumers);
+    if (!p.absmax && tid >= 32)  // fixed scale: one table (slot 0) for every segment
+        load_lut_smem(p.static_lut, sLut[0].e, sLut[0].T, sCanon, p.book, sHdr, tid - 32, kConsumers);
     __syncthreads();
     const uint32_t full0 = smem_addr(&sFull[0]), empty0 = smem_addr(&sEmpty[0]);  // ring barriers
 
@@ -370,6 +379,12 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
             int64_t tq2 = 0;
             int lo = 0;       // block of the current ticket (tickets only increase)
             unsigned int g = 0;
+            // table slots: every change of the E segment in this CTA's ticket
+            // stream moves to the other slot; the producer fills it with a
+            // bulk copy of the published table when it can (tpre = 1), else
+            // the consumers copy or build it (tpre = 2)
+            int pseg = -1, pslot = 1;
+            unsigned int uses0 = 0u, uses1 = 0u, fills0 = 0u, fills1 = 0u;  // per slot (scalars: no local memory)
             for (int it = 0;; ++it) {
                 const int st = it % kStages;
                 if (g == 0) tq2 = (int64_t)atomicAdd(&p.head->ticket, kTicketBatch);
@@ -403,9 +418,10 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                 const int64_t chunk = kind == kE ? c0 - k : c0 + k;
                 m.base = chunk * kChunk;
                 m.cnt = (int32_t)min((int64_t)kChunk, sg.n - m.base);
-                m.bulk = sg.aligned ? (m.cnt & ~3) : 0;
+                m.bulk = (sg.aligned && kind != kB) ? (m.cnt & ~3) : 0;  // B: the stage is build scratch
                 m.seg = bk.seg;
                 m.kind = kind;
+                m.tpre = 0;
                 {
                     const int64_t f0 = sg.flat_off + m.base;
                     if (f0 < L) {  // one block (the common layout): no 64-bit divide or multiply
@@ -423,6 +439,25 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                     const int64_t tn = tb + g;
                     m.last = !(tn < blks[lo + 1].tstart);
                 }
+                if (p.absmax && kind == kE && bk.seg != pseg) {
+                    pseg = bk.seg;
+                    pslot ^= 1;
+                    const unsigned int u = pslot ? uses1++ : uses0++;
+                    m.tslot = pslot;
+                    m.tpre = 2;
+                    // the slot is free once all consumer warps left its previous table
+                    if (u == 0u || *(volatile unsigned int*)&sRel[pslot] >= kConsumerWarps * u) {
+                        const uint2 rl = ld_acquire_v2(&p.ctl[bk.seg].ready);  // {ready, len}
+                        if (rl.x == 2u) {
+                            fence_proxy_async();  // the acquired table, seen by the bulk copy
+                            const uint32_t bytes = (uint32_t)(offsetof(a8_lut_t, e) + ((rl.y * 4u + 15u) & ~15u));
+                            mbar_arrive_expect_tx(&sTFull[pslot], bytes);
+                            bulk_g2s(&sLut[pslot], p.luts + bk.seg, bytes, &sTFull[pslot], keep);
+                            m.tpre = 1;
+                            m.tpar = (int32_t)((pslot ? fills1++ : fills0++) & 1u);
+                        }
+                    }
+                }
 #ifdef A8_TICKET_TRACE
                 m.tkt = (int32_t)t;
                 if (t < kTraceTickets) {
@@ -436,9 +471,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                 const uint32_t tx = (uint32_t)m.bulk * 4u;
                 if (tx > 0) {
                     mbar_arrive_expect_tx(&sFull[st], tx);
-                    if (m.bulk > 0)
-                        bulk_g2s(sStage + (size_t)st * kChunk, sg.x + m.base, (uint32_t)m.bulk * 4u, &sFull[st],
-                                 kind == kA ? keep : drop);
+                    bulk_g2s(sStage + (size_t)st * kChunk, sg.x + m.base, tx, &sFull[st], kind == kA ? keep : drop);
                 } else {
                     mbar_arrive(&sFull[st]);
                 }
@@ -448,7 +481,9 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
         // ===================== consumers =====================
         const int ctid = tid - 32;
         const int cw = warp - 1;
-        int cur = p.absmax ? -1 : -2;  // segment whose table is in shared memory (-2: static)
+        int cur = p.absmax ? -1 : -2;  // segment whose table is in slot `cslot` (-2: static)
+        int cslot = 0;
+        const a8_lut_t* tab = &sLut[0];
         int tvalid = sHdr[0], tkbase = sHdr[1], tlenm1 = sHdr[2];  // that table's geometry
         unsigned int tamax = 0;  // that table's max |x| bits
         uint8_t* const codes_base = p.lay.codes;
@@ -458,8 +493,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
         // A-chunks of one segment are reduced in registers; the CTA publishes
         // its partial max and chunk count once per run (when the next stage
         // is not an A-chunk of the same segment), so the global atomics and
-        // barriers are off the per-chunk path.  The CTA whose count completes
-        // the segment builds its table.  Flushing happens before any wait.
+        // barriers are off the per-chunk path.
         int aseg = -1;          // segment of the pending A run
         unsigned int amx = 0;   // per-thread max of bits(|x|) * 2
         unsigned int acnt = 0;  // A-chunks in the pending run
@@ -467,8 +501,6 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
         // A-run flush: the CTA's partial max and chunk count go out as
         // fire-and-forget reductions (the count with release semantics, so
         // the max is visible before it); nobody waits for a round trip here.
-        // The E side builds each segment's table locally once the count is
-        // complete (see the E switch below).
         int fpar = 0;  // sRed2 buffer of this flush (double-buffered: no trailing barrier)
         auto flush = [&]() {
             const unsigned int wmx = __reduce_max_sync(0xffffffffu, amx) >> 1;
@@ -486,6 +518,100 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
             aseg = -1;
             amx = 0;
             acnt = 0;
+        };
+
+        // K2 for segment `seg` into table `L` (shared memory): wait for the
+        // segment's A pass, then copy its published table, or build it
+        // (thresholds, 2 predicate evaluations each; carry-format buckets)
+        // and, as the first CTA there, publish it.  All consumer threads.
+        // kind B: only the claimant builds (T into sT, the buckets into the
+        // B ticket's own 16 KB stage; Lt = null) and publishes.
+        auto table_switch = [&](int seg, uint32_t* T, uint32_t* E, a8_lut_t* Lt, bool btk) {
+            if (ctid == 0) {
+                // every A-chunk of the segment reduced -> its max is final
+                const SegCtl* c = p.ctl + seg;
+                const unsigned int nA = (unsigned int)segs[seg].nA;
+                if (ld_acquire(&c->a_done) != nA) {
+                    const unsigned long long w0 = gtime();
+                    unsigned int ns = 32;
+                    while (ld_acquire(&c->a_done) != nA) {
+                        __nanosleep(ns);
+                        ns = min(ns * 2u, 256u);
+                    }
+                    atomicAdd(&p.head->wait_ns, gtime() - w0);  // trace
+                    atomicAdd(&p.head->waits, 1u);
+                }
+                sHdr[3] = (int)__ldcg(&c->amax);
+                // ready: 0 none, 1 being built, 2 published
+                const unsigned int r = ld_acquire(&p.ctl[seg].ready);
+                int mode = 1;  // 1 build locally, 2 copy, 3 build + publish
+                if (r == 2u)
+                    mode = 2;
+                else if (r == 0u && atomicCAS(&p.ctl[seg].ready, 0u, 1u) == 0u)
+                    mode = 3;
+                if (btk && mode != 3) mode = 0;  // B: someone else has it
+                sMode = mode;
+            }
+            nbar_sync(kBarC, kConsumers);
+            const unsigned int amax = (unsigned int)sHdr[3];
+            const int mode = sMode;
+            if (mode == 0) return;
+            if (mode == 2) {
+                load_lut_smem(p.luts + seg, E, T, sCanon, p.book, sHdr, ctid, kConsumers);
+                nbar_sync(kBarC, kConsumers);
+                if (ctid == 0) {
+                    Lt->valid = (uint32_t)sHdr[0];
+                    Lt->kbase = sHdr[1];
+                    Lt->len = (uint32_t)sHdr[2] + 1u;
+                    Lt->scale = __ldcg(&p.luts[seg].scale);
+                }
+                nbar_sync(kBarC, kConsumers);
+                return;
+            }
+            const float scale = amax == 0u ? 1.0f : __uint_as_float(amax);
+            uint32_t t = kInfBits;
+            if (ctid < 128) {
+                if (scale_ok(scale) && ctid + 1 < p.book->ndistinct) t = threshold_fast((double)scale, sV[ctid], sV[ctid + 1]);
+                T[ctid] = t;
+            }
+            const int nf = nbar_popc(kBarC, kConsumers, ctid < 127 && t < kInfBits);
+            int32_t kb;
+            uint32_t len;
+            lut_geometry(T, (uint32_t)nf, &kb, &len);
+            // carry tables reach the key of the max itself: no upper clamp
+            len = max((int32_t)len, (int32_t)(amax >> kKeyShift) - kb + 1);
+            const bool ok = len <= (uint32_t)kLutMax && fill_lut_local<true>(T, nf, sCanon, kb, E, sRed, ctid);
+            const int valid = nbar_and(kBarC, kConsumers, ok);  // also: e[] complete
+            if (Lt && ctid == 0) {
+                Lt->len = len;
+                Lt->kbase = kb;
+                Lt->valid = (uint32_t)valid;
+                Lt->nfinite = (uint32_t)nf;
+                Lt->scale = scale;
+            }
+            if (mode == 3) {  // publish for the CTAs that come later
+                a8_lut_t* G = p.luts + seg;
+                if (ctid < 128) G->T[ctid] = T[ctid];
+                if (valid) {
+                    uint4* d4 = reinterpret_cast<uint4*>(G->e);
+                    const uint4* s4 = reinterpret_cast<const uint4*>(E);
+                    for (uint32_t j = ctid; j < (len + 3) >> 2; j += kConsumers) d4[j] = s4[j];
+                }
+                if (ctid == 0) {
+                    G->len = len;
+                    G->kbase = kb;
+                    G->valid = (uint32_t)valid;
+                    G->nfinite = (uint32_t)nf;
+                    G->scale = scale;
+                    p.ctl[seg].len = len;
+                }
+                nbar_sync(kBarC, kConsumers);
+                if (ctid == 0) {
+                    __threadfence();
+                    st_release(&p.ctl[seg].ready, 2u);
+                }
+            }
+            nbar_sync(kBarC, kConsumers);  // the table in Lt is complete
         };
 
         for (int it = 0;; ++it) {
@@ -534,9 +660,19 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                 if (m.last) flush();
                 continue;
             }
+            if (m.kind == kB) {
+                // ---------------- B: build + publish the segment's table ---------
+                // (if nobody has claimed it); the stage is the scratch table
+                nbar_sync(kBarC, kConsumers);  // every warp is at this stage
+                table_switch(m.seg, sT, reinterpret_cast<uint32_t*>(sStage + (size_t)st * kChunk), nullptr, true);
+                __syncwarp();
+                if (lane == 0) mbar_arrive_a(empty0 + 8u * st);
+                continue;
+            }
 
             int valid;
             int32_t kbase, lenm1;
+            const uint32_t* Tsrch = sT;  // thresholds for the search fallback
             if (m.kind == kF) {
                 // -------- F: a single-chunk segment, entirely in this CTA ------
                 const unsigned int wmx = __reduce_max_sync(0xffffffffu, part_max()) >> 1;
@@ -558,102 +694,35 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                 valid = 0;  // encode by branch-free search over sT
                 kbase = 0;
                 lenm1 = 0;
-                cur = -1;  // sT now holds this segment's thresholds
             } else {
-            // ---------------- E: encode the chunk (B: only build) -----------
+            // ---------------- E: encode the chunk -----------
             if (cur != m.seg && cur != -2) {
-                nbar_sync(kBarC, kConsumers);  // everyone is done with the old table
-                if (ctid == 0) {
-                    // every A-chunk of the segment reduced -> its max is final
-                    const SegCtl* c = p.ctl + m.seg;
-                    const unsigned int nA = (unsigned int)segs[m.seg].nA;
-                    if (ld_acquire(&c->a_done) != nA) {
-                        const unsigned long long w0 = gtime();
-                        unsigned int ns = 32;
-                        while (ld_acquire(&c->a_done) != nA) {
-                            __nanosleep(ns);
-                            ns = min(ns * 2u, 256u);
-                        }
-                        atomicAdd(&p.head->wait_ns, gtime() - w0);  // trace
-                        atomicAdd(&p.head->waits, 1u);
-                    }
-                    sHdr[3] = (int)__ldcg(&c->amax);
-                    // the first CTA here builds the table and publishes it in the
-                    // workspace (ready: 0 none, 1 being built, 2 published); later
-                    // CTAs copy it (one 12-16 KB L2 read) instead of rebuilding
-                    unsigned int r = ld_acquire(&p.ctl[m.seg].ready);
-                    int mode = 1;  // 1 build locally, 2 copy, 3 build + publish
-                    if (r == 2u)
-                        mode = 2;
-                    else if (r == 0u && atomicCAS(&p.ctl[m.seg].ready, 0u, 1u) == 0u)
-                        mode = 3;
-                    if (m.kind == kB && mode != 3) mode = 0;  // B: someone else has it
-                    sMode = mode;
-                }
-                nbar_sync(kBarC, kConsumers);
-                const unsigned int amax = (unsigned int)sHdr[3];
-                const int mode = sMode;
-                if (mode == 0) {
-                    // B ticket, table already claimed: nothing to do
-                } else if (mode == 2) {
-                    load_lut_smem(p.luts + m.seg, sE, sT, sCanon, p.book, sHdr, ctid, kConsumers);
-                    nbar_sync(kBarC, kConsumers);
-                    tvalid = sHdr[0];
-                    tkbase = sHdr[1];
-                    tlenm1 = sHdr[2];
+                // switch to the table slot the producer chose for this run
+                const int ns = m.tslot;
+                a8_lut_t* Lt = &sLut[ns];
+                if (m.tpre == 1) {
+                    mbar_wait(&sTFull[ns], (uint32_t)m.tpar);  // the producer's bulk copy landed
                 } else {
-                    // K2, locally: scale, thresholds (2 predicate evaluations
-                    // each), bucket table in shared memory
-                    const float scale = amax == 0u ? 1.0f : __uint_as_float(amax);
-                    uint32_t t = kInfBits;
-                    if (ctid < 128) {
-                        if (scale_ok(scale) && ctid + 1 < p.book->ndistinct) t = threshold_fast((double)scale, sV[ctid], sV[ctid + 1]);
-                        sT[ctid] = t;
-                    }
-                    const int nf = nbar_popc(kBarC, kConsumers, ctid < 127 && t < kInfBits);
-                    int32_t kb;
-                    uint32_t len;
-                    lut_geometry(sT, (uint32_t)nf, &kb, &len);
-                    // carry tables reach the key of the max itself: no upper clamp
-                    len = max((int32_t)len, (int32_t)(amax >> kKeyShift) - kb + 1);
-                    tkbase = kb;
-                    tlenm1 = (int)len - 1;
-                    const bool ok = len <= (uint32_t)kLutMax && fill_lut_local<true>(sT, nf, sCanon, kb, sE, sRed, ctid);
-                    tvalid = nbar_and(kBarC, kConsumers, ok);  // also: sE complete
-                    if (mode == 3) {  // publish for the CTAs that come later
-                        a8_lut_t* L = p.luts + m.seg;
-                        if (ctid < 128) L->T[ctid] = sT[ctid];
-                        if (tvalid) {
-                            uint4* d4 = reinterpret_cast<uint4*>(L->e);
-                            const uint4* s4 = reinterpret_cast<const uint4*>(sE);
-                            for (uint32_t j = ctid; j < (len + 3) >> 2; j += kConsumers) d4[j] = s4[j];
-                        }
-                        if (ctid == 0) {
-                            L->len = len;
-                            L->kbase = kb;
-                            L->valid = (uint32_t)tvalid;
-                            L->nfinite = (uint32_t)nf;
-                        }
-                        nbar_sync(kBarC, kConsumers);
-                        if (ctid == 0) {
-                            __threadfence();
-                            st_release(&p.ctl[m.seg].ready, 2u);
-                        }
-                    }
+                    nbar_sync(kBarC, kConsumers);  // every warp is at this stage (left the old slot's table)
+                    table_switch(m.seg, Lt->T, Lt->e, Lt, false);
                 }
-                if (mode != 0) {
-                    tamax = amax;
-                    cur = m.seg;
-                }
-                if (m.kind == kB) {  // (a B ticket always switches: it precedes the segment's E pass)
+                if (cur >= 0) {  // this warp has left the previous slot
                     __syncwarp();
-                    if (lane == 0) mbar_arrive_a(empty0 + 8u * st);
-                    continue;
+                    if (lane == 0) {
+                        __threadfence_block();
+                        atomicAdd(&sRel[cslot], 1u);
+                    }
                 }
+                cur = m.seg;
+                cslot = ns;
+                tab = Lt;
+                tvalid = (int)Lt->valid;
+                tkbase = Lt->kbase;
+                tlenm1 = (int)Lt->len - 1;
+                tamax = __float_as_uint(Lt->scale);  // scale bits (1.0 for an all-zero segment)
             }
             if (cur != -2 && m.base == 0) {  // the CTA encoding chunk 0 publishes scale and status
-                const float scale = tamax == 0u ? 1.0f : __uint_as_float(tamax);
-                if (ctid < p.lay.scale_reps) p.lay.scales[ctid * p.lay.scale_block_stride + sg.scale_idx] = scale;
+                if (ctid < p.lay.scale_reps) p.lay.scales[ctid * p.lay.scale_block_stride + sg.scale_idx] = tab->scale;
                 if (ctid == 0 && tamax >= kInfBits) atomicOr(&p.head->status, A8_STATUS_NONFINITE);
             }
             if (cur == -2 && m.base == 0 && ctid < p.lay.scale_reps)
@@ -661,19 +730,28 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
             valid = tvalid;
             kbase = tkbase;
             lenm1 = tlenm1;
+            Tsrch = tab->T;
             }
+            const uint32_t* sEt = tab->e;
             unsigned int big = 0;  // max |x| bits (fixed-scale specs detect NaN/Inf here)
-            if (m.simple && valid) {
+            if (m.simple && valid && m.kind == kE) {
                 // fast path: a full chunk inside one block, bucket table
                 uint32_t* out = reinterpret_cast<uint32_t*>(codes_base + m.code_off) + ctid;
                 const uint4* in = reinterpret_cast<const uint4*>(stage) + ctid;
-                const uint32_t eb = smem_addr(sE) - (uint32_t)kbase * 4u;  // indexed by the clamped key
+                const uint32_t eb = smem_addr(sEt) - (uint32_t)kbase * 4u;  // indexed by the clamped key
                 const int32_t kmax = kbase + lenm1;
                 if (p.absmax) {  // carry table (a8_core.cuh), 5 instructions per element
-                    const int32_t emin = (int32_t)smem_addr(sE);
+                    const int32_t emin = (int32_t)smem_addr(sEt);
+                    if (p.code_hint) {
+                        const uint64_t pol = p.code_hint == 1 ? policy_evict_first() : policy_evict_last();
 #pragma unroll
-                    for (int q = 0; q < kChunk / (kConsumers * 4); ++q)
-                        out[q * kConsumers] = encode4_carry(in[q * kConsumers], eb, emin);
+                        for (int q = 0; q < kChunk / (kConsumers * 4); ++q)
+                            st_hint_u32(out + q * kConsumers, encode4_carry(in[q * kConsumers], eb, emin), pol);
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < kChunk / (kConsumers * 4); ++q)
+                            out[q * kConsumers] = encode4_carry(in[q * kConsumers], eb, emin);
+                    }
                 } else {
                     int32_t kacc = 0;  // max key: >= 0x7f80 iff some |x| is Inf/NaN
 #pragma unroll
@@ -698,20 +776,20 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                     const uint4 v = *reinterpret_cast<const uint4*>(stage + i);
                     uint32_t c0, c1, c2, c3;
                     if (valid && p.absmax) {
-                        c0 = encode_carry(v.x, sE, kbase, lenm1);
-                        c1 = encode_carry(v.y, sE, kbase, lenm1);
-                        c2 = encode_carry(v.z, sE, kbase, lenm1);
-                        c3 = encode_carry(v.w, sE, kbase, lenm1);
+                        c0 = encode_carry(v.x, sEt, kbase, lenm1);
+                        c1 = encode_carry(v.y, sEt, kbase, lenm1);
+                        c2 = encode_carry(v.z, sEt, kbase, lenm1);
+                        c3 = encode_carry(v.w, sEt, kbase, lenm1);
                     } else if (valid) {
-                        c0 = encode_lut(v.x, sE, kbase, lenm1);
-                        c1 = encode_lut(v.y, sE, kbase, lenm1);
-                        c2 = encode_lut(v.z, sE, kbase, lenm1);
-                        c3 = encode_lut(v.w, sE, kbase, lenm1);
+                        c0 = encode_lut(v.x, sEt, kbase, lenm1);
+                        c1 = encode_lut(v.y, sEt, kbase, lenm1);
+                        c2 = encode_lut(v.z, sEt, kbase, lenm1);
+                        c3 = encode_lut(v.w, sEt, kbase, lenm1);
                     } else {
-                        c0 = encode_search(v.x, sT, sCanon);
-                        c1 = encode_search(v.y, sT, sCanon);
-                        c2 = encode_search(v.z, sT, sCanon);
-                        c3 = encode_search(v.w, sT, sCanon);
+                        c0 = encode_search(v.x, Tsrch, sCanon);
+                        c1 = encode_search(v.y, Tsrch, sCanon);
+                        c2 = encode_search(v.z, Tsrch, sCanon);
+                        c3 = encode_search(v.w, Tsrch, sCanon);
                     }
                     big = max(big, max(max(v.x & 0x7fffffffu, v.y & 0x7fffffffu), max(v.z & 0x7fffffffu, v.w & 0x7fffffffu)));
                     *reinterpret_cast<uint32_t*>(codes_base + f + j * gap) = c0 | (c1 << 8) | (c2 << 16) | (c3 << 24);
@@ -719,9 +797,9 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                     const int e_end = min(i + 4, m.cnt);
                     for (int e = i; e < e_end; ++e) {
                         const uint32_t b = e < m.bulk ? __float_as_uint(stage[e]) : __float_as_uint(sg.x[m.base + e]);
-                        const uint32_t c = !valid ? encode_search(b, sT, sCanon)
-                                           : p.absmax ? encode_carry(b, sE, kbase, lenm1)
-                                                      : encode_lut(b, sE, kbase, lenm1);
+                        const uint32_t c = !valid ? encode_search(b, Tsrch, sCanon)
+                                           : p.absmax ? encode_carry(b, sEt, kbase, lenm1)
+                                                      : encode_lut(b, sEt, kbase, lenm1);
                         big = max(big, b & 0x7fffffffu);
                         const int64_t fe = f0 + e;
                         const int64_t je = fe / L;
@@ -753,6 +831,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
             p.ctl[i].amax = 0u;
             p.ctl[i].a_done = 0u;
             p.ctl[i].ready = 0u;
+            p.ctl[i].len = 0u;
         }
         if (tid < p.lay.scale_reps) {
             const unsigned int stt = atomicAdd(&p.head->status, 0u) | (p.status_in ? *p.status_in : 0u);
@@ -1729,6 +1808,13 @@ extern "C" int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_de
     p.nseg = nseg;
     p.nblk = nblk;
     p.absmax = absmax ? 1 : 0;
+    {
+        static const int hint = [] {
+            const char* v = getenv("A8_CODE_HINT");
+            return v ? atoi(v) : 0;
+        }();
+        p.code_hint = hint;
+    }
     p.total = blks[nblk].tstart;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if ((int)blks.size() > max_blocks(nseg)) return fail(A8_ERR_USAGE, "a8_encode: schedule overflow");

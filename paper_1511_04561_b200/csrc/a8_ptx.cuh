@@ -82,6 +82,10 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
     return p;
 }
 
+__device__ __forceinline__ void st_hint_u32(uint32_t* p, uint32_t v, uint64_t policy) {
+    asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(policy) : "memory");
+}
+
 // ---- named barriers (id 0 is __syncthreads) ------------------------------------
 
 __device__ __forceinline__ void nbar_sync(int id, int nthreads) {
@@ -121,6 +125,19 @@ __device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
     unsigned int v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
+}
+
+// {ready, len} of a segment's control block in one acquire load (8-byte aligned pair)
+__device__ __forceinline__ uint2 ld_acquire_v2(const unsigned int* p) {
+    uint2 v;
+    asm volatile("ld.acquire.gpu.global.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p) : "memory");
+    return v;
+}
+
+// Orders this thread's earlier generic-proxy accesses (e.g. an acquire
+// load) before its later async-proxy operations (bulk copies).
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async;" ::: "memory");
 }
 
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {

@@ -1,0 +1,15 @@
+# Same-box A/B of the bench's encode + step time: product build vs _lib_var/$1 (default: old).
+V=${1:-old}
+mkdir -p gpurun_out
+: > gpurun_out/ab_enc.txt
+for rep in 1 2 3; do
+for v in base $V; do
+  if [ $v = base ]; then lib=paper_1511_04561_b200/_lib/libapprox8_b200.so; else lib=paper_1511_04561_b200/_lib_var/$v/libapprox8_b200.so; fi
+  A8_LIB=$lib timeout 300 python bench.py --steps 200 --warmup 5 --no-cpu 2>>gpurun_out/ab_enc.err | python -c "
+import sys,json
+for l in sys.stdin:
+    r=json.loads(l); k=r['roofline']['kernel_ms_per_step']
+    print('$v', 'step', round(r['ms_per_step']*1e3,1), 'enc', round(k['encode']*1e3,1), 'dec', round(k['decode']*1e3,1), 'frac', round(r['roofline']['frac'],3))" >> gpurun_out/ab_enc.txt
+done
+done
+cat gpurun_out/ab_enc.txt
