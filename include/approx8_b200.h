@@ -228,6 +228,24 @@ int a8_onebit_quantize(const void* g, int g_is_f64, double* residual, int64_t n,
 /* onebit_decode (codecs.py:342-348): out[i] = bit ? levels[0] : levels[1]. */
 int a8_onebit_decode(const uint8_t* bits, int64_t n, const float* levels, float* out, void* stream);
 
+/* 1-bit data-parallel exchange, decode side (the DP seam mlp.py:313-321
+ * across N ranks; the reference has no multi-rank function).  Rank r's slab
+ * starts at slabs + r * rank_stride and holds, for segment s, its packed
+ * bits at segs[s].bit_off, its {pos, neg} levels (float32) at levels_off +
+ * 8 s and its quantizer status word at status_off + 4 s.
+ *   out_s[i] = sum_r (bit_r(i) ? pos_r : neg_r), rank order, float32
+ *   (round-to-nearest); op = 1 then divides by float32(nranks).
+ * status_out (optional, device uint32): OR of every rank's first nstatus
+ * status words.  At most 32 segments per call.                              */
+typedef struct a8_ob_seg {
+    float* out;
+    int64_t n;
+    int64_t bit_off; /* bytes from the slab start */
+} a8_ob_seg_t;
+int a8_onebit_reduce(const a8_ob_seg_t* segs, int nseg, const uint8_t* slabs, int64_t rank_stride,
+                     int64_t levels_off, int64_t status_off, int nstatus, int nranks, int op, uint32_t* status_out,
+                     void* stream);
+
 /* Per-block max-abs codec (north star: "optional per-block max-abs"; not a
  * reference feature).  Block b = elements [b*block, (b+1)*block) is encoded
  * exactly as encode_buffer(x[block b]) with absmax normalisation

@@ -27,10 +27,12 @@ from .codecs import (
 from .errorbench import ErrorReport, SampleSpec, measure_error, run_error_suite
 from .errors import ApproxError, ConfigError, InputError, TrainingError, UsageError
 from .exchange import (
+    ONEBIT,
     CompressedAllGather,
     DDPHookState,
     GradientExchange,
     LocalExchange,
+    OneBitExchange,
     a8_comm_hook,
     exchange,
 )
@@ -57,6 +59,8 @@ __all__ = [
     "DataTypeSpec",
     "ErrorReport",
     "GradientExchange",
+    "OneBitExchange",
+    "ONEBIT",
     "HookMode",
     "HookStats",
     "InputError",

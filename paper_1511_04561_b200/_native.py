@@ -77,6 +77,10 @@ class DecSeg(C.Structure):
     ]
 
 
+class ObSeg(C.Structure):
+    _fields_ = [("out", C.c_void_p), ("n", C.c_int64), ("bit_off", C.c_int64)]
+
+
 class Layout(C.Structure):
     _fields_ = [
         ("codes", C.c_void_p),
@@ -126,6 +130,8 @@ SIGNATURES = {
          C.c_size_t, C.c_void_p],
     ),
     "a8_onebit_decode": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "a8_onebit_reduce": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int,
+                                   C.c_int, C.c_void_p, C.c_void_p]),
     "a8_roundtrip": (
         C.c_int,
         [C.POINTER(EncSeg), C.POINTER(C.c_void_p), C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,

@@ -20,6 +20,7 @@
 #include <string>
 
 #include "a8_core.cuh"
+#include "a8_ptx.cuh"
 #include "approx8_b200.h"
 
 namespace a8 {
@@ -154,6 +155,172 @@ __global__ void __launch_bounds__(kThreads, 4) blocked_encode_kernel(const float
     if (__syncthreads_or(bad) && tid == 0) atomicOr(status, A8_STATUS_NONFINITE);
 }
 
+// ---------------------------------------------------------------------------
+// Per-block encode, streaming form (full 4096-element chunks of 16-byte
+// aligned input).  Warp 0 streams chunks global -> shared with bulk copies
+// into a kBStages ring; 8 consumer warps process chunk k in two halves
+// that are software-pipelined across iterations:
+//   iteration k: block maxes of chunk k -> barrier -> thresholds of chunk
+//   k's blocks (float64, the reference decision) AND the encode of chunk
+//   k-1 (whose thresholds the previous iteration computed) -> barrier
+// so the float64 latency of the thresholds overlaps the encode work.
+// Encode per element, exactly the reference decision (codecs.py:254-268):
+//   guess  c = G[key(fl32(|x| * fl32(1/s)))]   (G: scale-independent, per codebook)
+//   verify p = c + (bits|x| >= T_c(s))          (T: the block's exact thresholds)
+// G[k] counts the midpoints surely below bucket k, so c <= p <= c + 1 as
+// long as every bucket (widened by the rounding of the normalised value)
+// holds at most one midpoint -- true for the two absmax codebooks
+// (dynamic-tree, linear; tests/test_blocked.py checks it).  Scales outside
+// [2^-100, 2^100] and non-finite blocks take the 7-step threshold search.
+constexpr int kBStages = 6;
+constexpr int kBChunk = 4096;
+constexpr int kBWarps = 8;
+constexpr int kBCons = kBWarps * 32;
+constexpr int kGKey0 = 0x3400;                 // key (bits >> 16) of 2^-23: every midpoint lies above
+constexpr int kGLen = 0x3f80 - kGKey0 + 1;      // keys up to that of 1.0 (|x|/s <= 1 up to rounding)
+constexpr double kGMargin = 0x1p-18;            // > rounding of fl32(|x| * fl32(1/s)) and of T_i / s
+constexpr size_t kBDynSmem = (size_t)kBStages * kBChunk * sizeof(float);
+
+__device__ __forceinline__ uint32_t guess_verify(uint32_t b, float r, const uint8_t* sG, const uint32_t* T) {
+    const float y = fabsf(__uint_as_float(b)) * r;
+    const int key = (int)(__float_as_uint(y) >> 16);
+    const uint32_t c = sG[max(key - kGKey0, 0)];
+    return c + ((b & 0x7fffffffu) >= T[c] ? 1u : 0u);
+}
+
+template <int V>  // B = 1024 * V; NB = 4 / V blocks per chunk
+__global__ void __launch_bounds__(kBCons + 32, 2) blocked_encode_stream(const float* __restrict__ x, int64_t nchunks,
+                                                                       const a8_book_t* book, uint8_t* codes,
+                                                                       float* scales, unsigned int* status) {
+    constexpr int NB = 4 / V;
+    extern __shared__ __align__(128) float sStage[];  // [kBStages][kBChunk]
+    __shared__ uint8_t sG[(kGLen + 15) & ~15];
+    __shared__ uint32_t sT[2][NB][128];
+    __shared__ float sR[2][NB];
+    __shared__ int sFast[2][NB];
+    __shared__ unsigned int sRed[kBWarps][NB];
+    __shared__ double sMid[128];
+    __shared__ double sV[128];
+    __shared__ uint8_t sCanon[128];
+    __shared__ __align__(8) uint64_t sFull[kBStages];
+    __shared__ __align__(8) uint64_t sEmpty[kBStages];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int D = book->ndistinct;
+    if (tid < 128) {
+        sV[tid] = book->values[tid];
+        sCanon[tid] = book->codes[tid];
+        sMid[tid] = tid + 1 < D ? 0.5 * (book->values[tid] + book->values[tid + 1]) : 1e300;
+    }
+    if (tid == 0) {
+        for (int i = 0; i < kBStages; ++i) {
+            mbar_init(&sFull[i], 1);
+            mbar_init(&sEmpty[i], kBWarps);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    // G[k] = #{i : mid_i * (1 + margin) < lowest value of bucket k}
+    for (int j = tid; j < kGLen; j += blockDim.x) {
+        const double yk = (double)__uint_as_float((uint32_t)(kGKey0 + j) << 16);
+        int p = 0;
+#pragma unroll
+        for (int step = 64; step; step >>= 1)
+            if (p + step <= D - 1 && sMid[p + step - 1] * (1.0 + kGMargin) < yk) p += step;
+        sG[j] = (uint8_t)p;
+    }
+    __syncthreads();
+    const int64_t nmy = nchunks > blockIdx.x ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const uint32_t full0 = smem_addr(&sFull[0]), empty0 = smem_addr(&sEmpty[0]);
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint64_t drop = policy_evict_first();
+            for (int64_t it = 0; it < nmy; ++it) {
+                const int st = (int)(it % kBStages);
+                mbar_wait_a(empty0 + 8u * st, (uint32_t)((it / kBStages) & 1) ^ 1u);
+                mbar_arrive_expect_tx(&sFull[st], kBChunk * 4);
+                bulk_g2s(sStage + (size_t)st * kBChunk, x + (blockIdx.x + it * gridDim.x) * (int64_t)kBChunk,
+                         kBChunk * 4, &sFull[st], drop);
+            }
+        }
+        return;
+    }
+    const int ct = tid - 32, cw = warp - 1;
+    unsigned int bad = 0;
+    for (int64_t it = 0; it <= nmy; ++it) {
+        const int slot = (int)(it & 1);
+        const int64_t chunk = blockIdx.x + it * gridDim.x;
+        if (it < nmy) {  // ---- block maxes of chunk it
+            const int st = (int)(it % kBStages);
+            mbar_wait_a(full0 + 8u * st, (uint32_t)((it / kBStages) & 1));
+            const uint4* in = reinterpret_cast<const uint4*>(sStage + (size_t)st * kBChunk) + ct;
+            unsigned int mx[NB];
+#pragma unroll
+            for (int j = 0; j < NB; ++j) mx[j] = 0u;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint4 v = in[q * kBCons];
+                mx[q / V] = __vimax3_u32(mx[q / V], v.x * 2u, v.y * 2u);
+                mx[q / V] = __vimax3_u32(mx[q / V], v.z * 2u, v.w * 2u);
+            }
+#pragma unroll
+            for (int j = 0; j < NB; ++j) {
+                const unsigned int w = __reduce_max_sync(0xffffffffu, mx[j]) >> 1;
+                if (lane == 0) sRed[cw][j] = w;
+            }
+        }
+        nbar_sync(1, kBCons);
+        if (it < nmy) {  // ---- thresholds of chunk it's blocks (codecs.py:237-241, 260-265)
+            for (int k = ct; k < 128 * NB; k += kBCons) {
+                const int j = k >> 7, i = k & 127;
+                unsigned int amax = 0;
+#pragma unroll
+                for (int w = 0; w < kBWarps; ++w) amax = max(amax, sRed[w][j]);
+                const float scale = amax == 0u ? 1.0f : __uint_as_float(amax);
+                uint32_t t = kInfBits;
+                if (scale_ok(scale) && i + 1 < D) t = threshold_fast((double)scale, sV[i], sV[i + 1]);
+                sT[slot][j][i] = t;
+                if (i == 0) {
+                    scales[chunk * NB + j] = scale;
+                    sR[slot][j] = __frcp_rn(scale);
+                    sFast[slot][j] = amax >= 0x0d800000u && amax <= 0x71800000u;  // 2^-100 <= s <= 2^100
+                    if (amax >= kInfBits) bad = 1u;
+                }
+            }
+        }
+        if (it > 0) {  // ---- encode chunk it-1 with the previous iteration's thresholds
+            const int ps = slot ^ 1;
+            const int st = (int)((it - 1) % kBStages);
+            const uint4* in = reinterpret_cast<const uint4*>(sStage + (size_t)st * kBChunk) + ct;
+            uint32_t* out = reinterpret_cast<uint32_t*>(codes + (chunk - gridDim.x) * (int64_t)kBChunk) + ct;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int j = q / V;
+                const uint4 v = in[q * kBCons];
+                const uint32_t* T = sT[ps][j];
+                uint32_t c0, c1, c2, c3;
+                if (sFast[ps][j]) {
+                    const float r = sR[ps][j];
+                    c0 = guess_verify(v.x, r, sG, T);
+                    c1 = guess_verify(v.y, r, sG, T);
+                    c2 = guess_verify(v.z, r, sG, T);
+                    c3 = guess_verify(v.w, r, sG, T);
+                } else {  // search (codes carry their sign already: strip it, re-attached below)
+                    c0 = encode_search(v.x & 0x7fffffffu, T, sCanon);
+                    c1 = encode_search(v.y & 0x7fffffffu, T, sCanon);
+                    c2 = encode_search(v.z & 0x7fffffffu, T, sCanon);
+                    c3 = encode_search(v.w & 0x7fffffffu, T, sCanon);
+                }
+                const uint32_t packed = __byte_perm(__byte_perm(c0, c1, 0x0040), __byte_perm(c2, c3, 0x0040), 0x5410);
+                __stcs(out + q * kBCons, attach_signs4(packed, v.x, v.y, v.z, v.w));
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive_a(empty0 + 8u * st);
+        }
+        nbar_sync(1, kBCons);  // sT[slot] complete; sRed free
+    }
+    if (bad) atomicOr(status, A8_STATUS_NONFINITE);
+}
+
 template <int V>
 __global__ void __launch_bounds__(kThreads) blocked_decode_kernel(const uint8_t* __restrict__ codes, int64_t n,
                                                                  const float* __restrict__ scales,
@@ -203,6 +370,34 @@ extern "C" int a8_encode_blocked(const float* x, int64_t n, int64_t block, const
     if (reinterpret_cast<uintptr_t>(codes) & 3) return fail(A8_ERR_USAGE, "a8_encode_blocked: codes must be 4-byte aligned");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     cudaMemsetAsync(status_out, 0, sizeof(uint32_t), st);
+    // full 4096-element chunks of aligned input: the streaming kernel; the
+    // ragged tail (and unaligned input) below
+    const int64_t nchunks = (reinterpret_cast<uintptr_t>(x) & 15) ? 0 : n / kBChunk;
+    if (nchunks > 0) {
+        static int sms = 0;
+        if (!sms) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaFuncSetAttribute(blocked_encode_stream<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBDynSmem);
+            cudaFuncSetAttribute(blocked_encode_stream<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBDynSmem);
+            cudaFuncSetAttribute(blocked_encode_stream<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBDynSmem);
+        }
+        const int g = (int)std::min<int64_t>(nchunks, (int64_t)sms * 2);
+        const a8_book_t* book = static_cast<const a8_book_t*>(book_dev);
+        unsigned int* stt = reinterpret_cast<unsigned int*>(status_out);
+        if (block == 1024)
+            blocked_encode_stream<1><<<g, kBCons + 32, kBDynSmem, st>>>(x, nchunks, book, codes, scales, stt);
+        else if (block == 2048)
+            blocked_encode_stream<2><<<g, kBCons + 32, kBDynSmem, st>>>(x, nchunks, book, codes, scales, stt);
+        else
+            blocked_encode_stream<4><<<g, kBCons + 32, kBDynSmem, st>>>(x, nchunks, book, codes, scales, stt);
+        const int64_t done = nchunks * kBChunk;
+        x += done;
+        n -= done;
+        codes += done;
+        scales += done / block;
+    }
     const int64_t nblk = (n + block - 1) / block;
     if (nblk > 0) {
         const a8_book_t* book = static_cast<const a8_book_t*>(book_dev);

@@ -244,6 +244,38 @@ __device__ bool fill_lut_local(const uint32_t* T, uint32_t F, const uint8_t* can
     return ok;
 }
 
+// The carry-format table (a8_core.cuh carry_entry) without atomics, zero
+// fill or scans: thread ctid owns buckets [16 ctid, 16 ctid + 16); two
+// independent branch-free searches give the thresholds below and inside its
+// range, then it walks its 16 buckets.  No barrier inside (T[] must be
+// complete before the call).  Returns false (for this thread) if one of its
+// buckets holds two thresholds.
+__device__ __forceinline__ bool fill_lut_carry(const uint32_t* T, uint32_t F, int32_t kbase, uint32_t len,
+                                               uint32_t* e, int ctid) {
+    const int32_t j0 = 16 * ctid;
+    if ((uint32_t)j0 >= len) return true;
+    const int32_t k0 = kbase + j0;
+    uint32_t p = k0 <= 0 ? 0u : count_below(T, F, (uint32_t)k0 << kKeyShift);
+    const uint32_t hi = count_below(T, F, (uint32_t)(k0 + 16) << kKeyShift);
+    uint32_t tp = p < hi ? T[p] : 0xffffffffu;  // next threshold inside the range
+    bool ok = true;
+    uint32_t v[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        const bool has = (int32_t)(tp >> kKeyShift) == k0 + q;
+        v[q] = carry_entry(p, has ? 1u : 0u, tp);
+        if (has) {
+            ++p;
+            tp = p < hi ? T[p] : 0xffffffffu;
+            ok &= (int32_t)(tp >> kKeyShift) != k0 + q;  // a second threshold in this bucket
+        }
+    }
+    uint4* e4 = reinterpret_cast<uint4*>(e) + 4 * ctid;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) e4[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    return ok;
+}
+
 // Copy a table into shared memory.  Readers bypass L1: the table may have
 // been written by another CTA of this launch.
 __device__ void load_lut_smem(const a8_lut_t* src, uint32_t* sE, uint32_t* sT, uint8_t* sCanon,
@@ -288,6 +320,14 @@ struct StageMeta {
 constexpr int kTraceTickets = 1 << 17;
 __device__ unsigned long long g_ticket_trace[kTraceTickets][5];  // issue, done, kind|seg|cta, t known, stage free
 __device__ unsigned long long g_flush_trace[32][512][4];  // per (seg, cta): flush start, atom back, amax back, chunks
+// table switches / B builds: ticket, cta | kind << 16 | tpre << 20 | mode << 24, seg, t0 (stage ready),
+// t1 (max final), t2 (thresholds), t3 (table complete), t4 (published / switch done)
+constexpr int kTraceSw = 1 << 14;
+__device__ unsigned long long g_switch_trace[kTraceSw][8];
+__device__ unsigned int g_switch_n;
+#define SW_STAMP(k) do { if (ctid == 0) sw[k] = gtime(); } while (0)
+#else
+#define SW_STAMP(k) do { } while (0)
 #endif
 
 #ifndef A8_TICKET_BATCH
@@ -494,6 +534,9 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
         // its partial max and chunk count once per run (when the next stage
         // is not an A-chunk of the same segment), so the global atomics and
         // barriers are off the per-chunk path.
+#ifdef A8_TICKET_TRACE
+        int sw_tkt = 0;  // ticket of the stage being processed (switch trace)
+#endif
         int aseg = -1;          // segment of the pending A run
         unsigned int amx = 0;   // per-thread max of bits(|x|) * 2
         unsigned int acnt = 0;  // A-chunks in the pending run
@@ -527,6 +570,9 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
         // kind B: only the claimant builds (T into sT, the buckets into the
         // B ticket's own 16 KB stage; Lt = null) and publishes.
         auto table_switch = [&](int seg, uint32_t* T, uint32_t* E, a8_lut_t* Lt, bool btk) {
+#ifdef A8_TICKET_TRACE
+            unsigned long long sw[5] = {gtime(), 0, 0, 0, 0};
+#endif
             if (ctid == 0) {
                 // every A-chunk of the segment reduced -> its max is final
                 const SegCtl* c = p.ctl + seg;
@@ -552,10 +598,30 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                 if (btk && mode != 3) mode = 0;  // B: someone else has it
                 sMode = mode;
             }
+            SW_STAMP(1);
             nbar_sync(kBarC, kConsumers);
             const unsigned int amax = (unsigned int)sHdr[3];
             const int mode = sMode;
-            if (mode == 0) return;
+#ifdef A8_TICKET_TRACE
+            auto sw_log = [&](int md) {
+                if (ctid == 0) {
+                    sw[4] = gtime();
+                    const unsigned int i = atomicAdd(&g_switch_n, 1u);
+                    if (i < kTraceSw) {
+                        g_switch_trace[i][0] = (unsigned long long)sw_tkt;
+                        g_switch_trace[i][1] = blockIdx.x | ((unsigned long long)btk << 16) | ((unsigned long long)md << 24);
+                        g_switch_trace[i][2] = seg;
+                        for (int q = 0; q < 5; ++q) g_switch_trace[i][3 + q] = sw[q];
+                    }
+                }
+            };
+#else
+            auto sw_log = [&](int) {};
+#endif
+            if (mode == 0) {
+                sw_log(0);
+                return;
+            }
             if (mode == 2) {
                 load_lut_smem(p.luts + seg, E, T, sCanon, p.book, sHdr, ctid, kConsumers);
                 nbar_sync(kBarC, kConsumers);
@@ -566,6 +632,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                     Lt->scale = __ldcg(&p.luts[seg].scale);
                 }
                 nbar_sync(kBarC, kConsumers);
+                sw_log(2);
                 return;
             }
             const float scale = amax == 0u ? 1.0f : __uint_as_float(amax);
@@ -575,13 +642,15 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                 T[ctid] = t;
             }
             const int nf = nbar_popc(kBarC, kConsumers, ctid < 127 && t < kInfBits);
+            SW_STAMP(2);
             int32_t kb;
             uint32_t len;
             lut_geometry(T, (uint32_t)nf, &kb, &len);
             // carry tables reach the key of the max itself: no upper clamp
             len = max((int32_t)len, (int32_t)(amax >> kKeyShift) - kb + 1);
-            const bool ok = len <= (uint32_t)kLutMax && fill_lut_local<true>(T, nf, sCanon, kb, E, sRed, ctid);
+            const bool ok = len <= (uint32_t)kLutMax && fill_lut_carry(T, (uint32_t)nf, kb, len, E, ctid);
             const int valid = nbar_and(kBarC, kConsumers, ok);  // also: e[] complete
+            SW_STAMP(3);
             if (Lt && ctid == 0) {
                 Lt->len = len;
                 Lt->kbase = kb;
@@ -612,12 +681,16 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                 }
             }
             nbar_sync(kBarC, kConsumers);  // the table in Lt is complete
+            sw_log(mode);
         };
 
         for (int it = 0;; ++it) {
             const int st = it % kStages;
             mbar_wait_a(full0 + 8u * st, (it / kStages) & 1);
             const StageMeta m = sMeta[st];
+#ifdef A8_TICKET_TRACE
+            sw_tkt = m.tkt | (m.tpre << 28);
+#endif
             if (aseg >= 0 && (m.kind != kA || m.seg != aseg)) flush();
             if (m.kind == kEnd) break;
             const EncSegD& sg = segs[m.seg];
@@ -701,7 +774,23 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                 const int ns = m.tslot;
                 a8_lut_t* Lt = &sLut[ns];
                 if (m.tpre == 1) {
+#ifdef A8_TICKET_TRACE
+                    const unsigned long long w0 = gtime();
+#endif
                     mbar_wait(&sTFull[ns], (uint32_t)m.tpar);  // the producer's bulk copy landed
+#ifdef A8_TICKET_TRACE
+                    if (ctid == 0) {
+                        const unsigned int i = atomicAdd(&g_switch_n, 1u);
+                        if (i < kTraceSw) {
+                            g_switch_trace[i][0] = (unsigned long long)sw_tkt;
+                            g_switch_trace[i][1] = blockIdx.x | (4ull << 24);
+                            g_switch_trace[i][2] = m.seg;
+                            g_switch_trace[i][3] = w0;
+                            g_switch_trace[i][4] = g_switch_trace[i][5] = g_switch_trace[i][6] = 0;
+                            g_switch_trace[i][7] = gtime();
+                        }
+                    }
+#endif
                 } else {
                     nbar_sync(kBarC, kConsumers);  // every warp is at this stage (left the old slot's table)
                     table_switch(m.seg, Lt->T, Lt->e, Lt, false);
@@ -1610,6 +1699,17 @@ extern "C" int a8_debug_ticket_trace(uint64_t* out, int64_t n) {
 extern "C" int a8_debug_res_trace(uint64_t* out) {  // [2][8]
     cudaError_t e = cudaMemcpyFromSymbol(out, a8::g_res_trace, sizeof(a8::g_res_trace));
     return e == cudaSuccess ? A8_OK : fail(A8_ERR_CUDA, cudaGetErrorString(e));
+}
+extern "C" int a8_debug_switch_trace(uint64_t* out, int64_t n, int reset) {  // [n][8]; returns the count
+    unsigned int cnt = 0;
+    cudaMemcpyFromSymbol(&cnt, a8::g_switch_n, sizeof(cnt));
+    if (n > a8::kTraceSw) n = a8::kTraceSw;
+    cudaError_t e = cudaMemcpyFromSymbol(out, a8::g_switch_trace, sizeof(uint64_t) * 8 * n);
+    if (reset) {
+        const unsigned int z = 0;
+        cudaMemcpyToSymbol(a8::g_switch_n, &z, sizeof(z));
+    }
+    return e == cudaSuccess ? (int)cnt : -fail(A8_ERR_CUDA, cudaGetErrorString(e));
 }
 extern "C" int a8_debug_flush_trace(uint64_t* out) {  // [32][512][4]
     cudaError_t e = cudaMemcpyFromSymbol(out, a8::g_flush_trace, sizeof(a8::g_flush_trace));

@@ -205,6 +205,70 @@ __global__ void __launch_bounds__(kThreads) onebit_decode_k(const uint8_t* bits,
         out[i] = (bits[i >> 3] >> (7 - (i & 7))) & 1u ? pl : nl;
 }
 
+// The 1-bit exchange's decode-sum(-average) over N gathered slabs (the DP
+// seam of mlp.py:313-321 across ranks): out[i] = sum_r (bit_r(i) ? pos_r :
+// neg_r), rank order, float32, then / N.  One thread per byte of bits (8
+// elements); segments are located by a search over the byte prefix sums.
+constexpr int kObSegs = 32;
+struct ObParams {
+    a8_ob_seg_t segs[kObSegs];
+    int64_t byte_start[kObSegs + 1];  // prefix sums of ceil(n/8)
+    const uint8_t* slabs;
+    int64_t rank_stride, levels_off, status_off;
+    int nseg, nranks, op, nstatus;
+    uint32_t* status_out;
+};
+
+__global__ void __launch_bounds__(kThreads) onebit_reduce_k(const __grid_constant__ ObParams p) {
+    if (p.status_out && blockIdx.x == 0) {
+        __shared__ unsigned int sSt;
+        if (threadIdx.x == 0) sSt = 0u;
+        __syncthreads();
+        for (int i = threadIdx.x; i < p.nranks * p.nstatus; i += kThreads) {
+            const int r = i / p.nstatus, sg = i % p.nstatus;
+            atomicOr(&sSt, *reinterpret_cast<const uint32_t*>(p.slabs + r * p.rank_stride + p.status_off + 4 * sg));
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) *p.status_out = sSt;
+    }
+    const int64_t total = p.byte_start[p.nseg];
+    const float invn = 1.0f / (float)p.nranks;
+    const bool pow2 = (p.nranks & (p.nranks - 1)) == 0;
+    for (int64_t u = (int64_t)blockIdx.x * kThreads + threadIdx.x; u < total; u += (int64_t)gridDim.x * kThreads) {
+        int lo = 0, hi = p.nseg;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (p.byte_start[mid] <= u) lo = mid; else hi = mid;
+        }
+        const a8_ob_seg_t sg = p.segs[lo];
+        const int64_t j = u - p.byte_start[lo];
+        float acc[8];
+        for (int r = 0; r < p.nranks; ++r) {
+            const uint8_t* slab = p.slabs + r * p.rank_stride;
+            const uint32_t b = slab[sg.bit_off + j];
+            const float* lv = reinterpret_cast<const float*>(slab + p.levels_off) + 2 * lo;
+            const float pl = lv[0], nl = lv[1];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const float d = (b >> (7 - t)) & 1u ? pl : nl;  // np.packbits order
+                acc[t] = r == 0 ? d : __fadd_rn(acc[t], d);
+            }
+        }
+        if (p.op == 1) {
+#pragma unroll
+            for (int t = 0; t < 8; ++t) acc[t] = pow2 ? __fmul_rn(acc[t], invn) : __fdiv_rn(acc[t], (float)p.nranks);
+        }
+        const int64_t e0 = 8 * j;
+        if (e0 + 8 <= sg.n && (reinterpret_cast<uintptr_t>(sg.out) & 15) == 0) {
+            float4* o = reinterpret_cast<float4*>(sg.out + e0);
+            o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+            o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+        } else {
+            for (int t = 0; t < 8 && e0 + t < sg.n; ++t) sg.out[e0 + t] = acc[t];
+        }
+    }
+}
+
 int grid_for(int64_t n) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -247,4 +311,34 @@ extern "C" int a8_onebit_decode(const uint8_t* bits, int64_t n, const float* lev
     if (n == 0) return A8_OK;
     onebit_decode_k<<<grid_for(n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(bits, n, levels, out);
     return check("a8_onebit_decode");
+}
+
+extern "C" int a8_onebit_reduce(const a8_ob_seg_t* segs, int nseg, const uint8_t* slabs, int64_t rank_stride,
+                                int64_t levels_off, int64_t status_off, int nstatus, int nranks, int op,
+                                uint32_t* status_out, void* stream) {
+    if (nseg < 0 || nseg > kObSegs || (nseg > 0 && !segs) || !slabs || nranks < 1 || nranks > 1024 || op < 0 ||
+        op > 1 || nstatus < 0)
+        return fail(A8_ERR_USAGE, "a8_onebit_reduce: bad argument (at most 32 segments per call)");
+    ObParams p{};
+    int64_t acc = 0;
+    for (int i = 0; i < nseg; ++i) {
+        if (segs[i].n < 0 || (segs[i].n > 0 && !segs[i].out)) return fail(A8_ERR_USAGE, "a8_onebit_reduce: bad segment");
+        p.segs[i] = segs[i];
+        p.byte_start[i] = acc;
+        acc += (segs[i].n + 7) / 8;
+    }
+    p.byte_start[nseg] = acc;
+    p.slabs = slabs;
+    p.rank_stride = rank_stride;
+    p.levels_off = levels_off;
+    p.status_off = status_off;
+    p.nseg = nseg;
+    p.nranks = nranks;
+    p.op = op;
+    p.nstatus = nstatus;
+    p.status_out = status_out;
+    if (acc == 0 && !status_out) return A8_OK;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((acc + kThreads - 1) / kThreads, 148 * 4));
+    onebit_reduce_k<<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(p);
+    return check("a8_onebit_reduce");
 }

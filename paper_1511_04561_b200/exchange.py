@@ -46,6 +46,7 @@ from .errors import InputError, UsageError
 
 MODES = ("allgather", "two_round")
 OPS = ("avg", "sum")
+ONEBIT = "onebit"  # the 1-bit error-feedback spec of the DP seam (mlp.py:52, 313-321)
 
 
 # ---------------------------------------------------------------------------
@@ -75,7 +76,44 @@ class SegmentCodec:
 
 
 class CudaSegmentCodec(SegmentCodec):
-    """a8_encode / a8_decode on the buffers' device and current stream."""
+    """a8_encode / a8_decode (and the 1-bit a8_onebit_quantize /
+    a8_onebit_reduce) on the buffers' device and current stream."""
+
+    def onebit_quantize(self, x: torch.Tensor, residual: torch.Tensor, buf: torch.Tensor, bits_off: int,
+                        levels_off: int, status_off: int) -> None:
+        """onebit_quantize (codecs.py:306-339) of x with the float64 device
+        residual (updated in place), bits / levels / status into buf."""
+        from .codecs import _ob_ws
+
+        dev = buf.device
+        n = x.numel()
+        base = buf.data_ptr()
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        if n == 0:
+            buf[levels_off:levels_off + 12].zero_()
+            return
+        ws = _ob_ws.get(dev.index)
+        if ws is None:
+            ws = _ob_ws[dev.index] = torch.empty(N.lib.a8_onebit_workspace_bytes(), dtype=torch.uint8, device=dev)
+        N.check(N.lib.a8_onebit_quantize(x.data_ptr(), 1 if x.dtype == torch.float64 else 0, residual.data_ptr(), n,
+                                         base + bits_off, base + levels_off, base + status_off, ws.data_ptr(),
+                                         ws.numel(), stream))
+
+    def onebit_reduce(self, outs, bit_offs, buf: torch.Tensor, rank_stride: int, levels_off: int, status_off: int,
+                      nranks: int, op: int, status_out: Optional[torch.Tensor] = None) -> None:
+        dev = buf.device
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        for c0 in range(0, max(len(outs), 1), 32):  # <= 32 segments per launch
+            chunk = list(range(c0, min(c0 + 32, len(outs))))
+            segs = (N.ObSeg * max(len(chunk), 1))()
+            for k, i in enumerate(chunk):
+                segs[k] = N.ObSeg(outs[i].data_ptr(), outs[i].numel(), bit_offs[i])
+            last = c0 + 32 >= len(outs)
+            # the status words of every segment are ORed by the last launch
+            N.check(N.lib.a8_onebit_reduce(segs, len(chunk), buf.data_ptr(), rank_stride, levels_off + 8 * c0,
+                                           status_off, len(outs) if last else 0, nranks, op,
+                                           None if (status_out is None or not last) else status_out.data_ptr(),
+                                           stream))
 
     def encode(self, xs, flat_offs, scale_idx, cb, buf, codes_off, scales_off, block_len,
                block_stride, scale_block_stride, reps, status_off, status_in=None):
@@ -242,6 +280,11 @@ class GradientExchange:
                (each slightly more accurate) averages.
     Every rank must call it with the same tensor shapes in the same order.
     """
+
+    def __new__(cls, spec=None, *args, **kwargs):
+        if cls is GradientExchange and isinstance(spec, str) and spec == ONEBIT:
+            return super().__new__(OneBitExchange)  # __init__ runs as OneBitExchange.__init__
+        return super().__new__(cls)
 
     def __init__(self, spec: DataTypeSpec, group=None, mode: str = "allgather", op: str = "avg",
                  check: str = "deferred", codec: Optional[SegmentCodec] = None, comm=None,
@@ -597,6 +640,120 @@ class GradientExchange:
         self._collect_status(status)
 
 
+class OneBitExchange(GradientExchange):
+    """1-bit error-feedback gradient exchange: ``GradientExchange("onebit")``.
+
+    The reference's 1-bit data-parallel seam (mlp.py:313-321) quantizes every
+    gradient with ``onebit_quantize`` and a residual carried per tensor
+    across steps (codecs.py:291-348), then trains on ``onebit_decode``.
+    Across N ranks: every rank quantizes each tensor with its own residual
+    (a float64 tensor kept on the device, one per tensor position), the
+    packed bits and the two float32 levels of every tensor travel in one slab
+    [bits (each tensor padded to 16 B) | levels | status words], the slabs
+    are all-gathered with NCCL, and one launch decodes, sums in rank order in
+    float32 and divides by N (a8_onebit_reduce).  32x less payload than
+    float32 on the wire.  Oracle: oracle.exchange_onebit.
+
+    Residuals are keyed by (position, numel); ``reset()`` drops them.
+    Non-finite input raises ``InputError`` (on every rank) and leaves every
+    residual untouched.  allgather only; ``graph`` is not supported.
+    """
+
+    def __init__(self, spec=ONEBIT, group=None, mode: str = "allgather", op: str = "avg", check: str = "deferred",
+                 codec: Optional[SegmentCodec] = None, comm=None, **unused):
+        if spec != ONEBIT:
+            raise UsageError(f"OneBitExchange needs spec={ONEBIT!r}")
+        if mode != "allgather":
+            raise UsageError("the 1-bit exchange is an all-gather (mode='allgather')")
+        if op not in OPS:
+            raise UsageError(f"op must be one of {OPS}, got {op!r}")
+        if check not in ("deferred", "sync", "none"):
+            raise UsageError("check must be 'deferred', 'sync' or 'none'")
+        if unused.get("graph") or unused.get("local_fp32"):
+            raise UsageError("graph / local_fp32 are not supported by the 1-bit exchange")
+        self.spec = ONEBIT
+        self.cb = None
+        self.group = group
+        self.mode = mode
+        self.op = op
+        self.check = check
+        self.codec = codec or CudaSegmentCodec()
+        self.comm = comm or TorchDistComm(group)
+        self._plans: dict = {}
+        self._bufs: dict = {}
+        self._pending = collections.deque()
+        self._ring = None
+        self._slot = 0
+        self.calls = 0
+        self.graph = False
+        self._graphs: dict = {}
+        self._gstream = None
+        self._capturing = None
+        self._seen: dict = {}
+        self.local_fp32 = False
+        self.residuals: dict = {}  # (position, numel) -> float64 residual tensor
+
+    def reset(self) -> None:
+        self.residuals.clear()
+
+    @staticmethod
+    def layout(sizes):
+        """(bit offsets, levels offset, status offset, slab bytes) of one rank's slab."""
+        offs, pos = [], 0
+        for n in sizes:
+            offs.append(pos)
+            pos += round16(-(-int(n) // 8))
+        lev = pos
+        st = lev + 8 * len(sizes)
+        return offs, lev, st, round16(st + 4 * len(sizes))
+
+    def __call__(self, tensors: Sequence[torch.Tensor], out: Optional[Sequence[torch.Tensor]] = None):
+        tensors = list(tensors)
+        if not tensors:
+            return []
+        self._poll()
+        dev = tensors[0].device
+        for t in tensors:
+            if t.dtype not in (torch.float32, torch.float64) or not t.is_contiguous() or t.device != dev:
+                raise UsageError("the 1-bit exchange needs contiguous float32/float64 tensors on one device")
+        outs = list(out) if out is not None else tensors
+        for t, o in zip(tensors, outs):
+            if o.dtype != torch.float32 or not o.is_contiguous() or o.device != dev or o.numel() != t.numel():
+                raise UsageError("each out tensor must be contiguous float32 on the inputs' device, "
+                                 "with as many elements as its input")
+        if len(outs) != len(tensors):
+            raise UsageError(f"out holds {len(outs)} tensors, the call has {len(tensors)}")
+        if any(t.dtype != torch.float32 for t in outs) and out is None:
+            raise UsageError("in-place 1-bit exchange needs float32 tensors (pass out= for float64 input)")
+        nranks, rank = self._world()
+        sizes = tuple(t.numel() for t in tensors)
+        offs, lev, st, P = self.layout(sizes)
+        buf = self._buffer("onebit", nranks * P, dev)
+        mine = rank * P
+        res = []
+        for i, t in enumerate(tensors):
+            key = (i, t.numel())
+            r = self.residuals.get(key)
+            if r is None:
+                r = self.residuals[key] = torch.zeros(t.numel(), dtype=torch.float64, device=dev)
+            res.append(r)
+        # each rank's residual follows its own onebit_quantize exactly: updated
+        # iff its own input is finite (the kernel leaves it untouched otherwise,
+        # codecs.py:317-318); a non-finite input on any rank raises InputError
+        # on every rank (the status words travel in the slabs)
+        for i, t in enumerate(tensors):
+            self.codec.onebit_quantize(t.reshape(-1), res[i], buf, mine + offs[i], mine + lev + 8 * i,
+                                       mine + st + 4 * i)
+        if nranks > 1:
+            self.comm.all_gather(buf, buf[mine:mine + P])
+        status = self._status_word(dev)
+        self.codec.onebit_reduce([o.reshape(-1) for o in outs], offs, buf, P, lev, st, nranks,
+                                 1 if self.op == "avg" else 0, status)
+        self._collect_status(status)
+        self.calls += 1
+        return outs
+
+
 def exchange(tensors, spec: DataTypeSpec, group=None, mode: str = "allgather", op: str = "avg"):
     """One-shot functional form of ``GradientExchange`` (check="sync")."""
     return GradientExchange(spec, group, mode, op, check="sync")(tensors)
@@ -704,8 +861,9 @@ class DDPHookState:
     the buckets of a ``DistributedDataParallel`` model.  ``codec`` / ``comm``
     as for ``GradientExchange`` (tests inject CPU stand-ins)."""
 
-    def __init__(self, spec: DataTypeSpec, group=None, mode: str = "allgather", codec: Optional[SegmentCodec] = None,
+    def __init__(self, spec, group=None, mode: str = "allgather", codec: Optional[SegmentCodec] = None,
                  comm=None, check: str = "deferred"):
+        # spec: a DataTypeSpec (8-bit) or "onebit" (1-bit error feedback, one residual per parameter view)
         self.exchange = GradientExchange(spec, group, mode, "avg", check=check, codec=codec, comm=comm)
 
 

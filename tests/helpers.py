@@ -170,6 +170,47 @@ class NumpyCodec:
                 w[0] = st
 
 
+class NumpyOneBitCodec:
+    """The 1-bit half of exchange.SegmentCodec (onebit_quantize /
+    onebit_reduce) with the oracle on CPU tensors, same slab byte layout."""
+
+    def onebit_quantize(self, x, residual, buf, bits_off, levels_off, status_off):
+        mem = buf.numpy()
+        xn = x.detach().cpu().numpy().ravel()
+        res = residual.numpy()
+        try:
+            bits, pos, neg, new = O.onebit_quantize(xn, res)
+            residual.copy_(torch.from_numpy(new))
+            st = 0
+        except O.NonFinite:
+            bits, pos, neg, st = np.zeros((xn.size + 7) // 8, np.uint8), 0.0, 0.0, 1
+        mem[bits_off:bits_off + bits.size] = bits
+        mem[levels_off:levels_off + 8] = np.frombuffer(np.array([pos, neg], np.float32).tobytes(), np.uint8)
+        mem[status_off:status_off + 4] = np.frombuffer(np.uint32(st).tobytes(), np.uint8)
+
+    def onebit_reduce(self, outs, bit_offs, buf, rank_stride, levels_off, status_off, nranks, op, status_out=None):
+        mem = buf.numpy()
+        for i, (o, bo) in enumerate(zip(outs, bit_offs)):
+            n = o.numel()
+            acc = None
+            for r in range(nranks):
+                base = r * rank_stride
+                lv = np.frombuffer(mem[base + levels_off + 8 * i:base + levels_off + 8 * i + 8].tobytes(), np.float32)
+                d = O.onebit_decode(mem[base + bo:base + bo + (n + 7) // 8], n, float(lv[0]), float(lv[1]))
+                acc = d.astype(np.float32) if acc is None else (acc + d).astype(np.float32)
+            if op == 1 and acc is not None:
+                acc = (acc / np.float32(nranks)).astype(np.float32)
+            if n:
+                o.view(-1).copy_(torch.from_numpy(acc))
+        if status_out is not None:
+            st = 0
+            for r in range(nranks):
+                for i in range(len(outs)):
+                    at = r * rank_stride + status_off + 4 * i
+                    st |= int(np.frombuffer(mem[at:at + 4].tobytes(), np.uint32)[0])
+            status_out.view(torch.int32)[0] = st
+
+
 # ---------------------------------------------------------------------------
 # virtual ranks: one thread per rank, collectives through shared memory
 

@@ -99,3 +99,59 @@ def test_blocked_beyond_2_to_31_elements(cuda):
     assert bool((y[:P * reps].view(reps, P) == db.view(1, P)).all())
     del y, q, c, s
     torch.cuda.empty_cache()
+
+
+# constants of a8_blocked.cu's streaming encode (guess-and-verify)
+G_KEY0, G_LEN, G_MARGIN = 0x3400, 0x3F80 - 0x3400 + 1, 2.0 ** -18
+
+
+def _guess_table(kind):
+    v = O.book(kind).values
+    mid = 0.5 * (v[:-1] + v[1:])
+    yk = (((np.arange(G_LEN) + G_KEY0).astype(np.uint32)) << 16).view(np.float32).astype(np.float64)
+    return np.searchsorted(mid * (1.0 + G_MARGIN), yk, side="left").astype(np.uint8), mid
+
+
+@pytest.mark.parametrize("kind", ["dynamic-tree", "linear"])
+def test_guess_buckets_hold_at_most_one_midpoint(kind):
+    """The streaming per-block encode guesses c from the normalised value's
+    bucket and verifies ONE threshold; that needs every bucket, widened by
+    the normalisation's rounding (2^-22) and the margin, to hold at most one
+    midpoint of the codebook."""
+    G, mid = _guess_table(kind)
+    lo = (((np.arange(G_LEN) + G_KEY0).astype(np.uint32)) << 16).view(np.float32).astype(np.float64)
+    hi = (((np.arange(G_LEN) + G_KEY0 + 1).astype(np.uint32)) << 16).view(np.float32).astype(np.float64)
+    w = 2.0 ** -22
+    a = np.searchsorted(mid, lo * (1 - w) / (1 + G_MARGIN), side="left")
+    b = np.searchsorted(mid, hi * (1 + w) * (1 + G_MARGIN), side="right")
+    assert (b - a).max() <= 1
+    assert mid[0] > 2.0 ** -23  # nothing below the table's first key
+
+
+@pytest.mark.parametrize("kind", ["dynamic-tree", "linear"])
+def test_guess_verify_restated_matches_reference(kind):
+    """The kernel's per-element arithmetic restated in NumPy (float32
+    normalisation, guess table, exact threshold verify) on blocks with
+    random scales and elements at every threshold and its neighbours."""
+    G, _ = _guess_table(kind)
+    rng = np.random.default_rng(11)
+    for trial in range(40):
+        s = np.float32(np.exp(rng.uniform(np.log(2.0 ** -90), np.log(2.0 ** 90))))
+        T = O.thresholds(kind, float(s))
+        fin = T[T < 0x7F800000]
+        near = np.concatenate([fin - 1, fin, fin + 1]).astype(np.uint32)
+        mags = np.concatenate([near, rng.integers(0, int(np.float32(s).view(np.uint32)) + 1, 3000)]).astype(np.uint32)
+        mags = mags[mags <= np.float32(s).view(np.uint32)]
+        x = mags.view(np.float32).copy()
+        x[::3] *= -1
+        x = np.concatenate([x, [s]]).astype(np.float32)
+        ref, rs = O.encode(x, kind, "absmax")
+        assert np.float32(rs) == s
+        r = np.float32(1.0) / s
+        y = (np.abs(x) * r).astype(np.float32)
+        key = (y.view(np.uint32) >> 16).astype(np.int64)
+        c = G[np.maximum(key - G_KEY0, 0)].astype(np.int64)
+        Tp = np.append(T, 0x7F800000)
+        p = c + ((x.view(np.uint32) & 0x7FFFFFFF) >= Tp[c])
+        code = (p | np.where((x < 0) & (p != 0), 0x80, 0)).astype(np.uint8)
+        assert np.array_equal(code, ref), trial

@@ -18,7 +18,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from helpers import NumpyCodec, O, run_virtual_ranks
+from helpers import NumpyCodec, NumpyOneBitCodec, O, run_virtual_ranks
 
 import paper_1511_04561_b200 as A
 
@@ -274,3 +274,101 @@ def test_local_fp32_orchestration(nranks, chunk):
 def test_local_fp32_needs_allgather():
     with pytest.raises(A.UsageError):
         A.GradientExchange(A.DataTypeSpec("linear", "absmax"), mode="two_round", local_fp32=True)
+
+
+# ---------------------------------------------------------------------------
+# the 1-bit error-feedback exchange (GradientExchange("onebit"))
+
+ONEBIT_SIZES = [(40, 30), (1,), (17,), (0,), (300,), (4, 4, 4), (5000,)]
+
+
+def _onebit_grads(rank, step):
+    rng = np.random.default_rng(500 + 31 * rank + step)
+    return [rng.normal(0, 1e-2, size=s).astype(np.float32) for s in ONEBIT_SIZES]
+
+
+@pytest.mark.parametrize("nranks", [1, 2, 4])
+def test_onebit_exchange_chained_steps_match_oracle(nranks):
+    """5 chained steps: per-rank residuals carried on each rank, bits +
+    levels all-gathered, rank-ordered float32 average -- bit-exact against
+    oracle.exchange_onebit (codecs.py:306-348 per rank)."""
+    steps = 5
+
+    def body(rank, comm):
+        ex = A.GradientExchange("onebit", check="sync", codec=NumpyOneBitCodec(), comm=comm)
+        outs = []
+        for k in range(steps):
+            ts = [torch.from_numpy(g) for g in _onebit_grads(rank, k)]
+            ex(ts)
+            outs.append([t.numpy().copy() for t in ts])
+        return outs
+
+    res = run_virtual_ranks(nranks, body)
+    resid = [[np.zeros(int(np.prod(s))) .reshape(s) for s in ONEBIT_SIZES] for _ in range(nranks)]
+    for k in range(steps):
+        want = O.exchange_onebit([_onebit_grads(r, k) for r in range(nranks)], resid)
+        for r in range(nranks):
+            for a, b in zip(res[r][k], want):
+                assert a.tobytes() == b.astype(np.float32).tobytes(), (r, k)
+
+
+def test_onebit_exchange_nonfinite_raises_everywhere_and_keeps_residuals():
+    def body(rank, comm):
+        ex = A.GradientExchange("onebit", check="sync", codec=NumpyOneBitCodec(), comm=comm)
+        ex([torch.from_numpy(g) for g in _onebit_grads(rank, 0)])
+        before = {k: v.clone() for k, v in ex.residuals.items()}
+        ts = [torch.from_numpy(g) for g in _onebit_grads(rank, 1)]
+        if rank == 1:
+            ts[6][3] = float("inf")
+        try:
+            ex(ts)
+            return "ok", None
+        except A.InputError:
+            k6 = (6, ts[6].numel())  # the non-finite tensor's own residual is untouched (codecs.py:317-318)
+            return "raised", torch.equal(before[k6], ex.residuals[k6])
+
+    res = run_virtual_ranks(2, body)
+    assert [r[0] for r in res] == ["raised", "raised"]
+    assert res[1][1] is True
+
+
+def test_onebit_exchange_rejects_unsupported():
+    with pytest.raises(A.UsageError):
+        A.GradientExchange("onebit", mode="two_round")
+    with pytest.raises(A.UsageError):
+        A.GradientExchange("onebit", graph=True)
+
+
+def _ddp_onebit_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        model = torch.nn.parallel.DistributedDataParallel(_ddp_model())
+        model.register_comm_hook(A.DDPHookState("onebit", codec=NumpyOneBitCodec(), check="sync"), A.a8_comm_hook)
+        x, y = _ddp_inputs(rank)
+        torch.nn.functional.mse_loss(model(x), y).backward()
+        per_rank = [_local_grads(r) for r in range(world)]
+        resid = [[np.zeros(g.shape) for g in per_rank[r]] for r in range(world)]
+        ok = True
+        for i, p in enumerate(model.parameters()):
+            want = O.exchange_onebit([[per_rank[r][i]] for r in range(world)], [[resid[r][i]] for r in range(world)])[0]
+            ok &= bool(np.array_equal(p.grad.numpy(), want))
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ddp_comm_hook_onebit_gloo_world_size_2():
+    """DDPHookState("onebit"): a real DDP model's gradients are the 1-bit
+    exchange average (one residual per parameter), bit-exact vs the oracle."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ddp_onebit_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    results = dict(q.get(timeout=5) for _ in range(2))
+    assert results == {0: True, 1: True}

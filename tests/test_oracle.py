@@ -143,3 +143,21 @@ def test_c_restatement_matches_reference_vectors():
     assert sha(codes) == meta["c1"]["dynamic-tree/absmax"]["sha_codes"]
     with pytest.raises(O.NonFinite):
         O.c_encode(np.array([1.0, np.nan], np.float32), "linear")
+
+
+def test_onebit_restatement_matches_reference_chain():
+    """oracle.onebit_quantize / onebit_decode (codecs.py:306-348) against the
+    12 chained steps the real reference produced (residual carried)."""
+    g, _ = golden()
+    res = np.zeros(3000)
+    for k in range(12):
+        bits, pos, neg, res = O.onebit_quantize(g[f"onebit/{k}/g"], res)
+        assert np.array_equal(bits, g[f"onebit/{k}/bits"]), k
+        assert (pos, neg) == tuple(g[f"onebit/{k}/levels"]), k
+        assert res.tobytes() == g[f"onebit/{k}/residual"].tobytes(), k
+        assert O.onebit_decode(bits, 3000, pos, neg).tobytes() == g[f"onebit/{k}/decoded"].tobytes(), k
+    # the exchange oracle at N = 1 is the chained quantize/decode itself
+    r1 = [[np.zeros(3000)]]
+    for k in range(3):
+        out = O.exchange_onebit([[g[f"onebit/{k}/g"]]], r1)[0]
+        assert out.tobytes() == g[f"onebit/{k}/decoded"].tobytes(), k
