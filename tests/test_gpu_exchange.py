@@ -363,3 +363,56 @@ def test_local_fp32_unaligned_pieces(cuda):
         want = O.exchange_allgather_local(g, r, "linear", "absmax")
         for a, b in zip(res[r], want):
             assert a.tobytes() == b.tobytes(), r
+
+
+@pytest.mark.parametrize("nranks", [2, 4, 8])
+def test_onebit_exchange_virtual_ranks_match_oracle(cuda, nranks):
+    """GradientExchange("onebit") with the CUDA kernels: 5 chained steps, one
+    device residual per tensor and rank, bit-exact against
+    oracle.exchange_onebit (per-rank onebit_quantize, codecs.py:306-348;
+    rank-ordered float32 average)."""
+    sizes = SMALL + ALEXNET[:4]
+    steps = 5
+
+    def g(rank, k):
+        rng = np.random.default_rng(900 + 17 * rank + k)
+        return [rng.normal(0, 1e-2, size=s).astype(np.float32) for s in sizes]
+
+    def body(rank, comm):
+        ex = A.GradientExchange("onebit", check="sync", comm=comm)
+        outs = []
+        for k in range(steps):
+            ts = [torch.from_numpy(x).to(cuda) for x in g(rank, k)]
+            ex(ts)
+            outs.append([t.cpu().numpy() for t in ts])
+        return outs
+
+    res = run_virtual_ranks(nranks, body)
+    resid = [[np.zeros(s) for s in sizes] for _ in range(nranks)]
+    for k in range(steps):
+        want = O.exchange_onebit([g(r, k) for r in range(nranks)], resid)
+        for r in range(nranks):
+            for a, b in zip(res[r][k], want):
+                assert a.tobytes() == b.astype(np.float32).tobytes(), (r, k)
+
+
+def test_onebit_exchange_many_tensors_and_float64(cuda):
+    """> 32 tensors (several reduce launches, one status OR) and float64
+    gradients (the reference seam's dtype) at N = 1 == the chained 1-bit
+    round trip of each tensor."""
+    rng = np.random.default_rng(4)
+    sizes = [int(v) for v in rng.integers(1, 3000, size=40)]
+    ex = A.GradientExchange("onebit", check="sync")
+    resid = [[np.zeros(n) for n in sizes]]
+    for k in range(3):
+        xs = [rng.normal(size=n) for n in sizes]
+        ins = [torch.from_numpy(x).to(cuda) for x in xs]
+        outs = [torch.empty(n, device=cuda) for n in sizes]
+        ex(ins, out=outs)
+        want = O.exchange_onebit([xs], resid)
+        for o, w in zip(outs, want):
+            assert o.cpu().numpy().tobytes() == w.astype(np.float32).tobytes(), k
+    bad = [torch.from_numpy(rng.normal(size=n)).to(cuda) for n in sizes]
+    bad[37][0] = float("nan")
+    with pytest.raises(A.InputError):
+        ex(bad, out=[torch.empty(n, device=cuda) for n in sizes])
