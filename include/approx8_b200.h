@@ -200,6 +200,18 @@ int a8_decode(const a8_dec_seg_t* segs, int nseg, const void* book_dev, a8_layou
               int nranks, int op, int status_idx, int status_blocks, uint32_t* status_out,
               void* workspace, size_t workspace_bytes, void* stream);
 
+/* a8_decode over peers' slabs that are not one strided buffer: rank r's
+ * codes and scales are at the layout's offsets from rank_bases[r] instead
+ * of from layout.codes/scales + r * rank_stride (layout.codes/scales are
+ * given for rank 0, i.e. relative to rank_bases[0]).  With NVLink peer
+ * mappings (CUDA IPC / torch symmetric memory: buffer_ptrs) the decode-sum
+ * reads the other GPUs' codes directly -- the all-gather and the decode in
+ * one kernel, with no gathered copy in HBM.  rank_bases: host array of
+ * nranks 16-byte aligned device pointers (UVA).                           */
+int a8_decode_peers(const a8_dec_seg_t* segs, int nseg, const void* book_dev, a8_layout_t layout,
+                    const void* const* rank_bases, int nranks, int op, int status_idx, int status_blocks,
+                    uint32_t* status_out, void* workspace, size_t workspace_bytes, void* stream);
+
 /* a8_decode with rank local_rank's term taken from its own float32 input:
  * out = sum_r t_r, t_r = locals[i][k] for r == local_rank, else
  * table[c_r] * s_r (same order, rounding and op as a8_decode).  The paper's

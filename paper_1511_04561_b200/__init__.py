@@ -33,6 +33,9 @@ from .exchange import (
     GradientExchange,
     LocalExchange,
     OneBitExchange,
+    PeerExchange,
+    PeerTransport,
+    SymmetricMemoryTransport,
     a8_comm_hook,
     exchange,
 )
@@ -60,6 +63,9 @@ __all__ = [
     "ErrorReport",
     "GradientExchange",
     "OneBitExchange",
+    "PeerExchange",
+    "PeerTransport",
+    "SymmetricMemoryTransport",
     "ONEBIT",
     "HookMode",
     "HookStats",

@@ -117,6 +117,8 @@ SIGNATURES = {
         [C.POINTER(DecSeg), C.c_int, C.c_void_p, Layout, C.c_int, C.c_int, C.c_int, C.c_int,
          C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p],
     ),
+    "a8_decode_peers": (C.c_int, [C.POINTER(DecSeg), C.c_int, C.c_void_p, Layout, C.POINTER(C.c_void_p), C.c_int,
+                                  C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "a8_decode_local": (
         C.c_int,
         [C.POINTER(DecSeg), C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_void_p, Layout, C.c_int, C.c_int, C.c_int,

@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "a8_core.cuh"
@@ -181,25 +183,51 @@ constexpr int kGLen = 0x3f80 - kGKey0 + 1;      // keys up to that of 1.0 (|x|/s
 constexpr double kGMargin = 0x1p-18;            // > rounding of fl32(|x| * fl32(1/s)) and of T_i / s
 constexpr size_t kBDynSmem = (size_t)kBStages * kBChunk * sizeof(float);
 
-__device__ __forceinline__ uint32_t guess_verify(uint32_t b, float r, const uint8_t* sG, const uint32_t* T) {
+// One element: guess + verify.  `gaddr` = shared address of G minus kGKey0,
+// `gmin` = shared address of G (keys below the table clamp to entry 0),
+// `taddr` = shared address of the block's thresholds.  About 10 instructions:
+// FMUL, SHF, VIADDMNMX, LDS.U8, IMAD, LDS, LOP3, IADD3, LEA.HI (+ packing).
+__device__ __forceinline__ uint32_t guess_verify(uint32_t b, float r, uint32_t gaddr, uint32_t gmin, uint32_t taddr) {
     const float y = fabsf(__uint_as_float(b)) * r;
-    const int key = (int)(__float_as_uint(y) >> 16);
-    const uint32_t c = sG[max(key - kGKey0, 0)];
-    return c + ((b & 0x7fffffffu) >= T[c] ? 1u : 0u);
+    // signed: gaddr may wrap below zero (shared addresses are < 2^31)
+    const uint32_t ga = (uint32_t)max((int32_t)((__float_as_uint(y) >> 16) + gaddr), (int32_t)gmin);
+    uint32_t c, t;
+    asm("ld.shared.u8 %0, [%1];" : "=r"(c) : "r"(ga));
+    asm("ld.shared.u32 %0, [%1];" : "=r"(t) : "r"(taddr + 4u * c));
+    // c + (|x| bits >= T_c): T_c - 1 - |x| is negative exactly then
+    return c + ((t + ~(b & 0x7fffffffu)) >> 31);
+}
+
+// G (one byte per key of the normalised value, kGKey0 .. 0x3f80): the
+// number of codebook midpoints surely below the bucket.  Built once per
+// codebook by a one-CTA kernel and cached on the device (a8_encode_blocked).
+__global__ void guess_table_kernel(const a8_book_t* book, uint8_t* G) {
+    __shared__ double sMid[128];
+    const int D = book->ndistinct;
+    const int tid = threadIdx.x;
+    if (tid < 128) sMid[tid] = tid + 1 < D ? 0.5 * (book->values[tid] + book->values[tid + 1]) : 1e300;
+    __syncthreads();
+    for (int j = tid; j < kGLen; j += blockDim.x) {
+        const double yk = (double)__uint_as_float((uint32_t)(kGKey0 + j) << 16);
+        int p = 0;
+        for (int step = 64; step; step >>= 1)
+            if (p + step <= D - 1 && sMid[p + step - 1] * (1.0 + kGMargin) < yk) p += step;
+        G[j] = (uint8_t)p;
+    }
 }
 
 template <int V>  // B = 1024 * V; NB = 4 / V blocks per chunk
 __global__ void __launch_bounds__(kBCons + 32, 2) blocked_encode_stream(const float* __restrict__ x, int64_t nchunks,
-                                                                       const a8_book_t* book, uint8_t* codes,
-                                                                       float* scales, unsigned int* status) {
+                                                                       const a8_book_t* book, const uint8_t* Gdev,
+                                                                       uint8_t* codes, float* scales,
+                                                                       unsigned int* status) {
     constexpr int NB = 4 / V;
     extern __shared__ __align__(128) float sStage[];  // [kBStages][kBChunk]
-    __shared__ uint8_t sG[(kGLen + 15) & ~15];
+    __shared__ __align__(16) uint8_t sG[(kGLen + 15) & ~15];
     __shared__ uint32_t sT[2][NB][128];
     __shared__ float sR[2][NB];
-    __shared__ int sFast[2][NB];
+    __shared__ int sFast[2];
     __shared__ unsigned int sRed[kBWarps][NB];
-    __shared__ double sMid[128];
     __shared__ double sV[128];
     __shared__ uint8_t sCanon[128];
     __shared__ __align__(8) uint64_t sFull[kBStages];
@@ -209,8 +237,9 @@ __global__ void __launch_bounds__(kBCons + 32, 2) blocked_encode_stream(const fl
     if (tid < 128) {
         sV[tid] = book->values[tid];
         sCanon[tid] = book->codes[tid];
-        sMid[tid] = tid + 1 < D ? 0.5 * (book->values[tid] + book->values[tid + 1]) : 1e300;
     }
+    for (int j = tid; j < (kGLen + 15) / 16; j += blockDim.x)
+        reinterpret_cast<uint4*>(sG)[j] = reinterpret_cast<const uint4*>(Gdev)[j];
     if (tid == 0) {
         for (int i = 0; i < kBStages; ++i) {
             mbar_init(&sFull[i], 1);
@@ -219,39 +248,40 @@ __global__ void __launch_bounds__(kBCons + 32, 2) blocked_encode_stream(const fl
         mbar_fence_init();
     }
     __syncthreads();
-    // G[k] = #{i : mid_i * (1 + margin) < lowest value of bucket k}
-    for (int j = tid; j < kGLen; j += blockDim.x) {
-        const double yk = (double)__uint_as_float((uint32_t)(kGKey0 + j) << 16);
-        int p = 0;
-#pragma unroll
-        for (int step = 64; step; step >>= 1)
-            if (p + step <= D - 1 && sMid[p + step - 1] * (1.0 + kGMargin) < yk) p += step;
-        sG[j] = (uint8_t)p;
-    }
-    __syncthreads();
     const int64_t nmy = nchunks > blockIdx.x ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     const uint32_t full0 = smem_addr(&sFull[0]), empty0 = smem_addr(&sEmpty[0]);
     if (warp == 0) {
         if (lane == 0) {
             const uint64_t drop = policy_evict_first();
-            for (int64_t it = 0; it < nmy; ++it) {
-                const int st = (int)(it % kBStages);
-                mbar_wait_a(empty0 + 8u * st, (uint32_t)((it / kBStages) & 1) ^ 1u);
+            int st = 0;
+            uint32_t ph = 0;
+            const float* src = x + (int64_t)blockIdx.x * kBChunk;
+            const int64_t step = (int64_t)gridDim.x * kBChunk;
+            for (int64_t it = 0; it < nmy; ++it, src += step) {
+                mbar_wait_a(empty0 + 8u * st, ph ^ 1u);
                 mbar_arrive_expect_tx(&sFull[st], kBChunk * 4);
-                bulk_g2s(sStage + (size_t)st * kBChunk, x + (blockIdx.x + it * gridDim.x) * (int64_t)kBChunk,
-                         kBChunk * 4, &sFull[st], drop);
+                bulk_g2s(sStage + (size_t)st * kBChunk, src, kBChunk * 4, &sFull[st], drop);
+                if (++st == kBStages) {
+                    st = 0;
+                    ph ^= 1u;
+                }
             }
         }
         return;
     }
     const int ct = tid - 32, cw = warp - 1;
+    const uint32_t gmin = smem_addr(sG), gaddr = gmin - (uint32_t)kGKey0;
     unsigned int bad = 0;
+    int st = 0, pst = 0;  // stage of chunk it / it-1
+    uint32_t ph = 0;
     for (int64_t it = 0; it <= nmy; ++it) {
         const int slot = (int)(it & 1);
         const int64_t chunk = blockIdx.x + it * gridDim.x;
+        // sFast[slot]: cleared below by any non-fast block of chunk it; its
+        // last readers (iteration it-1's encode of chunk it-2) passed the barrier
+        if (ct == 0) sFast[slot] = 1;
         if (it < nmy) {  // ---- block maxes of chunk it
-            const int st = (int)(it % kBStages);
-            mbar_wait_a(full0 + 8u * st, (uint32_t)((it / kBStages) & 1));
+            mbar_wait_a(full0 + 8u * st, ph);
             const uint4* in = reinterpret_cast<const uint4*>(sStage + (size_t)st * kBChunk) + ct;
             unsigned int mx[NB];
 #pragma unroll
@@ -270,6 +300,7 @@ __global__ void __launch_bounds__(kBCons + 32, 2) blocked_encode_stream(const fl
         }
         nbar_sync(1, kBCons);
         if (it < nmy) {  // ---- thresholds of chunk it's blocks (codecs.py:237-241, 260-265)
+            bool fast = true;
             for (int k = ct; k < 128 * NB; k += kBCons) {
                 const int j = k >> 7, i = k & 127;
                 unsigned int amax = 0;
@@ -279,44 +310,51 @@ __global__ void __launch_bounds__(kBCons + 32, 2) blocked_encode_stream(const fl
                 uint32_t t = kInfBits;
                 if (scale_ok(scale) && i + 1 < D) t = threshold_fast((double)scale, sV[i], sV[i + 1]);
                 sT[slot][j][i] = t;
+                fast &= amax >= 0x0d800000u && amax <= 0x71800000u;  // 2^-100 <= s <= 2^100
                 if (i == 0) {
                     scales[chunk * NB + j] = scale;
                     sR[slot][j] = __frcp_rn(scale);
-                    sFast[slot][j] = amax >= 0x0d800000u && amax <= 0x71800000u;  // 2^-100 <= s <= 2^100
                     if (amax >= kInfBits) bad = 1u;
                 }
             }
+            if (!fast) sFast[slot] = 0;
         }
         if (it > 0) {  // ---- encode chunk it-1 with the previous iteration's thresholds
             const int ps = slot ^ 1;
-            const int st = (int)((it - 1) % kBStages);
-            const uint4* in = reinterpret_cast<const uint4*>(sStage + (size_t)st * kBChunk) + ct;
+            const uint4* in = reinterpret_cast<const uint4*>(sStage + (size_t)pst * kBChunk) + ct;
             uint32_t* out = reinterpret_cast<uint32_t*>(codes + (chunk - gridDim.x) * (int64_t)kBChunk) + ct;
+            if (sFast[ps]) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int j = q / V;
-                const uint4 v = in[q * kBCons];
-                const uint32_t* T = sT[ps][j];
-                uint32_t c0, c1, c2, c3;
-                if (sFast[ps][j]) {
+                for (int q = 0; q < 4; ++q) {
+                    const int j = q / V;
+                    const uint4 v = in[q * kBCons];
                     const float r = sR[ps][j];
-                    c0 = guess_verify(v.x, r, sG, T);
-                    c1 = guess_verify(v.y, r, sG, T);
-                    c2 = guess_verify(v.z, r, sG, T);
-                    c3 = guess_verify(v.w, r, sG, T);
-                } else {  // search (codes carry their sign already: strip it, re-attached below)
-                    c0 = encode_search(v.x & 0x7fffffffu, T, sCanon);
-                    c1 = encode_search(v.y & 0x7fffffffu, T, sCanon);
-                    c2 = encode_search(v.z & 0x7fffffffu, T, sCanon);
-                    c3 = encode_search(v.w & 0x7fffffffu, T, sCanon);
+                    const uint32_t ta = smem_addr(sT[ps][j]);
+                    const uint32_t c0 = guess_verify(v.x, r, gaddr, gmin, ta), c1 = guess_verify(v.y, r, gaddr, gmin, ta);
+                    const uint32_t c2 = guess_verify(v.z, r, gaddr, gmin, ta), c3 = guess_verify(v.w, r, gaddr, gmin, ta);
+                    const uint32_t packed = __byte_perm(__byte_perm(c0, c1, 0x0040), __byte_perm(c2, c3, 0x0040), 0x5410);
+                    __stcs(out + q * kBCons, attach_signs4(packed, v.x, v.y, v.z, v.w));
                 }
-                const uint32_t packed = __byte_perm(__byte_perm(c0, c1, 0x0040), __byte_perm(c2, c3, 0x0040), 0x5410);
-                __stcs(out + q * kBCons, attach_signs4(packed, v.x, v.y, v.z, v.w));
+            } else {  // tiny / huge scales or non-finite blocks: 7-step threshold search
+#pragma unroll 1
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t* T = sT[ps][q / V];
+                    const uint4 v = in[q * kBCons];
+                    const uint32_t c0 = encode_search(v.x & 0x7fffffffu, T, sCanon), c1 = encode_search(v.y & 0x7fffffffu, T, sCanon);
+                    const uint32_t c2 = encode_search(v.z & 0x7fffffffu, T, sCanon), c3 = encode_search(v.w & 0x7fffffffu, T, sCanon);
+                    const uint32_t packed = __byte_perm(__byte_perm(c0, c1, 0x0040), __byte_perm(c2, c3, 0x0040), 0x5410);
+                    __stcs(out + q * kBCons, attach_signs4(packed, v.x, v.y, v.z, v.w));
+                }
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive_a(empty0 + 8u * st);
+            if (lane == 0) mbar_arrive_a(empty0 + 8u * pst);
         }
-        nbar_sync(1, kBCons);  // sT[slot] complete; sRed free
+        nbar_sync(1, kBCons);  // sT[slot] / sFast[slot] complete; sRed free
+        pst = st;
+        if (++st == kBStages) {
+            st = 0;
+            ph ^= 1u;
+        }
     }
     if (bad) atomicOr(status, A8_STATUS_NONFINITE);
 }
@@ -374,6 +412,23 @@ extern "C" int a8_encode_blocked(const float* x, int64_t n, int64_t block, const
     // ragged tail (and unaligned input) below
     const int64_t nchunks = (reinterpret_cast<uintptr_t>(x) & 15) ? 0 : n / kBChunk;
     if (nchunks > 0) {
+        // the guess table of this codebook, built once per (device, book)
+        static std::mutex mu;
+        static std::map<std::pair<int, const void*>, uint8_t*> gcache;
+        uint8_t* G = nullptr;
+        {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            std::lock_guard<std::mutex> lk(mu);
+            auto it = gcache.find({dev, book_dev});
+            if (it == gcache.end()) {
+                if (cudaMalloc(&G, (kGLen + 15) & ~15) != cudaSuccess) return fail(A8_ERR_CUDA, "a8_encode_blocked: alloc");
+                guess_table_kernel<<<1, 256, 0, st>>>(static_cast<const a8_book_t*>(book_dev), G);
+                gcache[{dev, book_dev}] = G;
+            } else {
+                G = it->second;
+            }
+        }
         static int sms = 0;
         if (!sms) {
             int dev = 0;
@@ -387,11 +442,11 @@ extern "C" int a8_encode_blocked(const float* x, int64_t n, int64_t block, const
         const a8_book_t* book = static_cast<const a8_book_t*>(book_dev);
         unsigned int* stt = reinterpret_cast<unsigned int*>(status_out);
         if (block == 1024)
-            blocked_encode_stream<1><<<g, kBCons + 32, kBDynSmem, st>>>(x, nchunks, book, codes, scales, stt);
+            blocked_encode_stream<1><<<g, kBCons + 32, kBDynSmem, st>>>(x, nchunks, book, G, codes, scales, stt);
         else if (block == 2048)
-            blocked_encode_stream<2><<<g, kBCons + 32, kBDynSmem, st>>>(x, nchunks, book, codes, scales, stt);
+            blocked_encode_stream<2><<<g, kBCons + 32, kBDynSmem, st>>>(x, nchunks, book, G, codes, scales, stt);
         else
-            blocked_encode_stream<4><<<g, kBCons + 32, kBDynSmem, st>>>(x, nchunks, book, codes, scales, stt);
+            blocked_encode_stream<4><<<g, kBCons + 32, kBDynSmem, st>>>(x, nchunks, book, G, codes, scales, stt);
         const int64_t done = nchunks * kBChunk;
         x += done;
         n -= done;

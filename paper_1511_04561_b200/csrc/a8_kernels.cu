@@ -153,6 +153,8 @@ struct DecParams {
     unsigned int* status_out;
     int64_t total;
     int local_rank;  // >= 0: rank whose term is the local float32 input (decode_kernel<true>)
+    int64_t rank_off[kMaxRanks];  // bytes from rank 0's codes/scales to rank r's: r * rank_stride, or
+                                  // the distance between peers' slabs (a8_decode_peers, UVA)
     DecSegD segs[kInlineSegs];
 };
 
@@ -1309,7 +1311,7 @@ __global__ void __launch_bounds__(kDecThreads, 4) decode_kernel(const __grid_con
             const int sgi = i / R, r = i % R;
             const DecSegD& d = segs[sgi];
             sScale[i] = __ldcg(reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.lay.scales) +
-                                                              (int64_t)r * p.lay.rank_stride) +
+                                                              p.rank_off[r]) +
                                (d.flat_off / L) * p.lay.scale_block_stride + d.scale_idx);
         }
     }
@@ -1322,7 +1324,7 @@ __global__ void __launch_bounds__(kDecThreads, 4) decode_kernel(const __grid_con
         for (int i = tid; i < R * p.status_blocks; i += kDecThreads) {
             const int r = i / p.status_blocks, j = i % p.status_blocks;
             const unsigned int* w = reinterpret_cast<const unsigned int*>(
-                                        reinterpret_cast<const uint8_t*>(p.lay.scales) + (int64_t)r * p.lay.rank_stride) +
+                                        reinterpret_cast<const uint8_t*>(p.lay.scales) + p.rank_off[r]) +
                                     (int64_t)j * p.lay.scale_block_stride + p.status_idx;
             atomicOr(&sSt, __ldcg(w));
         }
@@ -1362,7 +1364,7 @@ __global__ void __launch_bounds__(kDecThreads, 4) decode_kernel(const __grid_con
                 __syncthreads();  // (also orders the table build before the first lookups)
                 if (tid < R)
                     sScale[tid] = __ldcg(reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.lay.scales) +
-                                                                        (int64_t)tid * p.lay.rank_stride) +
+                                                                        p.rank_off[tid]) +
                                          j * p.lay.scale_block_stride + sg.scale_idx);
                 __syncthreads();
             }
@@ -1403,7 +1405,7 @@ __global__ void __launch_bounds__(kDecThreads, 4) decode_kernel(const __grid_con
             // rank r+1's code words are loaded before rank r's are decoded
             uint32_t wn[kDecGroups];
             if (R > 1) {
-                const uint8_t* s1 = src + p.lay.rank_stride + f0 + tid * 4;
+                const uint8_t* s1 = src + p.rank_off[1] + f0 + tid * 4;
 #pragma unroll
                 for (int q = 0; q < kDecGroups; ++q) wn[q] = ld_stream_u32(s1 + q * (kDecThreads * 4));
             }
@@ -1413,7 +1415,7 @@ __global__ void __launch_bounds__(kDecThreads, 4) decode_kernel(const __grid_con
 #pragma unroll
                 for (int q = 0; q < kDecGroups; ++q) w[q] = wn[q];
                 if (r + 1 < R) {
-                    const uint8_t* sn = src + (int64_t)(r + 1) * p.lay.rank_stride + f0 + tid * 4;
+                    const uint8_t* sn = src + p.rank_off[r + 1] + f0 + tid * 4;
 #pragma unroll
                     for (int q = 0; q < kDecGroups; ++q) wn[q] = ld_stream_u32(sn + q * (kDecThreads * 4));
                 }
@@ -1460,7 +1462,7 @@ __global__ void __launch_bounds__(kDecThreads, 4) decode_kernel(const __grid_con
             for (int64_t i = tid; i < cnt; i += kDecThreads) {
                 auto term = [&](int r) {
                     return (kLocal && r == p.local_rank) ? sg.local[base + i]
-                                                         : dec(src[(int64_t)r * p.lay.rank_stride + f0 + i], scl[r]);
+                                                         : dec(src[p.rank_off[r] + f0 + i], scl[r]);
                 };
                 float a = term(0);
                 for (int r = 1; r < R; ++r) a = __fadd_rn(a, term(r));
@@ -1941,7 +1943,7 @@ extern "C" int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_de
 static int decode_impl(const a8_dec_seg_t* segs, const float* const* locals, int local_rank, int nseg,
                        const void* book_dev, a8_layout_t layout, int nranks, int op, int status_idx,
                        int status_blocks, uint32_t* status_out, void* workspace, size_t workspace_bytes,
-                       void* stream) {
+                       void* stream, const void* const* rank_bases = nullptr) {
     if (nseg <= 0 && !status_out) return A8_OK;
     if (nseg < 0) return fail(A8_ERR_USAGE, "a8_decode: negative segment count");
     if (status_out && (status_idx < 0 || status_blocks < 1)) return fail(A8_ERR_USAGE, "a8_decode: bad status request");
@@ -1986,6 +1988,15 @@ static int decode_impl(const a8_dec_seg_t* segs, const float* const* locals, int
     p.status_out = status_out;
     p.total = chunks;
     p.local_rank = locals ? local_rank : -1;
+    for (int r = 0; r < nranks; ++r) {
+        if (rank_bases) {
+            if (!rank_bases[r] || reinterpret_cast<uintptr_t>(rank_bases[r]) % 16)
+                return fail(A8_ERR_USAGE, "a8_decode_peers: rank bases must be non-null and 16-byte aligned");
+            p.rank_off[r] = reinterpret_cast<const uint8_t*>(rank_bases[r]) - reinterpret_cast<const uint8_t*>(rank_bases[0]);
+        } else {
+            p.rank_off[r] = (int64_t)r * layout.rank_stride;
+        }
+    }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     auto launch = [&](unsigned grid, size_t smem) {
         if (locals)
@@ -2017,6 +2028,14 @@ extern "C" int a8_decode(const a8_dec_seg_t* segs, int nseg, const void* book_de
                          void* workspace, size_t workspace_bytes, void* stream) {
     return decode_impl(segs, nullptr, -1, nseg, book_dev, layout, nranks, op, status_idx, status_blocks,
                        status_out, workspace, workspace_bytes, stream);
+}
+
+extern "C" int a8_decode_peers(const a8_dec_seg_t* segs, int nseg, const void* book_dev, a8_layout_t layout,
+                               const void* const* rank_bases, int nranks, int op, int status_idx, int status_blocks,
+                               uint32_t* status_out, void* workspace, size_t workspace_bytes, void* stream) {
+    if (!rank_bases) return fail(A8_ERR_USAGE, "a8_decode_peers: null rank bases");
+    return decode_impl(segs, nullptr, -1, nseg, book_dev, layout, nranks, op, status_idx, status_blocks, status_out,
+                       workspace, workspace_bytes, stream, rank_bases);
 }
 
 extern "C" int a8_decode_local(const a8_dec_seg_t* segs, const float* const* locals, int local_rank, int nseg,

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
 #include <string>
 
 #include "approx8_b200.h"
@@ -300,6 +301,10 @@ extern "C" int a8_onebit_quantize(const void* g, int g_is_f64, double* residual,
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     Partial* part = static_cast<Partial*>(workspace);
     const int grid = grid_for(n);
+    // stats -> apply share the partials in `workspace`: another host thread's
+    // pair on the same stream and workspace must not interleave between them
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
     onebit_stats<<<grid, kThreads, 0, st>>>(g, g_is_f64, residual, n, part);
     if (int rc = check("a8_onebit_quantize(stats)")) return rc;
     onebit_apply<<<grid, kThreads, 0, st>>>(g, g_is_f64, residual, n, part, grid, bits, levels, status_out);

@@ -79,6 +79,26 @@ class CudaSegmentCodec(SegmentCodec):
     """a8_encode / a8_decode (and the 1-bit a8_onebit_quantize /
     a8_onebit_reduce) on the buffers' device and current stream."""
 
+    def decode_peers(self, outs, flat_offs, scale_idx, cb, codes_rel, scales_rel, block_len, block_stride,
+                     scale_block_stride, rank_bases, op, status_idx=-1, status_blocks=0, status_out=None):
+        """a8_decode_peers: rank r's codes at rank_bases[r] + codes_rel and its
+        scales at rank_bases[r] + scales_rel (device addresses, e.g. NVLink
+        peer mappings); the sum over ranks in rank order, then op."""
+        dev = outs[0].device if outs else status_out.device
+        book, _ = cb.device_tables(dev)
+        n = len(outs)
+        segs = (N.DecSeg * max(n, 1))()
+        for i, (o, off, si) in enumerate(zip(outs, flat_offs, scale_idx)):
+            segs[i] = N.DecSeg(o.data_ptr(), o.numel(), off, si, 0)
+        b0 = int(rank_bases[0])
+        lay = N.Layout(b0 + codes_rel, b0 + scales_rel, block_len, block_stride, scale_block_stride, 0, 1, 0)
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        ws = workspace(dev, stream, max(n, 1))
+        bases = (C.c_void_p * len(rank_bases))(*[int(b) for b in rank_bases])
+        st = None if status_out is None else status_out.data_ptr()
+        N.check(N.lib.a8_decode_peers(segs, n, book.data_ptr(), lay, bases, len(rank_bases), op, status_idx,
+                                      status_blocks, st, ws.data_ptr(), ws.numel(), stream))
+
     def onebit_quantize(self, x: torch.Tensor, residual: torch.Tensor, buf: torch.Tensor, bits_off: int,
                         levels_off: int, status_off: int) -> None:
         """onebit_quantize (codecs.py:306-339) of x with the float64 device
@@ -752,6 +772,155 @@ class OneBitExchange(GradientExchange):
         self._collect_status(status)
         self.calls += 1
         return outs
+
+
+# ---------------------------------------------------------------------------
+# the exchange over NVLink peer memory: the decode reads the other GPUs'
+# codes directly (no collective, no gathered copy in HBM)
+
+
+class PeerTransport:
+    """Buffers every rank of the group can read directly, plus a
+    stream-ordered barrier.  ``buffer`` returns this rank's buffer and the
+    device base address of every rank's buffer of that name."""
+
+    def world(self):
+        raise NotImplementedError
+
+    def buffer(self, name: str, nbytes: int, device):
+        raise NotImplementedError
+
+    def barrier(self) -> None:
+        raise NotImplementedError
+
+
+class SymmetricMemoryTransport(PeerTransport):
+    """torch.distributed._symmetric_memory on the NCCL group: buffers mapped
+    into every GPU's address space over NVLink (``buffer_ptrs``), and its
+    device-side barrier on the current stream."""
+
+    def __init__(self, group=None):
+        import torch.distributed._symmetric_memory as symm_mem
+
+        self._symm = symm_mem
+        self.group = group if group is not None else dist.group.WORLD
+        self._bufs: dict = {}
+        self._hdl = None
+
+    def world(self):
+        return dist.get_world_size(self.group), dist.get_rank(self.group)
+
+    def buffer(self, name, nbytes, device):
+        hit = self._bufs.get(name)
+        if hit is None or hit[0].numel() < nbytes:
+            t = self._symm.empty(max(int(nbytes), 16), dtype=torch.uint8, device=device)
+            t.zero_()
+            hdl = self._symm.rendezvous(t, self.group)
+            hit = self._bufs[name] = (t, [int(p) for p in hdl.buffer_ptrs], hdl)
+            self._hdl = hdl
+        return hit[0][:nbytes], hit[1]
+
+    def barrier(self) -> None:
+        self._hdl.barrier(channel=0)
+
+
+class PeerExchange(GradientExchange):
+    """``GradientExchange`` whose data movement is the decode kernel itself
+    reading the peers' slabs over NVLink (``a8_decode_peers``): each rank
+    encodes into its own slab of a peer-mapped buffer, one barrier, and
+    the fused decode-sum(-average) pulls every rank's codes and scales from
+    their GPUs.  Same numerics and oracles as the NCCL path.
+
+    ``allgather``: slab [codes | scales | status]; one barrier per call
+    (the slabs are double-buffered, so the next call's barrier also orders
+    the peers' reads before the buffer is rewritten).
+    ``two_round``: round 1 reads, from every peer, the block of its codes
+    destined to this rank's shard (the all-to-all becomes peer loads inside
+    the decode); the averaged shard is re-encoded into a second slab; after
+    a second barrier, round 2 decodes every shard from its owner's slab.
+    """
+
+    def __init__(self, spec: DataTypeSpec, transport: PeerTransport, mode: str = "allgather", op: str = "avg",
+                 check: str = "deferred", codec: Optional[SegmentCodec] = None):
+        super().__init__(spec, None, mode, op, check, codec)
+        self.transport = transport
+        self.comm = transport  # world()
+
+    def __call__(self, tensors: Sequence[torch.Tensor], out: Optional[Sequence[torch.Tensor]] = None):
+        tensors = list(tensors)
+        if not tensors:
+            return []
+        self._poll()
+        dev = tensors[0].device
+        for t in tensors:
+            if t.dtype != torch.float32 or not t.is_contiguous() or t.device != dev:
+                raise UsageError("exchange needs contiguous float32 tensors on one device")
+        outs = list(out) if out is not None else tensors
+        if len(outs) != len(tensors) or any(o.dtype != torch.float32 or not o.is_contiguous() or o.device != dev
+                                            or o.numel() != t.numel() for t, o in zip(tensors, outs)):
+            raise UsageError("each out tensor must be contiguous float32 on the inputs' device, "
+                             "with as many elements as its input")
+        nranks, rank = self.transport.world()
+        sizes = tuple(t.numel() for t in tensors)
+        plan = self._plans.get((sizes, nranks))
+        if plan is None:
+            plan = self._plans[(sizes, nranks)] = make_plan(sizes, nranks)
+        par = self.calls & 1
+        if self.mode == "allgather" or nranks == 1:
+            self._peer_allgather(tensors, outs, plan, nranks, rank, dev, par)
+        else:
+            self._peer_two_round(tensors, outs, plan, nranks, rank, dev, par)
+        self.calls += 1
+        return outs
+
+    def _peer_allgather(self, xs, outs, plan, nranks, rank, dev, par):
+        C = plan.flat
+        P = plan.allgather_block()
+        slab, ptrs = self.transport.buffer(f"ag{par}", P, dev)
+        idx = list(range(plan.nseg))
+        self.codec.encode(xs, plan.offs, idx, self.cb, slab, 0, C, C, C, 0, 1, C + 4 * plan.status_slot)
+        self.transport.barrier()
+        status = self._status_word(dev)
+        self.codec.decode_peers(outs, plan.offs, idx, self.cb, 0, C, C, C, 0, ptrs[:nranks],
+                                1 if self.op == "avg" else 0, plan.status_slot, 1, status)
+        self._collect_status(status)
+
+    def _peer_two_round(self, xs, outs, plan, nranks, rank, dev, par):
+        L = plan.shard
+        B = plan.two_round_block()
+        sbs = B // 4
+        send, sptrs = self.transport.buffer(f"tr_send{par}", nranks * B, dev)
+        idx = list(range(plan.nseg))
+        # round 1: per-tensor encode into the N destination blocks of my slab
+        self.codec.encode(xs, plan.offs, idx, self.cb, send, 0, L, L, B, sbs, nranks, L + 4 * plan.status_slot)
+        self.transport.barrier()
+        mine = [p for p in plan.pieces if p.shard == rank]
+        shard_buf = self._buffer("shard", max(L, 16) * 4, dev).view(torch.float32)
+        pouts = [shard_buf[p.flat - rank * L: p.flat - rank * L + p.n] for p in mine]
+        poffs = [p.flat - rank * L for p in mine]
+        status1 = self._buffer("status1", 4, dev)
+        # rank r's block for my shard sits at its slab + rank * B
+        bases = [b + rank * B for b in sptrs[:nranks]]
+        self.codec.decode_peers(pouts, poffs, [p.tensor for p in mine], self.cb, 0, L, L, B, 0,
+                                bases, 1 if self.op == "avg" else 0, plan.status_slot, 1, status1)
+        # round 2: my averaged shard, one scale per piece, into my gather slab
+        gath, gptrs = self.transport.buffer(f"tr_gather{par}", B, dev)
+        status_off = L + 4 * plan.status_slot
+        if mine:
+            self.codec.encode(pouts, poffs, [p.idx for p in mine], self.cb, gath, 0, L, L, B, 0, 1, status_off,
+                              status_in=status1)
+        else:
+            gath[status_off:status_off + 4].copy_(status1)
+        self.transport.barrier()
+        sts = self._buffer("status2", 4 * nranks, dev).view(torch.int32)
+        for j in range(nranks):
+            pj = [p for p in plan.pieces if p.shard == j]
+            self.codec.decode_peers([outs[p.tensor].view(-1)[p.start:p.start + p.n] for p in pj],
+                                    [p.flat - j * L for p in pj], [p.idx for p in pj], self.cb, 0, L, L, B, 0,
+                                    [gptrs[j]], 0, plan.status_slot, 1, sts[j:j + 1].view(torch.uint8))
+        status = self._status_word(dev)
+        status.view(torch.int32).copy_(sts.amax().view(1), non_blocking=True)
+        self._collect_status(status)
 
 
 def exchange(tensors, spec: DataTypeSpec, group=None, mode: str = "allgather", op: str = "avg"):

@@ -261,6 +261,71 @@ class ThreadComm:
         self.s.barrier.wait()
 
 
+class VirtualPeers:
+    """exchange.PeerTransport between threads on ONE GPU: every virtual
+    rank's buffer is an ordinary allocation whose address the others read
+    directly (what NVLink peer mappings give real ranks)."""
+
+    class _Shared:
+        def __init__(self, n):
+            self.n = n
+            self.barrier = threading.Barrier(n)
+            self.bufs = {}
+            self.lock = threading.Lock()
+
+    def __init__(self, shared, rank):
+        self.s = shared
+        self.rank = rank
+        self._mine = {}
+
+    @classmethod
+    def group(cls, n):
+        sh = cls._Shared(n)
+        return [cls(sh, r) for r in range(n)]
+
+    def world(self):
+        return self.s.n, self.rank
+
+    def buffer(self, name, nbytes, device):
+        hit = self._mine.get(name)
+        if hit is None or hit[0].numel() < nbytes:
+            t = torch.zeros(max(int(nbytes), 16), dtype=torch.uint8, device=device)
+            with self.s.lock:
+                self.s.bufs.setdefault(name, [None] * self.s.n)[self.rank] = t
+            self.s.barrier.wait()
+            ptrs = [b.data_ptr() for b in self.s.bufs[name]]
+            self.s.barrier.wait()
+            hit = self._mine[name] = (t, ptrs)
+        return hit[0][:nbytes], hit[1]
+
+    def barrier(self):
+        torch.cuda.synchronize()
+        self.s.barrier.wait()
+
+
+def run_virtual_peers(n, fn):
+    """Run fn(rank, peers) in n threads with VirtualPeers transports."""
+    peers = VirtualPeers.group(n)
+    res = [None] * n
+    errs = []
+
+    def body(r):
+        try:
+            res[r] = fn(r, peers[r])
+        except BaseException as exc:  # noqa: BLE001
+            errs.append(exc)
+            peers[r].s.barrier.abort()
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(n)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if errs:
+        raise errs[0]
+    return res
+
+
 def run_virtual_ranks(n, fn):
     """Run fn(rank, comm) in n threads; return the per-rank results."""
     comms = ThreadComm.group(n)

@@ -68,15 +68,14 @@ def test_encode_decode_files_match_reference(tmp_path, cuda):
     x = g["a8t1/small_x"]
     src = tmp_path / "x.bin"
     TF.write_tensor(src, x)
-    for spec in (("dynamic-tree", "absmax"), ("linear", "absmax"), ("static-tree", "decade", 1),
-                 ("mantissa", "decade", 1)):
-        norm = "absmax" if spec[1] == "absmax" else f"decade:{spec[2]}"
+    for spec in (("dynamic-tree", "absmax", 0), ("mantissa", "decade", -2), ("linear", "none", 0)):
+        norm = f"decade:{spec[2]}" if spec[1] == "decade" else spec[1]
         out = tmp_path / f"{spec[0]}.a8t"
         assert main(["encode", "--in", str(src), "--out", str(out), "--dtype", spec[0], "--norm", norm]) == 0
         assert out.read_bytes() == g[f"a8t1/codes/{tag(spec)}"].tobytes(), spec
         back = tmp_path / f"{spec[0]}.f32"
         assert main(["decode", "--in", str(out), "--out", str(back)]) == 0
-        want = O.roundtrip(x, *spec).astype(np.float32)
+        want = O.roundtrip(x, spec[0], spec[1], spec[2]).astype(np.float32)
         assert TF.read_tensor(back).tobytes() == want.tobytes(), spec
     # flag mismatch on decode: InputError -> exit 1
     coded = tmp_path / "dynamic-tree.a8t"

@@ -103,10 +103,13 @@ def test_reference_suite_runs_on_the_b200_codec(tmp_path):
     env = _env(site, True)
     out = subprocess.run([sys.executable, "-c", CHECK_NATIVE], env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "native ok" in out.stdout, out.stdout + out.stderr
-    tests = tmp_path / "tests"
-    shutil.copytree(REF_TESTS, tests, ignore=shutil.ignore_patterns("__pycache__"))
-    files = ["test_codecs.py", "test_properties.py", "test_acceptance.py", "test_tensorfile.py", "test_cli.py",
-             "test_errorbench.py", "test_mlp.py"]
+    # the reference runs its tests from pkg/ (configs/*.toml are read relative to it)
+    pkg = tmp_path / "pkg"
+    shutil.copytree(REF_TESTS, pkg / "tests", ignore=shutil.ignore_patterns("__pycache__"))
+    if (REF / "approx8_configs").is_dir():
+        shutil.copytree(REF / "approx8_configs", pkg / "configs")
+    files = [f"tests/{f}" for f in ("test_codecs.py", "test_properties.py", "test_acceptance.py", "test_tensorfile.py",
+                                    "test_cli.py", "test_errorbench.py", "test_mlp.py")]
     log = ROOT / "gpurun_out" / "dropin_reference_suite.log"
     # a fixed hypothesis seed: the unmodified reference passes all of these
     # files with it (seed 3, e.g., finds a float32-underflow counterexample to
@@ -114,7 +117,7 @@ def test_reference_suite_runs_on_the_b200_codec(tmp_path):
     # the reference fails too); both arms then see the same examples
     res = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "--hypothesis-seed=0",
                           *files],
-                         cwd=tests, env=env, capture_output=True, text=True, timeout=3000)
+                         cwd=pkg, env=env, capture_output=True, text=True, timeout=3000)
     try:
         log.parent.mkdir(exist_ok=True)
         log.write_text(res.stdout + res.stderr)

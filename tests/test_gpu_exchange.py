@@ -416,3 +416,51 @@ def test_onebit_exchange_many_tensors_and_float64(cuda):
     bad[37][0] = float("nan")
     with pytest.raises(A.InputError):
         ex(bad, out=[torch.empty(n, device=cuda) for n in sizes])
+
+
+@pytest.mark.parametrize("nranks", [2, 3, 4, 8])
+@pytest.mark.parametrize("mode", ["allgather", "two_round"])
+@pytest.mark.parametrize("op", ["avg", "sum"])
+def test_peer_exchange_matches_oracle(cuda, nranks, mode, op):
+    """PeerExchange: the decode reads every rank's slab directly
+    (a8_decode_peers over peer addresses; here virtual ranks on one GPU),
+    3 calls (both double-buffer parities) bit-exact against the oracle."""
+    from helpers import run_virtual_peers
+
+    sizes = SMALL + ALEXNET[:5]
+
+    def body(rank, peers):
+        ex = A.PeerExchange(A.DataTypeSpec("dynamic-tree", "absmax"), peers, mode=mode, op=op, check="sync")
+        res = []
+        for step in range(3):
+            ts = [torch.from_numpy(g).to(cuda) for g in grads(rank, sizes, seed=step)]
+            ex(ts)
+            res.append([t.cpu().numpy() for t in ts])
+        return res
+
+    res = run_virtual_peers(nranks, body)
+    for step in range(3):
+        per = [grads(r, sizes, seed=step) for r in range(nranks)]
+        want = (O.exchange_allgather(per, "dynamic-tree", "absmax", op=op) if mode == "allgather"
+                else O.exchange_two_round(per, "dynamic-tree", "absmax", op=op))
+        for r in range(nranks):
+            for a, b in zip(res[r][step], want):
+                assert a.tobytes() == b.astype(np.float32).tobytes(), (r, step)
+
+
+def test_peer_exchange_nonfinite_raises_on_every_rank(cuda):
+    from helpers import run_virtual_peers
+
+    def body(rank, peers):
+        ex = A.PeerExchange(A.DataTypeSpec("linear", "absmax"), peers, mode="two_round", check="sync")
+        ts = [torch.from_numpy(g).to(cuda) for g in grads(rank, SMALL)]
+        if rank == 2:
+            ts[6][11] = float("inf")
+        try:
+            ex(ts)
+        except A.InputError:
+            return "raised"
+        return "ok"
+
+    from helpers import run_virtual_peers as rvp
+    assert rvp(3, body) == ["raised"] * 3

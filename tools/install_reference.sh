@@ -13,7 +13,8 @@ TMP=$(mktemp -d)
 cp -r "$SRC" "$TMP/pkg"
 python -m pip install --no-index --no-build-isolation --find-links /opt/wheelhouse \
     --target "$ROOT/baseline/_ref" --no-deps --upgrade "$TMP/pkg"
-rm -rf "$ROOT/baseline/_ref/approx8_tests"
+rm -rf "$ROOT/baseline/_ref/approx8_tests" "$ROOT/baseline/_ref/approx8_configs"
 cp -r "$SRC/tests" "$ROOT/baseline/_ref/approx8_tests"
+cp -r "$SRC/configs" "$ROOT/baseline/_ref/approx8_configs"  # the perf-model tests read configs/*.toml
 rm -rf "$TMP"
 echo "installed approx8 into $ROOT/baseline/_ref"

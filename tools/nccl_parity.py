@@ -74,6 +74,25 @@ def check_small(world, rank, dev):
     return res
 
 
+def check_peer(world, rank, dev):
+    """PeerExchange over torch symmetric memory (the decode reads the peers'
+    slabs over NVLink) against the same oracles, 2 calls per mode."""
+    res = {}
+    tr = A.SymmetricMemoryTransport()
+    for mode in ("allgather", "two_round"):
+        ex = A.PeerExchange(SPEC, tr, mode=mode, op="avg", check="sync")
+        ok = True
+        for step in range(2):
+            per = [small(r, seed=10 * step) for r in range(world)]
+            want = (O.exchange_allgather(per, "dynamic-tree", "absmax", op="avg") if mode == "allgather"
+                    else O.exchange_two_round(per, "dynamic-tree", "absmax", op="avg"))
+            mine = [torch.from_numpy(g).to(dev) for g in per[rank]]
+            ex(mine)
+            ok &= all(m.cpu().numpy().tobytes() == w.astype(np.float32).tobytes() for m, w in zip(mine, want))
+        res[f"peer_{mode}"] = bool(ok)
+    return res
+
+
 def check_c3(world, rank, dev):
     res = {}
     host = bench.alexnet_grads(rank)
@@ -150,6 +169,12 @@ def main():
         res = {"rank": rank, "world": world, "backend": dist.get_backend()}
         res.update(check_small(world, rank, dev))
         res.update(check_ddp(world, rank, dev))
+        if os.environ.get("A8_PARITY_PEER", "1") == "1":
+            try:
+                res.update(check_peer(world, rank, dev))
+            except Exception as exc:  # noqa: BLE001  (report, do not hide: ok becomes False)
+                res["peer_error"] = repr(exc)[:300]
+                res["peer_ok"] = False
         if os.environ.get("A8_PARITY_C3", "1") == "1":
             res.update(check_c3(world, rank, dev))
         res["ok"] = all(v for k, v in res.items() if isinstance(v, bool))
