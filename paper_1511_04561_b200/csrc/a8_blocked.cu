@@ -27,6 +27,23 @@
 
 namespace a8 {
 int fail(int code, const char* msg);
+
+// G for the codebook `book_dev` (device pointer), built once per (device,
+// book) by a one-CTA kernel on `stream` and cached for the process.
+const uint8_t* guess_table_dev(const void* book_dev, cudaStream_t stream) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, uint8_t*> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find({dev, book_dev});
+    if (it != cache.end()) return it->second;
+    uint8_t* G = nullptr;
+    if (cudaMalloc(&G, (kGLen + 15) & ~15) != cudaSuccess) return nullptr;
+    guess_table_kernel<<<1, 256, 0, stream>>>(static_cast<const a8_book_t*>(book_dev), G);
+    cache[{dev, book_dev}] = G;
+    return G;
+}
 }  // namespace a8
 
 using namespace a8;
@@ -178,43 +195,7 @@ constexpr int kBStages = 6;
 constexpr int kBChunk = 4096;
 constexpr int kBWarps = 8;
 constexpr int kBCons = kBWarps * 32;
-constexpr int kGKey0 = 0x3400;                 // key (bits >> 16) of 2^-23: every midpoint lies above
-constexpr int kGLen = 0x3f80 - kGKey0 + 1;      // keys up to that of 1.0 (|x|/s <= 1 up to rounding)
-constexpr double kGMargin = 0x1p-18;            // > rounding of fl32(|x| * fl32(1/s)) and of T_i / s
 constexpr size_t kBDynSmem = (size_t)kBStages * kBChunk * sizeof(float);
-
-// One element: guess + verify.  `gaddr` = shared address of G minus kGKey0,
-// `gmin` = shared address of G (keys below the table clamp to entry 0),
-// `taddr` = shared address of the block's thresholds.  About 10 instructions:
-// FMUL, SHF, VIADDMNMX, LDS.U8, IMAD, LDS, LOP3, IADD3, LEA.HI (+ packing).
-__device__ __forceinline__ uint32_t guess_verify(uint32_t b, float r, uint32_t gaddr, uint32_t gmin, uint32_t taddr) {
-    const float y = fabsf(__uint_as_float(b)) * r;
-    // signed: gaddr may wrap below zero (shared addresses are < 2^31)
-    const uint32_t ga = (uint32_t)max((int32_t)((__float_as_uint(y) >> 16) + gaddr), (int32_t)gmin);
-    uint32_t c, t;
-    asm("ld.shared.u8 %0, [%1];" : "=r"(c) : "r"(ga));
-    asm("ld.shared.u32 %0, [%1];" : "=r"(t) : "r"(taddr + 4u * c));
-    // c + (|x| bits >= T_c): T_c - 1 - |x| is negative exactly then
-    return c + ((t + ~(b & 0x7fffffffu)) >> 31);
-}
-
-// G (one byte per key of the normalised value, kGKey0 .. 0x3f80): the
-// number of codebook midpoints surely below the bucket.  Built once per
-// codebook by a one-CTA kernel and cached on the device (a8_encode_blocked).
-__global__ void guess_table_kernel(const a8_book_t* book, uint8_t* G) {
-    __shared__ double sMid[128];
-    const int D = book->ndistinct;
-    const int tid = threadIdx.x;
-    if (tid < 128) sMid[tid] = tid + 1 < D ? 0.5 * (book->values[tid] + book->values[tid + 1]) : 1e300;
-    __syncthreads();
-    for (int j = tid; j < kGLen; j += blockDim.x) {
-        const double yk = (double)__uint_as_float((uint32_t)(kGKey0 + j) << 16);
-        int p = 0;
-        for (int step = 64; step; step >>= 1)
-            if (p + step <= D - 1 && sMid[p + step - 1] * (1.0 + kGMargin) < yk) p += step;
-        G[j] = (uint8_t)p;
-    }
-}
 
 template <int V>  // B = 1024 * V; NB = 4 / V blocks per chunk
 __global__ void __launch_bounds__(kBCons + 32, 2) blocked_encode_stream(const float* __restrict__ x, int64_t nchunks,
@@ -412,23 +393,8 @@ extern "C" int a8_encode_blocked(const float* x, int64_t n, int64_t block, const
     // ragged tail (and unaligned input) below
     const int64_t nchunks = (reinterpret_cast<uintptr_t>(x) & 15) ? 0 : n / kBChunk;
     if (nchunks > 0) {
-        // the guess table of this codebook, built once per (device, book)
-        static std::mutex mu;
-        static std::map<std::pair<int, const void*>, uint8_t*> gcache;
-        uint8_t* G = nullptr;
-        {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            std::lock_guard<std::mutex> lk(mu);
-            auto it = gcache.find({dev, book_dev});
-            if (it == gcache.end()) {
-                if (cudaMalloc(&G, (kGLen + 15) & ~15) != cudaSuccess) return fail(A8_ERR_CUDA, "a8_encode_blocked: alloc");
-                guess_table_kernel<<<1, 256, 0, st>>>(static_cast<const a8_book_t*>(book_dev), G);
-                gcache[{dev, book_dev}] = G;
-            } else {
-                G = it->second;
-            }
-        }
+        const uint8_t* G = guess_table_dev(book_dev, st);
+        if (!G) return fail(A8_ERR_CUDA, "a8_encode_blocked: guess table");
         static int sms = 0;
         if (!sms) {
             int dev = 0;

@@ -311,6 +311,54 @@ __device__ __forceinline__ uint32_t encode4_carry(uint4 v, uint32_t ebase, int32
 }
 #endif
 
+// ---------------------------------------------------------------------------
+// Guess-and-verify encode for an absmax scale s (dynamic-tree / linear):
+//   guess  c = G[key(fl32(|x| * fl32(1/s)))]   (G: scale-independent, per codebook)
+//   verify p = c + (bits|x| >= T_c(s))          (T: the scale's exact thresholds)
+// G[k] counts the midpoints surely below bucket k, so c <= p <= c + 1 as
+// long as every bucket (widened by the rounding of the normalised value)
+// holds at most one midpoint -- true for both absmax codebooks
+// (tests/test_blocked.py checks it).  Valid for 2^-100 <= s <= 2^100.
+inline constexpr int kGKey0 = 0x3400;                 // key (bits >> 16) of 2^-23: every midpoint lies above
+inline constexpr int kGLen = 0x3f80 - kGKey0 + 1;      // keys up to that of 1.0 (|x|/s <= 1 up to rounding)
+inline constexpr double kGMargin = 0x1p-18;            // > rounding of fl32(|x| * fl32(1/s)) and of T_i / s
+
+#if defined(__CUDACC__)
+// One element: guess + verify.  `gaddr` = shared address of G minus kGKey0,
+// `gmin` = shared address of G (keys below the table clamp to entry 0),
+// `taddr` = shared address of the block's thresholds.  About 10 instructions:
+// FMUL, SHF, VIADDMNMX, LDS.U8, IMAD, LDS, LOP3, IADD3, LEA.HI (+ packing).
+__device__ __forceinline__ uint32_t guess_verify(uint32_t b, float r, uint32_t gaddr, uint32_t gmin, uint32_t taddr) {
+    const float y = fabsf(__uint_as_float(b)) * r;
+    // signed: gaddr may wrap below zero (shared addresses are < 2^31)
+    const uint32_t ga = (uint32_t)max((int32_t)((__float_as_uint(y) >> 16) + gaddr), (int32_t)gmin);
+    uint32_t c, t;
+    asm("ld.shared.u8 %0, [%1];" : "=r"(c) : "r"(ga));
+    asm("ld.shared.u32 %0, [%1];" : "=r"(t) : "r"(taddr + 4u * c));
+    // c + (|x| bits >= T_c): T_c - 1 - |x| is negative exactly then
+    return c + ((t + ~(b & 0x7fffffffu)) >> 31);
+}
+
+// G (one byte per key of the normalised value, kGKey0 .. 0x3f80): the
+// number of codebook midpoints surely below the bucket.  Built once per
+// codebook by a one-CTA kernel and cached on the device (a8_encode_blocked).
+__global__ void guess_table_kernel(const a8_book_t* book, uint8_t* G) {
+    __shared__ double sMid[128];
+    const int D = book->ndistinct;
+    const int tid = threadIdx.x;
+    if (tid < 128) sMid[tid] = tid + 1 < D ? 0.5 * (book->values[tid] + book->values[tid + 1]) : 1e300;
+    __syncthreads();
+    for (int j = tid; j < kGLen; j += blockDim.x) {
+        const double yk = (double)__uint_as_float((uint32_t)(kGKey0 + j) << 16);
+        int p = 0;
+        for (int step = 64; step; step >>= 1)
+            if (p + step <= D - 1 && sMid[p + step - 1] * (1.0 + kGMargin) < yk) p += step;
+        G[j] = (uint8_t)p;
+    }
+}
+
+#endif
+
 // One element by binary search over the padded thresholds (paper's method).
 A8_HD uint32_t encode_search(uint32_t b, const uint32_t* T128, const uint8_t* canon128) {
     const uint32_t a = b & 0x7fffffffu;
