@@ -342,7 +342,7 @@ __device__ __forceinline__ uint32_t guess_verify(uint32_t b, float r, uint32_t g
 // G (one byte per key of the normalised value, kGKey0 .. 0x3f80): the
 // number of codebook midpoints surely below the bucket.  Built once per
 // codebook by a one-CTA kernel and cached on the device (a8_encode_blocked).
-__global__ void guess_table_kernel(const a8_book_t* book, uint8_t* G) {
+static __global__ void guess_table_kernel(const a8_book_t* book, uint8_t* G) {
     __shared__ double sMid[128];
     const int D = book->ndistinct;
     const int tid = threadIdx.x;
