@@ -290,9 +290,11 @@ A8_HD uint32_t encode_carry(uint32_t b, const uint32_t* e, int32_t kbase, int32_
 __device__ __forceinline__ uint32_t carry_sum(uint32_t b, uint32_t ebase, int32_t emin) {
     const uint32_t m = b & 0x7fff0000u;
     const int32_t a = max((int32_t)(__umulhi(m, 1u << 18) + ebase), emin);
-    uint32_t e;
+    uint32_t e, r;
     asm("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(a));
-    return e + b - m;
+    // e + b - m in one IADD3 (the compiler otherwise forms b & 0x8000ffff first)
+    asm("{\n\t.reg .u32 t;\n\tsub.u32 t, %1, %2;\n\tadd.u32 %0, t, %3;\n\t}" : "=r"(r) : "r"(b), "r"(m), "r"(e));
+    return r;
 }
 
 // Four table sums -> four final code bytes, little-endian: code | sign for
