@@ -1473,6 +1473,198 @@ __global__ void __launch_bounds__(kDecThreads, 4) decode_kernel(const __grid_con
     }
 }
 
+// ---------------------------------------------------------------------------
+// K4/K5 streaming form for 1-2 ranks (the N = 1 round trip, N = 2
+// all-gather): codes come in by bulk copies (TMA) into a 3-stage ring, each
+// chunk is decoded (+ rank sum, + 1/N) into one of 3 shared-memory output
+// buffers, and the decoded chunk leaves by ONE bulk store (full lines, no
+// per-thread global stores) -- the decode writes 4 of every 5 bytes it moves.
+// Warp 0 is the producer; 8 consumer warps decode.  One consumer barrier per
+// chunk: the bulk store of chunk k is issued after it, and the wait for the
+// store of chunk k-1 to finish reading its buffer happens before the next
+// barrier, so with 3 buffers no chunk overwrites a buffer still being read.
+constexpr int kDtWarps = 8;
+constexpr int kDtCons = kDtWarps * 32;
+constexpr int kDtStages = 3;
+constexpr int kDtOut = 3;
+constexpr int kDtMaxRanks = 2;
+constexpr int kDtChunk = 4096;  // elements (16 KB out)
+static size_t dt_smem(int R) {
+    return 256u * 32u * sizeof(float) + (size_t)kDtStages * R * kDtChunk + (size_t)kDtOut * kDtChunk * sizeof(float);
+}
+
+struct DtMeta {
+    int32_t seg;
+    int32_t pad;
+    int64_t base;  // first element of the chunk inside its segment
+    int32_t cnt;
+    int32_t pad2;
+};
+
+__global__ void __launch_bounds__(kDtCons + 32, 2) decode_tma_kernel(const __grid_constant__ DecParams p) {
+    extern __shared__ __align__(128) float sDyn[];
+    float* const sTab = sDyn;                                                              // [256][32]
+    uint8_t* const sCodes = reinterpret_cast<uint8_t*>(sDyn + 256 * 32);                  // [stage][rank][4096]
+    float* const sOut = reinterpret_cast<float*>(sCodes + (size_t)kDtStages * p.nranks * kDtChunk);  // [3][4096]
+    __shared__ float sScale[kInlineSegs * kDtMaxRanks];
+    __shared__ __align__(8) uint64_t sFull[kDtStages];
+    __shared__ __align__(8) uint64_t sEmpty[kDtStages];
+    __shared__ DtMeta sMeta[kDtStages];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const DecSegD* segs = p.segs;  // inline plans only
+    const int R = p.nranks;
+    const int64_t L = p.lay.block_len;
+    const int64_t gap = p.lay.block_stride - p.lay.block_len;
+    if (tid == 0) {
+        for (int i = 0; i < kDtStages; ++i) {
+            mbar_init(&sFull[i], 1);
+            mbar_init(&sEmpty[i], kDtWarps);
+        }
+        mbar_fence_init();
+    }
+    if (tid >= 32) {
+        const int t = tid - 32;
+        const float v = p.book->table[t];
+        float4* d = reinterpret_cast<float4*>(sTab + t * 32);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) d[q] = make_float4(v, v, v, v);
+    }
+    for (int i = tid; i < R * p.nseg; i += blockDim.x) {
+        const int sgi = i / R, r = i % R;
+        const DecSegD& d = segs[sgi];
+        sScale[i] = __ldcg(reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.lay.scales) + p.rank_off[r]) +
+                           (d.flat_off / L) * p.lay.scale_block_stride + d.scale_idx);
+    }
+    if (p.status_out && blockIdx.x == 0) {
+        __shared__ unsigned int sSt;
+        if (tid == 0) sSt = 0u;
+        __syncthreads();
+        for (int i = tid; i < R * p.status_blocks; i += blockDim.x) {
+            const int r = i / p.status_blocks, j = i % p.status_blocks;
+            const unsigned int* w = reinterpret_cast<const unsigned int*>(
+                                        reinterpret_cast<const uint8_t*>(p.lay.scales) + p.rank_off[r]) +
+                                    (int64_t)j * p.lay.scale_block_stride + p.status_idx;
+            atomicOr(&sSt, __ldcg(w));
+        }
+        __syncthreads();
+        if (tid == 0) {
+            if (p.lay.flags & A8_LAYOUT_STATUS_COUNT) {
+                volatile unsigned int* w = p.status_out;
+                if (sSt) *w = *w + 1u;
+            } else {
+                *p.status_out = sSt;
+            }
+        }
+    }
+    __syncthreads();
+    auto seg_of = [&](int64_t c) {
+        int lo = 0, hi = p.nseg;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (segs[mid].cstart <= c) lo = mid; else hi = mid;
+        }
+        return lo;
+    };
+    const uint32_t full0 = smem_addr(&sFull[0]), empty0 = smem_addr(&sEmpty[0]);
+    const int64_t nmy = p.total > blockIdx.x ? (p.total - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint64_t drop = policy_evict_first();
+            int st = 0;
+            uint32_t ph = 0;
+            for (int64_t k = 0; k < nmy; ++k) {
+                const int64_t c = blockIdx.x + k * gridDim.x;
+                const int lo = seg_of(c);
+                const DecSegD& sg = segs[lo];
+                DtMeta m;
+                m.seg = lo;
+                m.base = (c - sg.cstart) * kDtChunk;
+                m.cnt = (int32_t)min((int64_t)kDtChunk, sg.n - m.base);
+                mbar_wait_a(empty0 + 8u * st, ph ^ 1u);
+                sMeta[st] = m;
+                const uint32_t bytes = ((uint32_t)m.cnt + 15u) & ~15u;  // segments are padded to 16 codes
+                mbar_arrive_expect_tx(&sFull[st], bytes * (uint32_t)R);
+                const int64_t f0 = sg.flat_off + m.base;
+                const uint8_t* src = p.lay.codes + (f0 / L) * p.lay.block_stride + f0 % L;
+                for (int r = 0; r < R; ++r)
+                    bulk_g2s(sCodes + ((size_t)st * R + r) * kDtChunk, src + p.rank_off[r], bytes, &sFull[st], drop);
+                if (++st == kDtStages) {
+                    st = 0;
+                    ph ^= 1u;
+                }
+            }
+        }
+        return;
+    }
+    const int ct = tid - 32;
+    const float* tl = sTab + lane;
+    const float invN = 1.0f / (float)R;
+    const bool pow2 = (R & (R - 1)) == 0;
+    const uint64_t wpol = policy_evict_first();
+    int st = 0, ob = 0;
+    uint32_t ph = 0;
+    for (int64_t k = 0; k < nmy; ++k) {
+        mbar_wait_a(full0 + 8u * st, ph);
+        const DtMeta m = sMeta[st];
+        const DecSegD& sg = segs[m.seg];
+        const float* scl = sScale + m.seg * R;
+        float* out = sOut + (size_t)ob * kDtChunk;
+        float acc[4][4];
+#pragma unroll
+        for (int r = 0; r < kDtMaxRanks; ++r) {
+            if (r >= R) break;
+            const uint8_t* cs = sCodes + ((size_t)st * R + r) * kDtChunk;
+            const float s = scl[r];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t w = *reinterpret_cast<const uint32_t*>(cs + q * 1024 + ct * 4);
+                const float d0 = __fmul_rn(tl[(w & 255u) * 32u], s), d1 = __fmul_rn(tl[((w >> 8) & 255u) * 32u], s);
+                const float d2 = __fmul_rn(tl[((w >> 16) & 255u) * 32u], s), d3 = __fmul_rn(tl[(w >> 24) * 32u], s);
+                if (r == 0) {
+                    acc[q][0] = d0; acc[q][1] = d1; acc[q][2] = d2; acc[q][3] = d3;
+                } else {
+                    acc[q][0] = __fadd_rn(acc[q][0], d0); acc[q][1] = __fadd_rn(acc[q][1], d1);
+                    acc[q][2] = __fadd_rn(acc[q][2], d2); acc[q][3] = __fadd_rn(acc[q][3], d3);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_a(empty0 + 8u * st);  // this warp is done with the codes
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            float a0 = acc[q][0], a1 = acc[q][1], a2 = acc[q][2], a3 = acc[q][3];
+            if (p.op == 1) {
+                if (pow2) {
+                    a0 = __fmul_rn(a0, invN); a1 = __fmul_rn(a1, invN); a2 = __fmul_rn(a2, invN); a3 = __fmul_rn(a3, invN);
+                } else {
+                    a0 = __fdiv_rn(a0, (float)R); a1 = __fdiv_rn(a1, (float)R); a2 = __fdiv_rn(a2, (float)R); a3 = __fdiv_rn(a3, (float)R);
+                }
+            }
+            const int e = q * 1024 + ct * 4;
+            reinterpret_cast<float4*>(out)[e >> 2] = make_float4(a0, a1, a2, a3);
+            // the ragged end of a segment: the elements past the last full 4 go out directly
+            if (e + 4 > (m.cnt & ~3) && e < m.cnt) {
+                const float a[4] = {a0, a1, a2, a3};
+                for (int t = max(e, m.cnt & ~3); t < min(e + 4, m.cnt); ++t) sg.out[m.base + t] = a[t - e];
+            }
+        }
+        fence_proxy_async_smem();
+        nbar_sync(1, kDtCons);
+        if (ct == 0) {
+            const uint32_t bytes = (uint32_t)(m.cnt & ~3) * 4u;
+            if (bytes) bulk_s2g(sg.out + m.base, out, bytes, wpol);
+            bulk_commit();
+            bulk_wait_read<kDtOut - 2>();  // the buffer of the next chunk (used 2 stores ago) is free
+        }
+        if (++st == kDtStages) {
+            st = 0;
+            ph ^= 1u;
+        }
+        if (++ob == kDtOut) ob = 0;
+    }
+    if (ct == 0) bulk_wait_all();
+}
+
 static size_t dec_smem(int) { return 256u * 32u * sizeof(float); }  // lane-private table copies
 
 // ---------------------------------------------------------------------------
@@ -2004,7 +2196,22 @@ static int decode_impl(const a8_dec_seg_t* segs, const float* const* locals, int
         else
             decode_kernel<false><<<grid, kDecThreads, smem, st>>>(p);
     };
-    if (nseg <= kInlineSegs) {
+    static const int dt_env = [] {
+        const char* v = getenv("A8_DEC_TMA");
+        return v ? atoi(v) : 1;
+    }();
+    bool tma = dt_env && !locals && nranks <= kDtMaxRanks && nseg <= kInlineSegs && chunks > 0;
+    for (int i = 0; tma && i < nseg; ++i) tma = d[i].aligned;
+    if (tma) {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(decode_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dt_smem(kDtMaxRanks));
+            attr = true;
+        }
+        std::copy(d.begin(), d.begin() + nseg, p.segs);
+        const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)di.sms * 2, chunks));
+        decode_tma_kernel<<<(unsigned)grid, kDtCons + 32, dt_smem(nranks), st>>>(p);
+    } else if (nseg <= kInlineSegs) {
         std::copy(d.begin(), d.begin() + nseg, p.segs);
         const size_t smem = dec_smem(nranks);
         const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)di.sms * di.dec_occ, chunks));
