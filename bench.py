@@ -290,8 +290,11 @@ def nccl_leg(dist, algo, n, steps, rank, nranks, local_rank):
     env.pop("NCCL_ALGO", None)
     if algo != "default":
         env["NCCL_ALGO"] = algo
-    res = subprocess.run([sys.executable, str(Path(__file__).resolve()), "--nccl-leg", str(n), "--steps", str(steps)],
-                         env=env, capture_output=True, text=True, timeout=600)
+    try:
+        res = subprocess.run([sys.executable, str(Path(__file__).resolve()), "--nccl-leg", str(n), "--steps", str(steps)],
+                             env=env, capture_output=True, text=True, timeout=300)
+    except subprocess.TimeoutExpired:
+        return {"algo_requested": algo, "error": "timed out after 300 s"} if rank == 0 else None
     out = None
     for line in res.stdout.splitlines():
         if line.startswith("{"):
@@ -564,11 +567,14 @@ def run_b200(args, nranks, rank, local_rank):
                          "AlexNet-shaped tensors vs the composed oracle, bit-exact on every rank; C3 outputs "
                          "identical (sha256) on every rank"}
         legs = {}
-        for algo in ("Ring", "default"):
-            legs[algo] = nccl_leg(dist, algo, n, args.steps, rank, nranks, local_rank)
+        if dist.get_backend() == "nccl":
+            for algo in ("Ring", "default"):
+                legs[algo] = nccl_leg(dist, algo, n, args.steps, rank, nranks, local_rank)
+        else:  # A8_BENCH_BACKEND=gloo plumbing runs (ranks sharing one GPU): NCCL cannot run there
+            legs = {"skipped": f"backend {dist.get_backend()}"}
         nccl = {"legs": legs}
         for algo, leg in legs.items():
-            if leg and "value" in leg:
+            if isinstance(leg, dict) and "value" in leg:
                 leg["speedup_8bit"] = value / leg["value"]
 
     # NVLink roofline of the exchange: bytes each rank must

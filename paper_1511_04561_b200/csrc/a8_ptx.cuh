@@ -49,7 +49,22 @@ __device__ __forceinline__ void mbar_arrive_a(uint32_t bar) {
     asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(bar) : "memory");
 }
 
+// A8_MBAR_SUSPEND_NS: suspend-time hint of the waits (ns).  A suspended
+// thread resumes when the phase completes, so the hint only bounds how often
+// a waiting warp re-polls (and takes issue slots) -- not the wake-up latency.
+#ifndef A8_MBAR_SUSPEND_NS
+#define A8_MBAR_SUSPEND_NS 0
+#endif
 __device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t parity) {
+#if A8_MBAR_SUSPEND_NS > 0
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+        "r"(parity), "n"(A8_MBAR_SUSPEND_NS)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAIT_%=:\n\t"
@@ -57,6 +72,7 @@ __device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t parity) {
         "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
         "r"(parity)
         : "memory");
+#endif
 }
 
 // ---- bulk async copy global -> shared (completes on an mbarrier) -------------
