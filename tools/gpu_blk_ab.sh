@@ -1,0 +1,5 @@
+timeout 600 python -m pytest tests/test_blocked.py -m gpu -x -q 2>&1 | tail -1
+for v in base gv; do
+  if [ $v = base ]; then lib=paper_1511_04561_b200/_lib/libapprox8_b200.so; else lib=paper_1511_04561_b200/_lib_var/$v/libapprox8_b200.so; fi
+  echo "== $v"; A8_LIB=$lib timeout 300 python tools/prof_blocked.py 2>&1 | tail -4
+done
