@@ -271,7 +271,7 @@ def outputs_agree(dist, outs, nranks):
     return len(set(digests)) == 1, digests[0][:16]
 
 
-def nccl_leg(dist, algo, n, steps, rank, nranks, local_rank):
+def nccl_leg(dist, algo, n, steps, rank, nranks, local_rank, child_args=None):
     """fp32 NCCL all-reduce of an n-float buffer, in child processes (one per
     rank) with NCCL_ALGO=<algo> (or NCCL's default choice), since NCCL reads
     its tuning environment once per process.  NCCL_DEBUG output is scanned
@@ -291,7 +291,8 @@ def nccl_leg(dist, algo, n, steps, rank, nranks, local_rank):
     if algo != "default":
         env["NCCL_ALGO"] = algo
     try:
-        res = subprocess.run([sys.executable, str(Path(__file__).resolve()), "--nccl-leg", str(n), "--steps", str(steps)],
+        cmd = child_args or ["--nccl-leg", str(n)]
+        res = subprocess.run([sys.executable, str(Path(__file__).resolve()), *cmd, "--steps", str(steps)],
                              env=env, capture_output=True, text=True, timeout=300)
     except subprocess.TimeoutExpired:
         return {"algo_requested": algo, "error": "timed out after 300 s"} if rank == 0 else None
@@ -335,6 +336,62 @@ def nccl_leg_child(n, steps):
         ms = float(t.item())
         print(json.dumps({"value": world * 4.0 * n / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
                           "busbw_GBps": 2 * (world - 1) / world * 4.0 * n / (ms * 1e-3) / 1e9}), flush=True)
+    dist.destroy_process_group()
+
+
+def peer_leg_child(mode, steps):
+    """--peer-leg MODE: the C3 exchange through PeerExchange (the decode reads
+    the peers' slabs over NVLink, torch symmetric memory) in child processes
+    (isolated: a failure or hang cannot take the main measurement with it),
+    with the reduced-size oracle parity check first.  Rank 0 prints JSON."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1511_04561_b200 as A
+    from oracle import approx8_oracle as O
+
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    idx = int(os.environ["LOCAL_RANK"]) % torch.cuda.device_count()
+    dev = torch.device("cuda", idx)
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", device_id=dev)
+    spec = A.parse_spec(SPEC_LABEL)
+    tr = A.SymmetricMemoryTransport()
+    # parity: reduced AlexNet-shaped tensors, 2 calls, against the composed oracle
+    small = [[np.random.default_rng(1000 + 16 * r + t).normal(0.0, SIGMA, n0).astype(np.float32)
+              for t, (n0,) in enumerate(PARITY_SIZES)] for r in range(world)]
+    want = (O.exchange_allgather(small, "dynamic-tree", "absmax", op="avg") if mode == "allgather"
+            else O.exchange_two_round(small, "dynamic-tree", "absmax", op="avg"))
+    pex_small = A.PeerExchange(spec, tr, mode=mode, check="sync")
+    ok = True
+    for _ in range(2):
+        mine = [torch.from_numpy(g).to(dev) for g in small[rank]]
+        pex_small(mine)
+        ok &= all(m.cpu().numpy().tobytes() == w.astype(np.float32).tobytes() for m, w in zip(mine, want))
+    grads = [torch.from_numpy(g).to(dev) for g in alexnet_grads(rank)]
+    n = sum(g.numel() for g in grads)
+    outs = [torch.empty_like(g) for g in grads]
+    pex = A.PeerExchange(spec, tr, mode=mode, check="deferred")
+    for _ in range(3):
+        pex(grads, out=outs)
+    pex.synchronize()
+    torch.cuda.synchronize()
+    dist.barrier(device_ids=[idx])
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record()
+    for _ in range(steps):
+        pex(grads, out=outs)
+    a1.record()
+    torch.cuda.synchronize()
+    pex.synchronize()
+    t = torch.tensor([a0.elapsed_time(a1) / steps, 0.0 if ok else 1.0], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        ms = float(t[0].item())
+        print(json.dumps({"value": world * 4.0 * n / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
+                          "mode": mode, "parity_reduced_sizes": bool(t[1].item() == 0.0),
+                          "how": "PeerExchange: encode into this rank's slab of a torch symmetric-memory buffer, "
+                                 "device barrier, a8_decode_peers reads every rank's codes over NVLink"}), flush=True)
     dist.destroy_process_group()
 
 
@@ -555,6 +612,7 @@ def run_b200(args, nranks, rank, local_rank):
     # NCCL_ALGO=Ring and with NCCL's default choice
     nccl = None
     parity = None
+    peer = None
     if nranks > 1:
         ex.synchronize()
         agree, digest = outputs_agree(dist, outs, nranks)
@@ -573,6 +631,11 @@ def run_b200(args, nranks, rank, local_rank):
         else:  # A8_BENCH_BACKEND=gloo plumbing runs (ranks sharing one GPU): NCCL cannot run there
             legs = {"skipped": f"backend {dist.get_backend()}"}
         nccl = {"legs": legs}
+        if dist.get_backend() == "nccl" and os.environ.get("A8_BENCH_PEER", "1") == "1":
+            peer = nccl_leg(dist, "default", n, args.steps, rank, nranks, local_rank,
+                            child_args=["--peer-leg", args.mode])
+        else:
+            peer = {"skipped": f"backend {dist.get_backend()}"}
         for algo, leg in legs.items():
             if isinstance(leg, dict) and "value" in leg:
                 leg["speedup_8bit"] = value / leg["value"]
@@ -699,6 +762,7 @@ def run_b200(args, nranks, rank, local_rank):
             "nccl_fp32_allreduce": nccl,
             "nvlink_roofline": nvlink,
             "parity": parity,
+            "peer_exchange": peer,
             "codec_sweep": sweep,
         }
         print(json.dumps(line), flush=True)
@@ -714,10 +778,14 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the config-1/4/per-block codec sub-measurements")
     ap.add_argument("--nccl-leg", type=int, default=0, help=argparse.SUPPRESS)  # child of nccl_leg()
+    ap.add_argument("--peer-leg", default="", help=argparse.SUPPRESS)  # child: PeerExchange timing
     ap.add_argument("--eager", action="store_true", help="no CUDA graph for the N=1 step")
     args = ap.parse_args()
     if args.nccl_leg:
         nccl_leg_child(args.nccl_leg, args.steps)
+        return
+    if args.peer_leg:
+        peer_leg_child(args.peer_leg, args.steps)
         return
     if args.warmup < 3:
         args.warmup = 3

@@ -10,4 +10,4 @@ cat gpurun_out/bench.json
 timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.json 2>gpurun_out/bench_ref.err; echo ref=$?
 cat gpurun_out/bench_ref.json
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-sweep > /dev/null 2>&1; echo launches=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"encode_kernel|decode_kernel" -s 6 -c 2 -o gpurun_out/full python bench.py --steps 2 --warmup 3 --no-cpu --no-sweep > gpurun_out/ncu_full.log 2>&1; echo full=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"encode_kernel|decode_kernel|decode_tma_kernel" -s 6 -c 2 -o gpurun_out/full python bench.py --steps 2 --warmup 3 --no-cpu --no-sweep > gpurun_out/ncu_full.log 2>&1; echo full=$?
