@@ -340,93 +340,6 @@ __global__ void __launch_bounds__(kBCons + 32, 2) blocked_encode_stream(const fl
     if (bad) atomicOr(status, A8_STATUS_NONFINITE);
 }
 
-// Per-block decode, streaming form (full 4096-element chunks, aligned
-// output): codes in by bulk copies, decoded chunk out by one bulk store per
-// chunk (as the per-tensor decode_tma_kernel), one scale per 1024-element
-// group (a group never straddles blocks).
-constexpr int kBdStages = 3;
-constexpr int kBdOut = 3;
-constexpr size_t kBdDynSmem = 256u * 32u * sizeof(float) + (size_t)kBdStages * kBChunk + (size_t)kBdOut * kBChunk * 4;
-
-__global__ void __launch_bounds__(kBCons + 32, 2) blocked_decode_stream(const uint8_t* __restrict__ codes, int64_t nchunks,
-                                                                       int64_t block, const float* __restrict__ scales,
-                                                                       const a8_book_t* book, float* out) {
-    extern __shared__ __align__(128) float sDyn[];
-    float* const sTab = sDyn;
-    uint8_t* const sCodes = reinterpret_cast<uint8_t*>(sDyn + 256 * 32);
-    float* const sOut = reinterpret_cast<float*>(sCodes + (size_t)kBdStages * kBChunk);
-    __shared__ __align__(8) uint64_t sFull[kBdStages];
-    __shared__ __align__(8) uint64_t sEmpty[kBdStages];
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    if (tid == 0) {
-        for (int i = 0; i < kBdStages; ++i) {
-            mbar_init(&sFull[i], 1);
-            mbar_init(&sEmpty[i], kBWarps);
-        }
-        mbar_fence_init();
-    }
-    if (tid >= 32) {
-        const float v = book->table[tid - 32];
-        float4* d = reinterpret_cast<float4*>(sTab + (tid - 32) * 32);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) d[q] = make_float4(v, v, v, v);
-    }
-    __syncthreads();
-    const int64_t nmy = nchunks > blockIdx.x ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    const uint32_t full0 = smem_addr(&sFull[0]), empty0 = smem_addr(&sEmpty[0]);
-    if (warp == 0) {
-        if (lane == 0) {
-            const uint64_t drop = policy_evict_first();
-            int st = 0;
-            uint32_t ph = 0;
-            for (int64_t k = 0; k < nmy; ++k) {
-                mbar_wait_a(empty0 + 8u * st, ph ^ 1u);
-                mbar_arrive_expect_tx(&sFull[st], kBChunk);
-                bulk_g2s(sCodes + (size_t)st * kBChunk, codes + (blockIdx.x + k * gridDim.x) * (int64_t)kBChunk, kBChunk,
-                         &sFull[st], drop);
-                if (++st == kBdStages) {
-                    st = 0;
-                    ph ^= 1u;
-                }
-            }
-        }
-        return;
-    }
-    const int ct = tid - 32;
-    const float* tl = sTab + lane;
-    const uint64_t wpol = policy_evict_first();
-    int st = 0, ob = 0;
-    uint32_t ph = 0;
-    for (int64_t k = 0; k < nmy; ++k) {
-        const int64_t chunk = blockIdx.x + k * gridDim.x;
-        mbar_wait_a(full0 + 8u * st, ph);
-        float* o = sOut + (size_t)ob * kBChunk;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const float s = __ldg(scales + (chunk * kBChunk + q * 1024) / block);
-            const uint32_t w = *reinterpret_cast<const uint32_t*>(sCodes + (size_t)st * kBChunk + q * 1024 + ct * 4);
-            reinterpret_cast<float4*>(o)[q * 256 + ct] =
-                make_float4(__fmul_rn(tl[(w & 255u) * 32u], s), __fmul_rn(tl[((w >> 8) & 255u) * 32u], s),
-                            __fmul_rn(tl[((w >> 16) & 255u) * 32u], s), __fmul_rn(tl[(w >> 24) * 32u], s));  // codecs.py:281
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive_a(empty0 + 8u * st);
-        fence_proxy_async_smem();
-        nbar_sync(1, kBCons);
-        if (ct == 0) {
-            bulk_s2g(out + chunk * kBChunk, o, kBChunk * 4, wpol);
-            bulk_commit();
-            bulk_wait_read<kBdOut - 2>();
-        }
-        if (++st == kBdStages) {
-            st = 0;
-            ph ^= 1u;
-        }
-        if (++ob == kBdOut) ob = 0;
-    }
-    if (ct == 0) bulk_wait_all();
-}
-
 template <int V>
 __global__ void __launch_bounds__(kThreads) blocked_decode_kernel(const uint8_t* __restrict__ codes, int64_t n,
                                                                  const float* __restrict__ scales,
@@ -529,24 +442,6 @@ extern "C" int a8_decode_blocked(const uint8_t* codes, int64_t n, int64_t block,
         return fail(A8_ERR_USAGE, "a8_decode_blocked: block must be 1024, 2048 or 4096");
     if (reinterpret_cast<uintptr_t>(codes) & 3) return fail(A8_ERR_USAGE, "a8_decode_blocked: codes must be 4-byte aligned");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const int64_t nchunks = ((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(codes)) & 15) ? 0 : n / kBChunk;
-    if (nchunks > 0) {  // full chunks: the streaming kernel; the tail below
-        static int sms = 0;
-        if (!sms) {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            cudaFuncSetAttribute(blocked_decode_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBdDynSmem);
-        }
-        const int g = (int)std::min<int64_t>(nchunks, (int64_t)sms * 2);
-        blocked_decode_stream<<<g, kBCons + 32, kBdDynSmem, st>>>(codes, nchunks, block, scales,
-                                                                    static_cast<const a8_book_t*>(book_dev), out);
-        const int64_t done = nchunks * kBChunk;
-        codes += done;
-        out += done;
-        scales += done / block;
-        n -= done;
-    }
     const int64_t nblk = (n + block - 1) / block;
     if (nblk > 0) {
         const a8_book_t* book = static_cast<const a8_book_t*>(book_dev);
