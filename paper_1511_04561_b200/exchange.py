@@ -79,6 +79,8 @@ class CudaSegmentCodec(SegmentCodec):
     """a8_encode / a8_decode (and the 1-bit a8_onebit_quantize /
     a8_onebit_reduce) on the buffers' device and current stream."""
 
+    _lib = N.lib  # a recording proxy while GradientExchange prepares a step (see _StepRecorder)
+
     def decode_peers(self, outs, flat_offs, scale_idx, cb, codes_rel, scales_rel, block_len, block_stride,
                      scale_block_stride, rank_bases, op, status_idx=-1, status_blocks=0, status_out=None):
         """a8_decode_peers: rank r's codes at rank_bases[r] + codes_rel and its
@@ -148,7 +150,7 @@ class CudaSegmentCodec(SegmentCodec):
                        scale_block_stride, 0, reps, 0)
         stream = torch.cuda.current_stream(dev).cuda_stream
         ws = workspace(dev, stream, n)
-        N.check(N.lib.a8_encode(segs, n, book.data_ptr(), cb.spec.norm_code,
+        N.check(self._lib.a8_encode(segs, n, book.data_ptr(), cb.spec.norm_code,
                                 None if lut is None else lut.data_ptr(), lay, ws.data_ptr(), ws.numel(),
                                 None if status_in is None else status_in.data_ptr(),
                                 base + status_off, stream))
@@ -169,11 +171,11 @@ class CudaSegmentCodec(SegmentCodec):
         ws = workspace(dev, stream, max(n, 1))
         st = None if status_out is None else status_out.data_ptr()
         if locals_ is None:
-            N.check(N.lib.a8_decode(segs, n, book.data_ptr(), lay, nranks, op, status_idx,
+            N.check(self._lib.a8_decode(segs, n, book.data_ptr(), lay, nranks, op, status_idx,
                                     status_blocks, st, ws.data_ptr(), ws.numel(), stream))
             return
         lp = (C.c_void_p * max(n, 1))(*[t.data_ptr() for t in locals_])
-        N.check(N.lib.a8_decode_local(segs, lp, local_rank, n, book.data_ptr(), lay, nranks, op, status_idx,
+        N.check(self._lib.a8_decode_local(segs, lp, local_rank, n, book.data_ptr(), lay, nranks, op, status_idx,
                                       status_blocks, st, ws.data_ptr(), ws.numel(), stream))
 
 
@@ -274,6 +276,89 @@ def make_plan(sizes: Sequence[int], nranks: int) -> Plan:
 # the exchange
 
 
+class _StepRecorder:
+    """Records one eager exchange step -- the C-ABI launches with their
+    ctypes arguments and the collectives with their tensor views -- so that
+    later calls with the same shapes, addresses, stream and workspace replay
+    it without rebuilding anything in Python (the eager step's host cost
+    otherwise exceeds its GPU time at N > 1).  Arguments equal to the
+    recording call's status word are re-pointed at each replay's word."""
+
+    class _Lib:
+        def __init__(self, rec):
+            self._rec = rec
+
+        def __getattr__(self, name):
+            fn = getattr(N.lib, name)
+
+            def call(*args):
+                self._rec.ops.append(("lib", fn, list(args)))
+                return fn(*args)
+
+            return call
+
+    class _Handle:
+        def __init__(self, rec, k, h):
+            self._rec, self._k, self._h = rec, k, h
+
+        def wait(self):
+            self._rec.ops.append(("wait", self._k))
+            return self._h.wait()
+
+    class _Comm:
+        def __init__(self, rec, comm):
+            self._rec, self._comm = rec, comm
+            if not hasattr(comm, "all_gather_async"):
+                self.all_gather_async = None  # the step then uses blocking all-gathers
+
+        def world(self):
+            return self._comm.world()
+
+        def all_gather(self, out, slot):
+            self._rec.ops.append(("ag", out, slot))
+            return self._comm.all_gather(out, slot)
+
+        def all_gather_async(self, out, slot):
+            k = self._rec.nhandles
+            self._rec.nhandles += 1
+            self._rec.ops.append(("ag_async", out, slot, k))
+            return _StepRecorder._Handle(self._rec, k, self._comm.all_gather_async(out, slot))
+
+        def all_to_all(self, recv, send):
+            self._rec.ops.append(("a2a", recv, send))
+            return self._comm.all_to_all(recv, send)
+
+    def __init__(self):
+        self.ops: list = []
+        self.nhandles = 0
+        self.status_ptr = None
+        self.dyn: list = []  # (op index, arg index) holding the status word
+
+    def finish(self, status_ptr: int) -> None:
+        for i, op in enumerate(self.ops):
+            if op[0] == "lib":
+                for j, a in enumerate(op[2]):
+                    if isinstance(a, int) and a == status_ptr:
+                        self.dyn.append((i, j))
+
+    def replay(self, comm, status_ptr: int) -> None:
+        for i, j in self.dyn:
+            self.ops[i][2][j] = status_ptr
+        handles: list = [None] * self.nhandles
+        for op in self.ops:
+            kind = op[0]
+            if kind == "lib":
+                N.check(op[1](*op[2]))
+            elif kind == "ag_async":
+                handles[op[3]] = comm.all_gather_async(op[1], op[2])
+            elif kind == "wait":
+                handles[op[1]].wait()
+            elif kind == "ag":
+                comm.all_gather(op[1], op[2])
+            else:
+                comm.all_to_all(op[1], op[2])
+
+
 class GradientExchange:
     """Compressed all-reduce of a list of float32 tensors (in place by default).
 
@@ -339,6 +424,7 @@ class GradientExchange:
         self._gstream = None
         self._capturing = None  # pinned host status word while capturing
         self._seen: dict = {}  # graph key -> non-finite count already reported
+        self._prepared: dict = {}  # eager-step key -> _StepRecorder (CUDA codec only)
         self.local_fp32 = bool(local_fp32)
 
     # -- distributed context
@@ -354,6 +440,7 @@ class GradientExchange:
             b = torch.zeros(nbytes, dtype=dtype, device=device)
             self._bufs[key] = b
             self._graphs.clear()  # captured graphs hold the old buffer's address
+            self._prepared.clear()  # and so do recorded steps
         return b[:nbytes]
 
     # -- status handling
@@ -447,10 +534,49 @@ class GradientExchange:
         # graphs need launch-inline plans (<= 32 tensors: no host->device plan upload)
         if self.graph and nranks == 1 and dev.type == "cuda" and plan.nseg <= 32:
             self._replay(tensors, outs, plan, nranks, rank, dev)
+        elif type(self.codec) is CudaSegmentCodec and dev.type == "cuda":
+            self._step_prepared(tensors, outs, plan, nranks, rank, dev)
         else:
             self._step(tensors, outs, plan, nranks, rank, dev)
         self.calls += 1
         return outs
+
+    def _step_prepared(self, tensors, outs, plan, nranks, rank, dev):
+        """Eager step through a recorded launch list (see _StepRecorder):
+        the first call with a key runs normally while recording; later calls
+        replay the list.  Steps whose host work is not all launches and
+        collectives (two_round on a rank that owns no piece) are not
+        recorded."""
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        key = (plan.sizes, nranks, rank, self.mode, self.op, self.local_fp32, stream,
+               workspace_epoch(dev, stream), tuple(t.data_ptr() for t in tensors),
+               tuple(o.data_ptr() for o in outs))
+        rec = self._prepared.get(key)
+        if rec is not None:
+            word = self._status_word(dev)
+            rec.replay(self.comm, word.data_ptr())
+            self._collect_status(word)
+            return
+        recordable = self.mode == "allgather" or nranks == 1 or any(p.shard == rank for p in plan.pieces)
+        if not recordable:
+            self._step(tensors, outs, plan, nranks, rank, dev)
+            return
+        rec = _StepRecorder()
+        codec, comm = self.codec, self.comm
+        self.codec._lib = _StepRecorder._Lib(rec)
+        self.comm = _StepRecorder._Comm(rec, comm)
+        words: list = []
+        collect = self._collect_status
+        self._collect_status = lambda w: (words.append(w), collect(w))
+        try:
+            self._step(tensors, outs, plan, nranks, rank, dev)
+        finally:
+            codec._lib = N.lib
+            self.comm = comm
+            self._collect_status = collect
+        if len(words) == 1 and key[7] == workspace_epoch(dev, stream):
+            rec.finish(words[0].data_ptr())
+            self._prepared[key] = rec
 
     def _step(self, tensors, outs, plan, nranks, rank, dev):
         if self.mode == "allgather" or nranks == 1:
@@ -710,6 +836,7 @@ class OneBitExchange(GradientExchange):
         self._gstream = None
         self._capturing = None
         self._seen: dict = {}
+        self._prepared: dict = {}
         self.local_fp32 = False
         self.residuals: dict = {}  # (position, numel) -> float64 residual tensor
 

@@ -464,3 +464,45 @@ def test_peer_exchange_nonfinite_raises_on_every_rank(cuda):
 
     from helpers import run_virtual_peers as rvp
     assert rvp(3, body) == ["raised"] * 3
+
+
+@pytest.mark.parametrize("nranks", [2, 4])
+@pytest.mark.parametrize("mode", ["allgather", "two_round"])
+def test_recorded_step_replays_match_oracle(cuda, nranks, mode):
+    """The eager step is recorded on its first call and replayed afterwards
+    (_StepRecorder): 4 calls with new data in the same tensors, each
+    bit-exact against the oracle; a non-finite input on one rank in a
+    replayed call raises on every rank (the status word is re-pointed)."""
+    sizes = SMALL + ALEXNET[:5]
+
+    def body(rank, comm):
+        ex = A.GradientExchange(A.DataTypeSpec("dynamic-tree", "absmax"), mode=mode, check="sync", comm=comm,
+                                chunk_elems=1 << 16)
+        ts = [torch.empty(s, device=cuda) for s in sizes]
+        res = []
+        for step in range(4):
+            for t, g in zip(ts, grads(rank, sizes, seed=20 + step)):
+                t.copy_(torch.from_numpy(g))
+            ex(ts)
+            res.append([t.cpu().numpy() for t in ts])
+        assert len(ex._prepared) == 1
+        for t, g in zip(ts, grads(rank, sizes, seed=99)):
+            t.copy_(torch.from_numpy(g))
+        if rank == nranks - 1:
+            ts[6][3] = float("nan")
+        try:
+            ex(ts)
+            res.append("ok")
+        except A.InputError:
+            res.append("raised")
+        return res
+
+    res = run_virtual_ranks(nranks, body)
+    for step in range(4):
+        per = [grads(r, sizes, seed=20 + step) for r in range(nranks)]
+        want = (O.exchange_allgather(per, "dynamic-tree", "absmax") if mode == "allgather"
+                else O.exchange_two_round(per, "dynamic-tree", "absmax"))
+        for r in range(nranks):
+            for a, b in zip(res[r][step], want):
+                assert a.tobytes() == b.astype(np.float32).tobytes(), (r, step)
+    assert [res[r][4] for r in range(nranks)] == ["raised"] * nranks
