@@ -452,6 +452,7 @@ class GradientExchange:
     # call's status is checked; graph mode bakes one word into each graph.
 
     _RING = 64
+    _PREPARED_MAX = 16  # recorded steps kept (oldest dropped first)
 
     def _status_word(self, dev) -> torch.Tensor:
         """Where this call's final decode writes its status (uint8[4] view)."""
@@ -576,6 +577,8 @@ class GradientExchange:
             self._collect_status = collect
         if len(words) == 1 and key[7] == workspace_epoch(dev, stream):
             rec.finish(words[0].data_ptr())
+            if len(self._prepared) >= self._PREPARED_MAX:  # callers passing fresh tensors every step
+                self._prepared.pop(next(iter(self._prepared)))
             self._prepared[key] = rec
 
     def _step(self, tensors, outs, plan, nranks, rank, dev):

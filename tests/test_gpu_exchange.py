@@ -506,3 +506,18 @@ def test_recorded_step_replays_match_oracle(cuda, nranks, mode):
             for a, b in zip(res[r][step], want):
                 assert a.tobytes() == b.astype(np.float32).tobytes(), (r, step)
     assert [res[r][4] for r in range(nranks)] == ["raised"] * nranks
+
+
+def test_recorded_steps_are_bounded(cuda):
+    """Fresh tensors every call (new addresses): at most _PREPARED_MAX
+    recordings are kept, and every call stays correct."""
+    ex = A.GradientExchange(A.DataTypeSpec("dynamic-tree", "absmax"), check="sync")
+    for step in range(A.GradientExchange._PREPARED_MAX + 5):
+        gs = grads(0, SMALL, seed=step)
+        ts = [torch.from_numpy(g).to(cuda) for g in gs]
+        keep = [t.clone() for t in ts]  # hold the previous tensors so addresses differ
+        ex(ts)
+        for t, g in zip(ts, gs):
+            assert t.cpu().numpy().tobytes() == O.roundtrip(g, "dynamic-tree", "absmax").tobytes(), step
+        del keep
+    assert len(ex._prepared) <= A.GradientExchange._PREPARED_MAX
