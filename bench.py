@@ -456,12 +456,52 @@ def codec_sweep(A, torch, dev, clk_sampler_cls):
         del x, y, box
         return r
 
+    def premax_c4(n):
+        """encode_buffer given the producer's max (one pass) vs computing it."""
+        cb = A.build_codebook(A.parse_spec("dynamic-tree/absmax"))
+        x = torch.randn(n, device=dev)
+        m = A.scale_absmax_([x], 1.0)
+        box = {}
+        t2 = time_graph(lambda: box.__setitem__("q", A.encode_buffer(x, cb, sync=False)), 7)
+        t1 = time_graph(lambda: box.__setitem__("q", A.encode_buffer(x, cb, sync=False, amax=m)), 7)
+        box["q"]._finish()
+        tm = time_graph(lambda: A.scale_absmax_([x], 1.0), 7)
+        del x, box
+        return {"n": n, "spec": "dynamic-tree/absmax", "encode_two_pass_ms": t2, "encode_premax_ms": t1,
+                "max_pass_ms": tm, "encode_premax_GBps": 5.0 * n / (t1 * 1e-3) / 1e9,
+                "encode_premax_frac": 5.0 * n / (t1 * 1e-3) / 1e9 / peak}
+
+    def premax_c3():
+        """Config-3 gradients through a producer pass (the data-parallel 1/2
+        pre-scale) and the N=1 exchange: torch's multiply + the two-pass
+        encode, against the fused producer + the one-pass encode."""
+        spec = A.parse_spec("dynamic-tree/absmax")
+        ts = [torch.randn(int(np.prod(s)), device=dev) * 1e-3 for s in ALEXNET]
+        ex1, ex2 = A.GradientExchange(spec, check="none"), A.GradientExchange(spec, check="none")
+        half = 0.5
+
+        def two_pass():
+            torch._foreach_mul_(ts, half)
+            ex1(ts)
+
+        def fused():
+            ex2(ts, amax=A.scale_absmax_(ts, half))
+
+        r = {"tensors": len(ts), "elements": sum(t.numel() for t in ts),
+             "torch_scale_then_exchange_ms": time_graph(two_pass, 15),
+             "fused_scale_absmax_then_premax_exchange_ms": time_graph(fused, 15),
+             "exchange_alone_ms": time_graph(lambda: ex1(ts), 15),
+             "max_pass_then_premax_exchange_ms": time_graph(lambda: ex2(ts, amax=A.scale_absmax_(ts, 1.0)), 15)}
+        del ts
+        return r
+
     out = {}
     with clk_sampler_cls(dev.index) as clk:
         out["c1"] = [case(1 << 20, lab) for lab in ("dynamic-tree/absmax", "linear/absmax", "static-tree/decade+1",
                                                     "mantissa/decade+1")]
         out["c4"] = [case(1 << k, lab) for k in (28, 30) for lab in ("dynamic-tree/absmax", "mantissa/decade+1")]
         out["blocked"] = [case(1 << 30, "dynamic-tree/absmax", b) for b in (4096, 1024)]
+        out["premax"] = {"c4": [premax_c4(1 << k) for k in (28, 30)], "c3": premax_c3()}
     out["clocks"] = clk.summary()
     out["how"] = ("one public-API encode_buffer / decode_buffer call per case, CUDA-graph replayed between events, "
                   "median of 7-15, 256 MB L2 flush before each; GB/s at 5 B/elem each way, round trip 10 B/elem; "

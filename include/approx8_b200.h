@@ -58,6 +58,7 @@ extern "C" {
 
 /* device status bits (a8_encode) */
 #define A8_STATUS_NONFINITE 1u
+#define A8_STATUS_AMAX_MISMATCH 2u /* a8_encode_premax: a supplied max != max|x| */
 
 #define A8_LUT_MAX 4096
 
@@ -168,6 +169,41 @@ int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_dev, int norm
               const void* static_lut_dev, a8_layout_t layout, void* workspace,
               size_t workspace_bytes, const uint32_t* status_in, uint32_t* status_out,
               void* stream);
+
+/* a8_encode for an absmax spec whose per-segment maxima are already known --
+ * computed by the kernel that produced the tensors (a8_produce_absmax, or
+ * any producer that writes float32 bits of max|x|).  The segment's scale is
+ * amax_dev[i] (codecs.py:237-241), so the encode is ONE pass over x (4 B read
+ * + 1 B written per element) instead of max pass + encode pass.  The kernel
+ * still computes max|x| of each segment as it encodes; if it differs from
+ * amax_dev[i] the status gets A8_STATUS_AMAX_MISMATCH (the codes of that
+ * call are then unspecified, but every access stays in bounds).  Two
+ * non-finite maxima (Inf / any NaN) agree: that input is reported with
+ * A8_STATUS_NONFINITE as by a8_encode.  Same
+ * layout / workspace / status conventions as a8_encode.
+ * Replaces the max pass of codecs.py:237-241 when the producer supplies it
+ * (the encode fused with its producer).                  */
+int a8_encode_premax(const a8_enc_seg_t* segs, int nseg, const void* book_dev, const uint32_t* amax_dev,
+                     a8_layout_t layout, void* workspace, size_t workspace_bytes, const uint32_t* status_in,
+                     uint32_t* status_out, void* stream);
+
+/* Producer pass with the absmax fused into it: for each segment,
+ *   A8_PRODUCE_SCALE      y = fl(alpha * x)   (alpha == 1 and y == x: max only)
+ *   A8_PRODUCE_RELU       y = x >= 0 || x is NaN ? x : 0      (mlp.py:205)
+ *   A8_PRODUCE_RELU_MASK  y = fl(relu(x) * mask)               (mlp.py:205-207)
+ * and amax_out[i] = bits(max|y|) (NaN bits when y holds a NaN), ready for
+ * a8_encode_premax.  y may alias x.  1 launch (+ a 4 B/segment memset) per
+ * 32 segments; the pass streams 8 B (12 B with a mask) per element.         */
+#define A8_PRODUCE_SCALE 0
+#define A8_PRODUCE_RELU 1
+#define A8_PRODUCE_RELU_MASK 2
+typedef struct a8_prod_seg {
+    const float* x;
+    float* y;
+    const float* mask; /* A8_PRODUCE_RELU_MASK only */
+    int64_t n;
+} a8_prod_seg_t;
+int a8_produce_absmax(const a8_prod_seg_t* segs, int nseg, int op, float alpha, uint32_t* amax_out, void* stream);
 
 /* roundtrip (codecs.py:285-288) fused: decode(encode(x)) for nseg float32
  * tensors in one launch, written to outs[i] (same length as segs[i]); the

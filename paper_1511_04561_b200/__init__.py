@@ -39,6 +39,7 @@ from .exchange import (
     a8_comm_hook,
     exchange,
 )
+from .produce import relu_absmax, scale_absmax_
 from .tensorfile import read_tensor, write_tensor
 from .hooks import (
     HookMode,
@@ -91,7 +92,9 @@ __all__ = [
     "onebit_quantize",
     "parse_spec",
     "read_tensor",
+    "relu_absmax",
     "roundtrip",
     "run_error_suite",
+    "scale_absmax_",
     "write_tensor",
 ]

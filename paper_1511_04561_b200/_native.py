@@ -17,6 +17,8 @@ _LIB_PATH = Path(os.environ.get("A8_LIB") or Path(__file__).resolve().parent / "
 
 A8_OK, A8_ERR_INPUT, A8_ERR_CONFIG, A8_ERR_USAGE, A8_ERR_CUDA = 0, 1, 2, 3, 4
 A8_STATUS_NONFINITE = 1
+A8_STATUS_AMAX_MISMATCH = 2
+A8_PRODUCE_SCALE, A8_PRODUCE_RELU, A8_PRODUCE_RELU_MASK = 0, 1, 2
 A8_LAYOUT_STATUS_COUNT = 1
 KIND_CODE = {"dynamic-tree": 0, "static-tree": 1, "linear": 2, "mantissa": 3}
 NORM_CODE = {"none": 0, "absmax": 1, "decade": 2}
@@ -77,6 +79,10 @@ class DecSeg(C.Structure):
     ]
 
 
+class ProdSeg(C.Structure):
+    _fields_ = [("x", C.c_void_p), ("y", C.c_void_p), ("mask", C.c_void_p), ("n", C.c_int64)]
+
+
 class ObSeg(C.Structure):
     _fields_ = [("out", C.c_void_p), ("n", C.c_int64), ("bit_off", C.c_int64)]
 
@@ -107,6 +113,12 @@ SIGNATURES = {
         [C.POINTER(EncSeg), C.c_int, C.c_void_p, C.c_int, C.c_void_p, Layout, C.c_void_p,
          C.c_size_t, C.c_void_p, C.c_void_p, C.c_void_p],
     ),
+    "a8_encode_premax": (
+        C.c_int,
+        [C.POINTER(EncSeg), C.c_int, C.c_void_p, C.c_void_p, Layout, C.c_void_p, C.c_size_t, C.c_void_p,
+         C.c_void_p, C.c_void_p],
+    ),
+    "a8_produce_absmax": (C.c_int, [C.POINTER(ProdSeg), C.c_int, C.c_int, C.c_float, C.c_void_p, C.c_void_p]),
     "a8_encode_f64": (
         C.c_int,
         [C.POINTER(EncSeg64), C.c_int, C.c_void_p, C.c_int, C.c_float, Layout, C.c_void_p, C.c_size_t,

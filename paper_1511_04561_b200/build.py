@@ -23,7 +23,7 @@ LIB = LIBDIR / "libapprox8_b200.so"
 INCLUDE = ROOT / "include"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["a8_kernels.cu", "a8_onebit.cu", "a8_errstats.cu", "a8_blocked.cu", "a8_codebook.cpp"]
+SOURCES = ["a8_kernels.cu", "a8_onebit.cu", "a8_errstats.cu", "a8_blocked.cu", "a8_produce.cu", "a8_codebook.cpp"]
 
 
 def nvcc() -> str:

@@ -317,6 +317,8 @@ class QuantizedTensor:
         if self._meta is not None:
             host = self._meta.cpu()
             status = int(host[0])
+            if status & N.A8_STATUS_AMAX_MISMATCH:
+                raise UsageError("the supplied amax is not max|x| of the input")
             if status & N.A8_STATUS_NONFINITE:
                 raise InputError("cannot encode non-finite values (NaN or Inf present)")
             self._scale = float(host[1:].view(torch.float32)[0])
@@ -430,7 +432,7 @@ BLOCK_SIZES = (1024, 2048, 4096)
 
 
 def encode_buffer(x, codebook: Codebook, *, device=None, sync: bool = True,
-                  block_size: Optional[int] = None) -> QuantizedTensor:
+                  block_size: Optional[int] = None, amax=None) -> QuantizedTensor:
     """Quantise ``x`` to the nearest codebook values (codecs.py:244-269).
 
     Ties go to the smaller magnitude; the sign bit is set only on non-zero
@@ -442,8 +444,20 @@ def encode_buffer(x, codebook: Codebook, *, device=None, sync: bool = True,
     as ``encode_buffer`` would encode it alone (its own absmax).  The scales
     are ``q.block_scales``.  Not a reference feature (the north star's
     optional per-block max-abs); single pass on the GPU.
+
+    ``amax`` (absmax specs, CUDA input): a float32 device tensor holding
+    max|x|, written by the kernel that produced x (``relu_absmax``,
+    ``scale_absmax_``): the encode skips its max pass (a8_encode_premax).
+    A value that is not max|x| raises UsageError.
     """
     spec = codebook.spec
+    if amax is not None:
+        if (spec.normalization is not NormKind.ABSMAX or block_size is not None
+                or not isinstance(x, torch.Tensor) or x.dtype != torch.float32 or not x.is_cuda):
+            raise UsageError("amax needs an absmax spec and a float32 CUDA tensor (no block_size)")
+        if (not isinstance(amax, torch.Tensor) or amax.dtype != torch.float32 or amax.numel() != 1
+                or amax.device != x.device):
+            raise UsageError("amax must be a 1-element float32 tensor on the input's device")
     if block_size is not None:
         return _encode_blocked(x, codebook, device, sync, int(block_size))
     if _is_f64(x):  # the reference computes float64 input in float64 (codecs.py:254)
@@ -465,9 +479,13 @@ def encode_buffer(x, codebook: Codebook, *, device=None, sync: bool = True,
         seg = N.EncSeg(t.data_ptr(), n, 0, 0, 0)
         lay = N.Layout(codes.data_ptr(), meta.data_ptr() + 4, round16(n), round16(n), 0, 0, 1, 0)
         ws = workspace(dev, stream, 1)
-        N.check(N.lib.a8_encode(C.byref(seg), 1, book.data_ptr(), spec.norm_code,
-                                None if lut is None else lut.data_ptr(), lay, ws.data_ptr(),
-                                ws.numel(), None, meta.data_ptr(), stream))
+        if amax is not None:
+            N.check(N.lib.a8_encode_premax(C.byref(seg), 1, book.data_ptr(), amax.data_ptr(), lay, ws.data_ptr(),
+                                           ws.numel(), None, meta.data_ptr(), stream))
+        else:
+            N.check(N.lib.a8_encode(C.byref(seg), 1, book.data_ptr(), spec.norm_code,
+                                    None if lut is None else lut.data_ptr(), lay, ws.data_ptr(),
+                                    ws.numel(), None, meta.data_ptr(), stream))
     q = QuantizedTensor(codes, shape, spec, scale_tensor=meta[1:].view(torch.float32), meta=meta)
     q._set_device_result(codes, host)
     q._keepalive = t  # input must outlive the asynchronous kernel

@@ -311,6 +311,37 @@ __device__ __forceinline__ uint32_t encode4_carry(uint4 v, uint32_t ebase, int32
     return pack4_carry(carry_sum(v.x, ebase, emin), carry_sum(v.y, ebase, emin), carry_sum(v.z, ebase, emin),
                        carry_sum(v.w, ebase, emin));
 }
+
+// carry_sum with the upper clamp too (`emax`: address of the table's last
+// entry), for tables whose top key comes from a caller-supplied max that
+// may be wrong (a8_encode_premax): any |x| stays inside the table.
+__device__ __forceinline__ uint32_t carry_sum_clamp(uint32_t b, uint32_t ebase, int32_t emin, int32_t emax) {
+    const uint32_t m = b & 0x7fff0000u;
+    const int32_t a = min(max((int32_t)(__umulhi(m, 1u << 18) + ebase), emin), emax);
+    uint32_t e, r;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(a));
+    asm("{\n\t.reg .u32 t;\n\tsub.u32 t, %1, %2;\n\tadd.u32 %0, t, %3;\n\t}" : "=r"(r) : "r"(b), "r"(m), "r"(e));
+    return r;
+}
+
+__device__ __forceinline__ uint32_t encode4_carry_clamp(uint4 v, uint32_t ebase, int32_t emin, int32_t emax) {
+    return pack4_carry(carry_sum_clamp(v.x, ebase, emin, emax), carry_sum_clamp(v.y, ebase, emin, emax),
+                       carry_sum_clamp(v.z, ebase, emin, emax), carry_sum_clamp(v.w, ebase, emin, emax));
+}
+
+// Running max of |x| over raw float32 bits without masking the sign: the
+// unsigned max over the raw bits is the largest negative magnitude (when
+// any x has its sign bit set), the signed max is the largest positive
+// magnitude (when any x has it clear).  abs_of_maxes folds the two.
+__device__ __forceinline__ void absmax_raw4(uint4 v, uint32_t& u, int32_t& s) {
+    u = __vimax3_u32(u, v.x, v.y);
+    u = __vimax3_u32(u, v.z, v.w);
+    s = __vimax3_s32(s, (int32_t)v.x, (int32_t)v.y);
+    s = __vimax3_s32(s, (int32_t)v.z, (int32_t)v.w);
+}
+__device__ __forceinline__ uint32_t abs_of_maxes(uint32_t u, int32_t s) {
+    return max(u >= 0x80000000u ? u & 0x7fffffffu : 0u, s >= 0 ? (uint32_t)s : 0u);
+}
 #endif
 
 // ---------------------------------------------------------------------------

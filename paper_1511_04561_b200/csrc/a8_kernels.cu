@@ -60,6 +60,8 @@ struct EncSegD {
     int32_t nA;       // absmax chunks (0 for fixed scales)
     int32_t nE;       // encode chunks
     int32_t aligned;  // x is 16-byte aligned (bulk copies allowed)
+    int32_t src;      // index of the segment in the caller's array (a8_encode_premax maxima)
+    int32_t pad;
 };
 
 // Ticket kinds.  A: max-abs of a chunk; E: encode a chunk with the segment's
@@ -137,6 +139,7 @@ struct EncParams {
     int absmax;
     int code_hint;  // L2 policy of the code stores: 0 default, 1 evict_first, 2 evict_last (A8_CODE_HINT)
     int64_t total;
+    const unsigned int* amax_in;  // a8_encode_premax: bits of max|x| per caller segment (else null)
     EncSegD segs[kInlineSegs];
     EncBlk blks[kInlineBlks];
 };
@@ -301,6 +304,13 @@ __device__ void load_lut_smem(const a8_lut_t* src, uint32_t* sE, uint32_t* sT, u
     }
 }
 
+// a8_encode_premax: a supplied max that is not max|x|.  Two non-finite
+// values agree (NaN payloads differ between producers; the encode reports
+// A8_STATUS_NONFINITE for them either way).
+__device__ __forceinline__ bool amax_differs(unsigned int a, unsigned int b) {
+    return a != b && (a < kInfBits || b < kInfBits);
+}
+
 struct StageMeta {
     int64_t base;      // first element of the chunk inside its segment
     int64_t code_off;  // byte offset of the chunk's first code (valid if simple)
@@ -354,6 +364,9 @@ constexpr int kSmemBlks = 6 * kSmemSegs + 8;  // larger plans are read from glob
 // wait, so HBM stays busy.  E-chunks run in reverse order so the data most
 // recently read by the A pass (still in L2) is re-read first.
 
+// kPremax: a8_encode_premax (maxima supplied; a separate instance so the
+// two-pass kernel's code is unchanged by the check)
+template <bool kPremax>
 __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_constant__ EncParams p) {
     extern __shared__ __align__(128) float sStage[];  // [kStages][kChunk], then a8_lut_t[2] (table slots)
     a8_lut_t* const sLut = reinterpret_cast<a8_lut_t*>(sStage + (size_t)kStages * kChunk);
@@ -539,6 +552,21 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
 #ifdef A8_TICKET_TRACE
         int sw_tkt = 0;  // ticket of the stage being processed (switch trace)
 #endif
+        // a8_encode_premax: max |x| of the E chunks this thread encoded since
+        // the segment changed (raw-bit maxima, see absmax_raw4; chk_a from the
+        // slow paths), published to ctl[seg].amax and compared at the end
+        uint32_t chk_u = 0u, chk_a = 0u;
+        int32_t chk_s = INT32_MIN;
+        int chk_seg = -1;
+        auto chk_flush = [&]() {
+            const uint32_t u = __reduce_max_sync(0xffffffffu, chk_u);
+            const int32_t sm = __reduce_max_sync(0xffffffffu, chk_s);
+            const uint32_t a = max(__reduce_max_sync(0xffffffffu, chk_a), abs_of_maxes(u, sm));
+            if (lane == 0 && a) red_max_u32(&p.ctl[chk_seg].amax, a);
+            chk_u = chk_a = 0u;
+            chk_s = INT32_MIN;
+            chk_seg = -1;
+        };
         int aseg = -1;          // segment of the pending A run
         unsigned int amx = 0;   // per-thread max of bits(|x|) * 2
         unsigned int acnt = 0;  // A-chunks in the pending run
@@ -589,7 +617,8 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                     atomicAdd(&p.head->wait_ns, gtime() - w0);  // trace
                     atomicAdd(&p.head->waits, 1u);
                 }
-                sHdr[3] = (int)__ldcg(&c->amax);
+                // the producer's max (a8_encode_premax: no A pass) or the A pass's
+                sHdr[3] = (int)(kPremax ? __ldg(p.amax_in + segs[seg].src) : __ldcg(&c->amax));
                 // ready: 0 none, 1 being built, 2 published
                 const unsigned int r = ld_acquire(&p.ctl[seg].ready);
                 int mode = 1;  // 1 build locally, 2 copy, 3 build + publish
@@ -694,6 +723,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
             sw_tkt = m.tkt | (m.tpre << 28);
 #endif
             if (aseg >= 0 && (m.kind != kA || m.seg != aseg)) flush();
+            if (kPremax && chk_seg >= 0 && (m.kind == kEnd || (m.kind == kE && m.seg != chk_seg))) chk_flush();
             if (m.kind == kEnd) break;
             const EncSegD& sg = segs[m.seg];
             const float* stage = sStage + (size_t)st * kChunk;
@@ -764,6 +794,8 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                     sT[ctid] = t;
                 }
                 if (amax >= kInfBits && ctid == 0) atomicOr(&p.head->status, A8_STATUS_NONFINITE);
+                if (kPremax && ctid == 0 && amax_differs(amax, __ldg(p.amax_in + sg.src)))
+                    atomicOr(&p.head->status, A8_STATUS_AMAX_MISMATCH);
                 if (ctid < p.lay.scale_reps) p.lay.scales[ctid * p.lay.scale_block_stride + sg.scale_idx] = scale;
                 nbar_sync(kBarC, kConsumers);  // thresholds ready; sRed fully read
                 valid = 0;  // encode by branch-free search over sT
@@ -833,7 +865,16 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                 const int32_t kmax = kbase + lenm1;
                 if (p.absmax) {  // carry table (a8_core.cuh), 5 instructions per element
                     const int32_t emin = (int32_t)smem_addr(sEt);
-                    if (p.code_hint) {
+                    if (kPremax) {  // supplied max: clamp the top too, and check the max
+                        const int32_t emax = emin + 4 * lenm1;
+#pragma unroll
+                        for (int q = 0; q < kChunk / (kConsumers * 4); ++q) {
+                            const uint4 v = in[q * kConsumers];
+                            out[q * kConsumers] = encode4_carry_clamp(v, eb, emin, emax);
+                            absmax_raw4(v, chk_u, chk_s);
+                        }
+                        chk_seg = m.seg;
+                    } else if (p.code_hint) {
                         const uint64_t pol = p.code_hint == 1 ? policy_evict_first() : policy_evict_last();
 #pragma unroll
                         for (int q = 0; q < kChunk / (kConsumers * 4); ++q)
@@ -901,6 +942,10 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
             }
             if (!p.absmax && __any_sync(0xffffffffu, big >= kInfBits) && lane == 0)
                 atomicOr(&p.head->status, A8_STATUS_NONFINITE);
+            if (kPremax && m.kind == kE && !(m.simple && valid)) {  // slow path: big is max |x|
+                chk_a = max(chk_a, big);
+                chk_seg = m.seg;
+            }
             __syncwarp();
             if (lane == 0) mbar_arrive_a(empty0 + 8u * st);
 #ifdef A8_TICKET_TRACE
@@ -919,11 +964,16 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
     if (sFinal) {
         __threadfence();
         for (int i = tid; i < p.nseg; i += kEncThreads) {
+            // a8_encode_premax: the E pass's max of each multi-chunk segment
+            // must be the supplied one (F segments checked their own)
+            if (kPremax && segs[i].nE > 0 && amax_differs(__ldcg(&p.ctl[i].amax), __ldg(p.amax_in + segs[i].src)))
+                atomicOr(&p.head->status, A8_STATUS_AMAX_MISMATCH);
             p.ctl[i].amax = 0u;
             p.ctl[i].a_done = 0u;
             p.ctl[i].ready = 0u;
             p.ctl[i].len = 0u;
         }
+        __syncthreads();
         if (tid < p.lay.scale_reps) {
             const unsigned int stt = atomicAdd(&p.head->status, 0u) | (p.status_in ? *p.status_in : 0u);
             p.status_out[(int64_t)tid * p.lay.scale_block_stride] = stt;
@@ -1043,6 +1093,7 @@ struct RParams {
     unsigned int* status_out;
     int nseg;
     int write_codes;  // 0: fused round trip only (no codes in memory)
+    const unsigned int* amax_in;  // a8_encode_premax: checked against the computed maxima
     RSeg segs[kInlineSegs + 1];  // segs[nseg].cta0 = grid
 };
 
@@ -1242,11 +1293,15 @@ __global__ void __launch_bounds__(kRThreads, 1) resident_encode_kernel(const __g
     if (q == 0) {  // the segment's first CTA publishes its scale
         if (tid < p.lay.scale_reps) p.lay.scales[tid * p.lay.scale_block_stride + g.scale_idx] = scale;
         if (tid == 0 && amax >= kInfBits) atomicOr(&p.head->status, A8_STATUS_NONFINITE);
+        if (tid == 0 && p.amax_in && amax_differs(amax, p.amax_in[s])) atomicOr(&p.head->status, A8_STATUS_AMAX_MISMATCH);
     }
     if (blockIdx.x == 0) {  // empty segments own no CTA: scale of an empty buffer (codecs.py:257-258)
-        for (int e = 0; e < p.nseg; ++e)
+        for (int e = 0; e < p.nseg; ++e) {
             if (p.segs[e].n == 0 && tid < p.lay.scale_reps)
                 p.lay.scales[tid * p.lay.scale_block_stride + p.segs[e].scale_idx] = 1.0f;
+            if (p.segs[e].n == 0 && tid == 0 && p.amax_in && p.amax_in[e] != 0u)
+                atomicOr(&p.head->status, A8_STATUS_AMAX_MISMATCH);
+        }
     }
     resident_encode_piece(p, g, dst, lo, hi, a0, a1, valid, kb, len, sE, sT, sCanon, sDec, tid);
     resident_finish(p, tid);
@@ -1688,7 +1743,9 @@ static int dev_info(int device, DevInfo* out) {
     if (d.sms == 0) {
         cudaError_t e = cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, device);
         if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
-        e = cudaFuncSetAttribute(encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEncDynSmem);
+        e = cudaFuncSetAttribute(encode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEncDynSmem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(encode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEncDynSmem);
         if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
         e = cudaFuncSetAttribute(decode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)dec_smem(kMaxRanks));
@@ -1696,7 +1753,7 @@ static int dev_info(int device, DevInfo* out) {
         e = cudaFuncSetAttribute(decode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)dec_smem(kMaxRanks));
         if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.enc_occ, encode_kernel, kEncThreads, kEncDynSmem);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.enc_occ, encode_kernel<false>, kEncThreads, kEncDynSmem);
         if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
         const size_t dsm = dec_smem(1);
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.dec_occ, decode_kernel<false>, kDecThreads, dsm);
@@ -1827,6 +1884,26 @@ static void schedule(const std::vector<EncSegD>& d, bool absmax, int64_t wf, std
     blks->push_back(EncBlk{t, -1, 0});  // sentinel: total tickets
 }
 
+// a8_encode_premax: the maxima are known, so there is no A pass and no
+// dependency to hide.  F tickets (single-chunk segments) first, then one B
+// ticket per multi-chunk segment (its table is built and published at once;
+// CTAs that reach the segment's E-chunks before that build their own copy),
+// then the E passes, largest segment first so the launch ends on small runs.
+static void schedule_premax(const std::vector<EncSegD>& d, std::vector<EncBlk>* blks) {
+    int64_t t = 0;
+    auto emit = [&](int s, int kind, int64_t c0, int64_t cnt) {
+        if (cnt <= 0) return;
+        blks->push_back(EncBlk{t, s, (int32_t)((c0 << 2) | kind)});
+        t += cnt;
+    };
+    const int nseg = (int)d.size();
+    for (int s = 0; s < nseg; ++s)
+        if (d[s].n <= kChunk) emit(s, kF, 0, 1);
+    for (int s = nseg - 1; s >= 0 && d[s].n > kChunk; --s) emit(s, kB, 0, 1);
+    for (int s = nseg - 1; s >= 0 && d[s].n > kChunk; --s) emit(s, kE, d[s].nE - 1, d[s].nE);
+    blks->push_back(EncBlk{t, -1, 0});  // sentinel: total tickets
+}
+
 // Fill distance in tickets: what the CTAs hold reserved (ring + ticket
 // batches) plus enough throughput for the B ticket's wait and build to end
 // before the E pass is reached.  Measured (C3, with B tickets): 2880 -> 115.0
@@ -1943,7 +2020,7 @@ static bool resident_enabled() {
 static int encode_resident(const a8_enc_seg_t* segs, int nseg, const void* book_dev, const void* static_lut_dev,
                            const a8_layout_t& layout, void* workspace, const uint32_t* status_in,
                            uint32_t* status_out, const DevInfo& di, cudaStream_t st, bool* done,
-                           float* const* outs = nullptr) {
+                           float* const* outs = nullptr, const uint32_t* amax_in = nullptr) {
     *done = false;
     if (!resident_enabled() || di.res_occ < 1 || nseg > kInlineSegs) return A8_OK;
     const int64_t per = kRCap - 4;  // elements per CTA (+ up to 3 of alignment offset)
@@ -1974,6 +2051,7 @@ static int encode_resident(const a8_enc_seg_t* segs, int nseg, const void* book_
     p.status_out = status_out;
     p.nseg = nseg;
     p.write_codes = outs ? 0 : 1;
+    p.amax_in = amax_in;
     int64_t grid = 0;
     for (int i = 0; i < nseg; ++i) {
         p.segs[i].x = segs[i].x;
@@ -2030,10 +2108,10 @@ extern "C" int a8_roundtrip(const a8_enc_seg_t* segs, float* const* outs, int ns
     return done ? A8_OK : fail(A8_ERR_USAGE, "a8_roundtrip: call does not fit the fused path (use a8_encode + a8_decode)");
 }
 
-extern "C" int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_dev, int norm,
-                         const void* static_lut_dev, a8_layout_t layout, void* workspace,
-                         size_t workspace_bytes, const uint32_t* status_in, uint32_t* status_out,
-                         void* stream) {
+static int encode_impl(const a8_enc_seg_t* segs, int nseg, const void* book_dev, int norm,
+                       const void* static_lut_dev, a8_layout_t layout, void* workspace,
+                       size_t workspace_bytes, const uint32_t* status_in, uint32_t* status_out,
+                       void* stream, const uint32_t* amax_in) {
     if (nseg <= 0) return fail(A8_ERR_USAGE, "a8_encode: need at least one segment");
     if (!segs || !book_dev || !workspace || !status_out) return fail(A8_ERR_USAGE, "a8_encode: null argument");
     if (norm != A8_NORM_ABSMAX && !static_lut_dev)
@@ -2056,7 +2134,8 @@ extern "C" int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_de
         if (ws_capacity(workspace_bytes) < nseg) return fail(A8_ERR_USAGE, "a8_encode: workspace too small for the segment count");
         bool done = false;
         const int rc = encode_resident(segs, nseg, book_dev, absmax ? nullptr : static_lut_dev, layout, workspace,
-                                       status_in, status_out, di, static_cast<cudaStream_t>(stream), &done);
+                                       status_in, status_out, di, static_cast<cudaStream_t>(stream), &done,
+                                       nullptr, amax_in);
         if (rc || done) return rc;
     }
 
@@ -2078,12 +2157,17 @@ extern "C" int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_de
         // absmax: multi-chunk segments take A- and E-chunks; single-chunk
         // (and empty) segments are one F ticket.  Fixed scale: E-chunks.
         const bool fused = absmax && s.n <= kChunk;
-        d[i].nA = absmax && !fused ? (int32_t)nch : 0;
+        d[i].nA = absmax && !fused && !amax_in ? (int32_t)nch : 0;  // premax: no A pass
         d[i].nE = fused ? 0 : absmax ? (int32_t)nch : (int32_t)std::max<int64_t>(1, nch);
         d[i].aligned = (reinterpret_cast<uintptr_t>(s.x) % 16) == 0;
+        d[i].src = order[i];
+        d[i].pad = 0;
     }
     std::vector<EncBlk> blks;
-    schedule(d, absmax, fill_distance((int64_t)di.sms * di.enc_occ), &blks);
+    if (amax_in)
+        schedule_premax(d, &blks);
+    else
+        schedule(d, absmax, fill_distance((int64_t)di.sms * di.enc_occ), &blks);
     const int nblk = (int)blks.size() - 1;
 
     uint8_t* ws = static_cast<uint8_t*>(workspace);
@@ -2110,13 +2194,17 @@ extern "C" int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_de
         p.code_hint = hint;
     }
     p.total = blks[nblk].tstart;
+    p.amax_in = reinterpret_cast<const unsigned int*>(amax_in);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if ((int)blks.size() > max_blocks(nseg)) return fail(A8_ERR_USAGE, "a8_encode: schedule overflow");
     const int64_t grid = std::min<int64_t>((int64_t)di.sms * di.enc_occ, std::max<int64_t>(1, p.total));
     if (nseg <= kInlineSegs && (int)blks.size() <= kInlineBlks) {
         std::copy(d.begin(), d.end(), p.segs);
         std::copy(blks.begin(), blks.end(), p.blks);
-        encode_kernel<<<(unsigned)grid, kEncThreads, kEncDynSmem, st>>>(p);
+        if (amax_in)
+            encode_kernel<true><<<(unsigned)grid, kEncThreads, kEncDynSmem, st>>>(p);
+        else
+            encode_kernel<false><<<(unsigned)grid, kEncThreads, kEncDynSmem, st>>>(p);
     } else {
         // the plan goes through the workspace: upload + launch must not be
         // interleaved with another thread's upload to the same workspace
@@ -2127,9 +2215,28 @@ extern "C" int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_de
         cudaMemcpyAsync(plan + sb, blks.data(), sizeof(EncBlk) * blks.size(), cudaMemcpyHostToDevice, st);
         p.segs_dev = reinterpret_cast<const EncSegD*>(plan);
         p.blks_dev = reinterpret_cast<const EncBlk*>(plan + sb);
-        encode_kernel<<<(unsigned)grid, kEncThreads, kEncDynSmem, st>>>(p);
+        if (amax_in)
+            encode_kernel<true><<<(unsigned)grid, kEncThreads, kEncDynSmem, st>>>(p);
+        else
+            encode_kernel<false><<<(unsigned)grid, kEncThreads, kEncDynSmem, st>>>(p);
     }
     return cuda_check("a8_encode");
+}
+
+extern "C" int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_dev, int norm,
+                         const void* static_lut_dev, a8_layout_t layout, void* workspace,
+                         size_t workspace_bytes, const uint32_t* status_in, uint32_t* status_out,
+                         void* stream) {
+    return encode_impl(segs, nseg, book_dev, norm, static_lut_dev, layout, workspace, workspace_bytes, status_in,
+                       status_out, stream, nullptr);
+}
+
+extern "C" int a8_encode_premax(const a8_enc_seg_t* segs, int nseg, const void* book_dev, const uint32_t* amax_dev,
+                                a8_layout_t layout, void* workspace, size_t workspace_bytes,
+                                const uint32_t* status_in, uint32_t* status_out, void* stream) {
+    if (!amax_dev) return fail(A8_ERR_USAGE, "a8_encode_premax: null amax_dev");
+    return encode_impl(segs, nseg, book_dev, A8_NORM_ABSMAX, nullptr, layout, workspace, workspace_bytes, status_in,
+                       status_out, stream, amax_dev);
 }
 
 static int decode_impl(const a8_dec_seg_t* segs, const float* const* locals, int local_rank, int nseg,

@@ -59,7 +59,10 @@ class SegmentCodec:
 
     def encode(self, xs, flat_offs, scale_idx, cb: Codebook, buf: torch.Tensor, codes_off: int,
                scales_off: int, block_len: int, block_stride: int, scale_block_stride: int,
-               reps: int, status_off: int, status_in: Optional[torch.Tensor] = None) -> None:
+               reps: int, status_off: int, status_in: Optional[torch.Tensor] = None,
+               amax: Optional[torch.Tensor] = None) -> None:
+        """``amax``: float32 device tensor, max|xs[i]| per tensor as written by
+        the producer (absmax specs): one-pass encode (a8_encode_premax)."""
         raise NotImplementedError
 
     def decode(self, outs, flat_offs, scale_idx, cb: Codebook, buf: torch.Tensor, codes_off: int,
@@ -138,7 +141,7 @@ class CudaSegmentCodec(SegmentCodec):
                                            stream))
 
     def encode(self, xs, flat_offs, scale_idx, cb, buf, codes_off, scales_off, block_len,
-               block_stride, scale_block_stride, reps, status_off, status_in=None):
+               block_stride, scale_block_stride, reps, status_off, status_in=None, amax=None):
         dev = buf.device
         book, lut = cb.device_tables(dev)
         n = len(xs)
@@ -150,6 +153,11 @@ class CudaSegmentCodec(SegmentCodec):
                        scale_block_stride, 0, reps, 0)
         stream = torch.cuda.current_stream(dev).cuda_stream
         ws = workspace(dev, stream, n)
+        if amax is not None:
+            N.check(self._lib.a8_encode_premax(segs, n, book.data_ptr(), amax.data_ptr(), lay, ws.data_ptr(),
+                                               ws.numel(), None if status_in is None else status_in.data_ptr(),
+                                               base + status_off, stream))
+            return
         N.check(self._lib.a8_encode(segs, n, book.data_ptr(), cb.spec.norm_code,
                                 None if lut is None else lut.data_ptr(), lay, ws.data_ptr(), ws.numel(),
                                 None if status_in is None else status_in.data_ptr(),
@@ -274,6 +282,20 @@ def make_plan(sizes: Sequence[int], nranks: int) -> Plan:
 
 # ---------------------------------------------------------------------------
 # the exchange
+
+
+def _check_amax(amax, tensors, spec) -> None:
+    """Validate producer maxima for ``tensors`` (see GradientExchange.__call__)."""
+    if amax is None:
+        return
+    if getattr(spec, "normalization", None) is None or spec.normalization.value != "absmax":
+        raise UsageError(f"amax applies to absmax specs only, not {spec.label()}")
+    dev = tensors[0].device
+    if (not isinstance(amax, torch.Tensor) or amax.dtype != torch.float32 or amax.device != dev
+            or amax.numel() != len(tensors) or not amax.is_contiguous()):
+        raise UsageError(f"amax must be a contiguous float32 tensor of {len(tensors)} maxima on {dev}")
+    if dev.type != "cuda":
+        raise UsageError("amax needs CUDA tensors")
 
 
 class _StepRecorder:
@@ -491,10 +513,15 @@ class GradientExchange:
             bad = count > self._seen.get(gkey, 0)
             self._seen[gkey] = count
         else:
-            bad = bool(int(word[0]) & N.A8_STATUS_NONFINITE)
+            w = int(word[0])
+            if w & N.A8_STATUS_AMAX_MISMATCH:
+                self._pending.clear()
+                raise UsageError(f"exchange call {call}: a supplied amax is not max|x| of its tensor")
+            bad = bool(w & N.A8_STATUS_NONFINITE)
         if bad:
             self._pending.clear()
-            raise InputError(f"exchange call {call}: cannot encode non-finite values (NaN or Inf present)")
+            raise InputError(f"exchange call {call}: cannot encode non-finite values (NaN or Inf present)"
+                             + (" (or a supplied amax is not max|x|)" if gkey is not None else ""))
         return True
 
     def synchronize(self) -> None:
@@ -508,12 +535,20 @@ class GradientExchange:
             pass
 
     # -- main entry
-    def __call__(self, tensors: Sequence[torch.Tensor], out: Optional[Sequence[torch.Tensor]] = None):
+    def __call__(self, tensors: Sequence[torch.Tensor], out: Optional[Sequence[torch.Tensor]] = None,
+                 amax: Optional[torch.Tensor] = None):
+        """``amax`` (absmax specs): float32 tensor on the inputs' device with
+        max|tensors[i]| at [i], written by the kernel that produced the
+        tensors (``produce.scale_absmax_``, ``produce.relu_absmax``): the
+        encode is then one pass over the inputs (a8_encode_premax).  A wrong
+        value raises UsageError at the status check."""
         tensors = list(tensors)
         if not tensors:
             return []
         self._poll()
         dev = tensors[0].device
+        _check_amax(amax, tensors, self.spec)
+        self._amax = amax
         for t in tensors:
             if t.dtype != torch.float32 or not t.is_contiguous() or t.device != dev:
                 raise UsageError("exchange needs contiguous float32 tensors on one device")
@@ -542,6 +577,11 @@ class GradientExchange:
         self.calls += 1
         return outs
 
+    _amax = None  # the current call's producer maxima (None: the encode computes them)
+
+    def _amax_kw(self) -> dict:
+        return {} if self._amax is None else {"amax": self._amax}
+
     def _step_prepared(self, tensors, outs, plan, nranks, rank, dev):
         """Eager step through a recorded launch list (see _StepRecorder):
         the first call with a key runs normally while recording; later calls
@@ -551,7 +591,7 @@ class GradientExchange:
         stream = torch.cuda.current_stream(dev).cuda_stream
         key = (plan.sizes, nranks, rank, self.mode, self.op, self.local_fp32, stream,
                workspace_epoch(dev, stream), tuple(t.data_ptr() for t in tensors),
-               tuple(o.data_ptr() for o in outs))
+               tuple(o.data_ptr() for o in outs), 0 if self._amax is None else self._amax.data_ptr())
         rec = self._prepared.get(key)
         if rec is not None:
             word = self._status_word(dev)
@@ -592,7 +632,7 @@ class GradientExchange:
         eagerly on a side stream (allocating every buffer and workspace the
         step uses) and captures the step; later calls replay it."""
         key = (plan.sizes, nranks, self.mode, tuple(t.data_ptr() for t in tensors),
-               tuple(o.data_ptr() for o in outs))
+               tuple(o.data_ptr() for o in outs), 0 if self._amax is None else self._amax.data_ptr())
         hit = self._graphs.get(key)
         cur = torch.cuda.current_stream(dev)
         if hit is not None and hit[2] != workspace_epoch(dev, self._gstream.cuda_stream):
@@ -661,7 +701,7 @@ class GradientExchange:
         idx = list(range(plan.nseg))
         mine = rank * P
         self.codec.encode(xs, plan.offs, idx, self.cb, gathered, mine, mine + C, C, BS, BS // 4, K,
-                          mine + C + 4 * plan.status_slot)
+                          mine + C + 4 * plan.status_slot, **self._amax_kw())
         status = self._status_word(dev)
         op = 1 if self.op == "avg" else 0
         loc = self.local_fp32
@@ -699,7 +739,7 @@ class GradientExchange:
         idx = list(range(plan.nseg))
         # round 1: per-tensor encode straight into the N send blocks
         self.codec.encode(xs, plan.offs, idx, self.cb, send, 0, L, L, B, sbs, nranks,
-                          L + 4 * plan.status_slot)
+                          L + 4 * plan.status_slot, **self._amax_kw())
         self.comm.all_to_all(recv, send)
         # decode-average the N contributions to my shard
         mine = [p for p in plan.pieces if p.shard == rank]
@@ -976,7 +1016,8 @@ class PeerExchange(GradientExchange):
         self.transport = transport
         self.comm = transport  # world()
 
-    def __call__(self, tensors: Sequence[torch.Tensor], out: Optional[Sequence[torch.Tensor]] = None):
+    def __call__(self, tensors: Sequence[torch.Tensor], out: Optional[Sequence[torch.Tensor]] = None,
+                 amax: Optional[torch.Tensor] = None):
         tensors = list(tensors)
         if not tensors:
             return []
@@ -985,6 +1026,8 @@ class PeerExchange(GradientExchange):
         for t in tensors:
             if t.dtype != torch.float32 or not t.is_contiguous() or t.device != dev:
                 raise UsageError("exchange needs contiguous float32 tensors on one device")
+        _check_amax(amax, tensors, self.spec)
+        self._amax = amax
         outs = list(out) if out is not None else tensors
         if len(outs) != len(tensors) or any(o.dtype != torch.float32 or not o.is_contiguous() or o.device != dev
                                             or o.numel() != t.numel() for t, o in zip(tensors, outs)):
@@ -1008,7 +1051,8 @@ class PeerExchange(GradientExchange):
         P = plan.allgather_block()
         slab, ptrs = self.transport.buffer(f"ag{par}", P, dev)
         idx = list(range(plan.nseg))
-        self.codec.encode(xs, plan.offs, idx, self.cb, slab, 0, C, C, C, 0, 1, C + 4 * plan.status_slot)
+        self.codec.encode(xs, plan.offs, idx, self.cb, slab, 0, C, C, C, 0, 1, C + 4 * plan.status_slot,
+                          **self._amax_kw())
         self.transport.barrier()
         status = self._status_word(dev)
         self.codec.decode_peers(outs, plan.offs, idx, self.cb, 0, C, C, C, 0, ptrs[:nranks],
@@ -1022,7 +1066,8 @@ class PeerExchange(GradientExchange):
         send, sptrs = self.transport.buffer(f"tr_send{par}", nranks * B, dev)
         idx = list(range(plan.nseg))
         # round 1: per-tensor encode into the N destination blocks of my slab
-        self.codec.encode(xs, plan.offs, idx, self.cb, send, 0, L, L, B, sbs, nranks, L + 4 * plan.status_slot)
+        self.codec.encode(xs, plan.offs, idx, self.cb, send, 0, L, L, B, sbs, nranks, L + 4 * plan.status_slot,
+                          **self._amax_kw())
         self.transport.barrier()
         mine = [p for p in plan.pieces if p.shard == rank]
         shard_buf = self._buffer("shard", max(L, 16) * 4, dev).view(torch.float32)
@@ -1072,9 +1117,13 @@ class CompressedAllGather:
         self.comm = comm or TorchDistComm(group)
         self._bufs: dict = {}
 
-    def __call__(self, shard: torch.Tensor, out: Optional[Sequence[torch.Tensor]] = None):
+    def __call__(self, shard: torch.Tensor, out: Optional[Sequence[torch.Tensor]] = None,
+                 amax: Optional[torch.Tensor] = None):
+        """``amax``: max|shard| from its producer (float32, 1 element), see
+        GradientExchange.__call__."""
         if shard.dtype != torch.float32 or not shard.is_contiguous():
             raise UsageError("all-gather needs a contiguous float32 tensor")
+        _check_amax(amax, [shard], self.spec)
         nranks, rank = self.comm.world()
         dev = shard.device
         n = shard.numel()
@@ -1086,7 +1135,8 @@ class CompressedAllGather:
                                torch.zeros(1, dtype=torch.int32, device=dev))
         slab, status = self._bufs[key]
         self.codec.encode([shard], [0], [0], self.cb, slab, rank * B, rank * B + plan.flat, plan.flat,
-                          plan.flat, 0, 1, rank * B + plan.flat + 4 * plan.status_slot)
+                          plan.flat, 0, 1, rank * B + plan.flat + 4 * plan.status_slot,
+                          **({} if amax is None else {"amax": amax}))
         if nranks > 1:
             self.comm.all_gather(slab, slab[rank * B:(rank + 1) * B])
         outs = list(out) if out is not None else [torch.empty_like(shard) for _ in range(nranks)]
@@ -1094,7 +1144,10 @@ class CompressedAllGather:
         flat_offs = [j * plan.flat for j in range(nranks)]
         self.codec.decode(outs, flat_offs, [0] * nranks, self.cb, slab, 0, plan.flat, plan.flat, B, B // 4,
                           0, 1, 0, plan.status_slot, nranks, status)
-        if int(status.cpu()[0]) & N.A8_STATUS_NONFINITE:
+        st = int(status.cpu()[0])
+        if st & N.A8_STATUS_AMAX_MISMATCH:
+            raise UsageError("the supplied amax is not max|shard|")
+        if st & N.A8_STATUS_NONFINITE:
             raise InputError("cannot encode non-finite values (NaN or Inf present)")
         return outs
 

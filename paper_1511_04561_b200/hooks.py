@@ -159,27 +159,49 @@ class ModelParallelFC:
                    (op="sum"): dx = sum_r q(dx_r), rank order, float32;
                    dW_r = x^T dy_r stays local.
     ``comm`` is the collective backend (torch.distributed by default).
+    ``activation="relu"``: the shipped tensor is the hidden activation
+    h_r = np.maximum(y_r, 0) [* mask_r] (mlp.py:205-209), produced by
+    ``relu_absmax`` so that its max comes with it and the encode is one pass
+    (absmax specs); backward then takes dy w.r.t. h.
     """
 
-    def __init__(self, weight_shard: torch.Tensor, spec: DataTypeSpec, group=None, comm=None, codec=None):
+    def __init__(self, weight_shard: torch.Tensor, spec: DataTypeSpec, group=None, comm=None, codec=None,
+                 activation: Optional[str] = None):
         from .exchange import CompressedAllGather, GradientExchange
 
+        if activation not in (None, "relu"):
+            raise ConfigError(f"activation must be None or 'relu', got {activation!r}")
         self.w = weight_shard
         self.spec = spec
+        self.activation = activation
         self.gather = CompressedAllGather(spec, group, codec=codec, comm=comm)
         self.reduce = GradientExchange(spec, group, mode="allgather", op="sum", check="sync", codec=codec, comm=comm)
         self._x = None
+        self._gate = None
 
-    def forward(self, x: torch.Tensor) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, mask: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """``mask``: this rank's dropout multipliers (same shape as y_r), relu only."""
+        from .produce import relu_absmax
+
         self._x = x
         y_r = (x @ self.w).contiguous()
-        parts = self.gather(y_r)
+        if self.activation is None:
+            if mask is not None:
+                raise ConfigError("mask needs activation='relu'")
+            parts = self.gather(y_r)
+        else:
+            gate = (y_r > 0).to(torch.float32)  # d h / d y = mask * (y > 0) (mlp.py:250-253)
+            self._gate = gate if mask is None else gate * mask
+            h_r, amax = relu_absmax(y_r, mask, out=y_r)
+            parts = self.gather(h_r, amax=amax if self.spec.normalization is NormKind.ABSMAX else None)
         return torch.cat(parts, dim=1)
 
     def backward(self, dy: torch.Tensor):
         n_r = self.w.shape[1]
         nranks, rank = self.gather.comm.world()
         dy_r = dy[:, rank * n_r:(rank + 1) * n_r]
+        if self._gate is not None:
+            dy_r = dy_r * self._gate
         dw = self._x.t() @ dy_r
         dx = (dy_r @ self.w.t()).contiguous()
         self.reduce([dx])

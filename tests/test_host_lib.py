@@ -44,6 +44,7 @@ def test_struct_sizes_match_the_header():
     assert C.sizeof(N.EncSeg) == 32 and C.sizeof(N.DecSeg) == 32
     assert C.sizeof(N.Layout) == 56
     assert C.sizeof(N.ObSeg) == 24
+    assert C.sizeof(N.ProdSeg) == 32
 
 
 @pytest.mark.parametrize("kind", ["dynamic-tree", "static-tree", "linear", "mantissa"])
