@@ -487,12 +487,29 @@ def codec_sweep(A, torch, dev, clk_sampler_cls):
         def fused():
             ex2(ts, amax=A.scale_absmax_(ts, half))
 
-        r = {"tensors": len(ts), "elements": sum(t.numel() for t in ts),
+        # the encode alone (one multi-tensor launch, as the exchange issues it)
+        from paper_1511_04561_b200.exchange import CudaSegmentCodec, make_plan
+
+        plan = make_plan(tuple(t.numel() for t in ts), 1)
+        C, P = plan.flat, plan.allgather_block()
+        slab = torch.zeros(P, dtype=torch.uint8, device=dev)
+        cb, codec, idx = A.build_codebook(spec), CudaSegmentCodec(), list(range(plan.nseg))
+        m = A.scale_absmax_(ts, 1.0)
+
+        def enc(**kw):
+            codec.encode(ts, plan.offs, idx, cb, slab, 0, C, C, C, 0, 1, C + 4 * plan.status_slot, **kw)
+
+        n_el = sum(t.numel() for t in ts)
+        te2, te1 = time_graph(enc, 15), time_graph(lambda: enc(amax=m), 15)
+        r = {"encode_two_pass_ms": te2, "encode_premax_ms": te1,
+             "encode_premax_frac": 5.0 * n_el / (te1 * 1e-3) / 1e9 / peak,
+             "encode_two_pass_frac": 5.0 * n_el / (te2 * 1e-3) / 1e9 / peak}
+        r.update({"tensors": len(ts), "elements": n_el,
              "torch_scale_then_exchange_ms": time_graph(two_pass, 15),
              "fused_scale_absmax_then_premax_exchange_ms": time_graph(fused, 15),
              "exchange_alone_ms": time_graph(lambda: ex1(ts), 15),
-             "max_pass_then_premax_exchange_ms": time_graph(lambda: ex2(ts, amax=A.scale_absmax_(ts, 1.0)), 15)}
-        del ts
+             "max_pass_then_premax_exchange_ms": time_graph(lambda: ex2(ts, amax=A.scale_absmax_(ts, 1.0)), 15)})
+        del ts, slab
         return r
 
     out = {}

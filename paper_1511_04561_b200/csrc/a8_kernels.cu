@@ -387,6 +387,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
     // on every ticket, and kernel-parameter / global reads cost it latency
     __shared__ EncSegD sSeg[kSmemSegs];
     __shared__ EncBlk sBlk[kSmemBlks];
+    __shared__ unsigned int sPmax[kPremax ? kSmemSegs : 1];  // supplied maxima, by (sorted) segment
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -417,6 +418,10 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
     }
     if (!p.absmax && tid >= 32)  // fixed scale: one table (slot 0) for every segment
         load_lut_smem(p.static_lut, sLut[0].e, sLut[0].T, sCanon, p.book, sHdr, tid - 32, kConsumers);
+    if (kPremax) {
+        const EncSegD* gs = p.segs_dev ? p.segs_dev : p.segs;
+        for (int i = tid; i < min(p.nseg, kSmemSegs); i += kEncThreads) sPmax[i] = __ldg(p.amax_in + gs[i].src);
+    }
     __syncthreads();
     const uint32_t full0 = smem_addr(&sFull[0]), empty0 = smem_addr(&sEmpty[0]);  // ring barriers
 
@@ -603,6 +608,75 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
 #ifdef A8_TICKET_TRACE
             unsigned long long sw[5] = {gtime(), 0, 0, 0, 0};
 #endif
+            if (kPremax) {
+                // The max is known (shared memory): build at once, no global
+                // round trip on the critical path.  The CAS that elects the
+                // segment's publisher is issued now and read after the build.
+                unsigned int claim = 1u;
+                if (ctid == 128) claim = atomicCAS(&p.ctl[seg].ready, 0u, 1u);
+                const unsigned int amax = seg < kSmemSegs ? sPmax[seg] : __ldg(p.amax_in + segs[seg].src);
+                const float scale = amax == 0u ? 1.0f : __uint_as_float(amax);
+                uint32_t t = kInfBits;
+                if (ctid < 128) {
+                    if (scale_ok(scale) && ctid + 1 < p.book->ndistinct) t = threshold_fast((double)scale, sV[ctid], sV[ctid + 1]);
+                    T[ctid] = t;
+                }
+                const int nf = nbar_popc(kBarC, kConsumers, ctid < 127 && t < kInfBits);
+                SW_STAMP(2);
+                int32_t kb;
+                uint32_t len;
+                lut_geometry(T, (uint32_t)nf, &kb, &len);
+                len = max((int32_t)len, (int32_t)(amax >> kKeyShift) - kb + 1);
+                const bool ok = len <= (uint32_t)kLutMax && fill_lut_carry(T, (uint32_t)nf, kb, len, E, ctid);
+                const int valid = nbar_and(kBarC, kConsumers, ok);
+                SW_STAMP(3);
+                if (Lt && ctid == 0) {
+                    Lt->len = len;
+                    Lt->kbase = kb;
+                    Lt->valid = (uint32_t)valid;
+                    Lt->nfinite = (uint32_t)nf;
+                    Lt->scale = scale;
+                }
+                if (ctid == 128) sMode = claim == 0u ? 3 : 1;
+                nbar_sync(kBarC, kConsumers);
+                const int mode = sMode;
+                if (mode == 3) {
+                    a8_lut_t* G = p.luts + seg;
+                    if (ctid < 128) G->T[ctid] = T[ctid];
+                    if (valid) {
+                        uint4* d4 = reinterpret_cast<uint4*>(G->e);
+                        const uint4* s4 = reinterpret_cast<const uint4*>(E);
+                        for (uint32_t j = ctid; j < (len + 3) >> 2; j += kConsumers) d4[j] = s4[j];
+                    }
+                    if (ctid == 0) {
+                        G->len = len;
+                        G->kbase = kb;
+                        G->valid = (uint32_t)valid;
+                        G->nfinite = (uint32_t)nf;
+                        G->scale = scale;
+                        p.ctl[seg].len = len;
+                    }
+                    nbar_sync(kBarC, kConsumers);
+                    if (ctid == 0) {
+                        __threadfence();
+                        st_release(&p.ctl[seg].ready, 2u);
+                    }
+                }
+                nbar_sync(kBarC, kConsumers);  // sMode read by all before the next switch rewrites it
+#ifdef A8_TICKET_TRACE
+                if (ctid == 0) {
+                    sw[4] = gtime();
+                    const unsigned int i = atomicAdd(&g_switch_n, 1u);
+                    if (i < kTraceSw) {
+                        g_switch_trace[i][0] = (unsigned long long)sw_tkt;
+                        g_switch_trace[i][1] = blockIdx.x | ((unsigned long long)btk << 16) | ((unsigned long long)mode << 24);
+                        g_switch_trace[i][2] = seg;
+                        for (int q = 0; q < 5; ++q) g_switch_trace[i][3 + q] = sw[q];
+                    }
+                }
+#endif
+                return;
+            }
             if (ctid == 0) {
                 // every A-chunk of the segment reduced -> its max is final
                 const SegCtl* c = p.ctl + seg;
@@ -1888,8 +1962,10 @@ static void schedule(const std::vector<EncSegD>& d, bool absmax, int64_t wf, std
 // dependency to hide.  F tickets (single-chunk segments) first, then one B
 // ticket per multi-chunk segment (its table is built and published at once;
 // CTAs that reach the segment's E-chunks before that build their own copy),
-// then the E passes, largest segment first so the launch ends on small runs.
-static void schedule_premax(const std::vector<EncSegD>& d, std::vector<EncBlk>* blks) {
+// then the E passes, largest segment first -- except that the last `hold`
+// chunks of the largest segment end the launch: every CTA finishes on a
+// long run whose table is published (no table switches in the tail).
+static void schedule_premax(const std::vector<EncSegD>& d, int64_t ctas, std::vector<EncBlk>* blks) {
     int64_t t = 0;
     auto emit = [&](int s, int kind, int64_t c0, int64_t cnt) {
         if (cnt <= 0) return;
@@ -1900,7 +1976,16 @@ static void schedule_premax(const std::vector<EncSegD>& d, std::vector<EncBlk>* 
     for (int s = 0; s < nseg; ++s)
         if (d[s].n <= kChunk) emit(s, kF, 0, 1);
     for (int s = nseg - 1; s >= 0 && d[s].n > kChunk; --s) emit(s, kB, 0, 1);
-    for (int s = nseg - 1; s >= 0 && d[s].n > kChunk; --s) emit(s, kE, d[s].nE - 1, d[s].nE);
+    const int big = nseg - 1;
+    const bool several = nseg >= 2 && d[nseg - 2].n > kChunk;
+    static const int64_t hold_per_cta = [] {  // A8_PREMAX_HOLD: tail chunks per CTA (tuning)
+        const char* v = getenv("A8_PREMAX_HOLD");
+        return v ? std::max(0ll, atoll(v)) : 4ll;
+    }();
+    const int64_t hold = several && d[big].n > kChunk ? std::min<int64_t>(d[big].nE / 2, hold_per_cta * ctas) : 0;
+    for (int s = nseg - 1; s >= 0 && d[s].n > kChunk; --s)
+        emit(s, kE, d[s].nE - 1, s == big ? d[s].nE - hold : d[s].nE);
+    emit(big, kE, hold - 1, hold);  // chunks hold-1 .. 0 of the largest segment
     blks->push_back(EncBlk{t, -1, 0});  // sentinel: total tickets
 }
 
@@ -2165,7 +2250,7 @@ static int encode_impl(const a8_enc_seg_t* segs, int nseg, const void* book_dev,
     }
     std::vector<EncBlk> blks;
     if (amax_in)
-        schedule_premax(d, &blks);
+        schedule_premax(d, (int64_t)di.sms * di.enc_occ, &blks);
     else
         schedule(d, absmax, fill_distance((int64_t)di.sms * di.enc_occ), &blks);
     const int nblk = (int)blks.size() - 1;

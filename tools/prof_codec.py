@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -41,9 +42,11 @@ def run(sizes, spec, iters, dev):
     idx = list(range(len(xs)))
     n = sum(x.numel() for x in xs)
 
+    kw = {"amax": A.scale_absmax_(xs, 1.0)} if PREMAX else {}
+
     def enc():
         codec.encode(xs, plan.offs, idx, cb, buf, 0, plan.flat, plan.flat, plan.flat, 0, 1,
-                     plan.flat + 4 * plan.status_slot)
+                     plan.flat + 4 * plan.status_slot, **kw)
 
     def dec():
         codec.decode(outs, plan.offs, idx, cb, buf, 0, plan.flat, plan.flat, plan.flat, 0, B, 1, 1,
@@ -88,6 +91,7 @@ def run(sizes, spec, iters, dev):
 
 
 TRACE = "--trace" in sys.argv
+PREMAX = "--premax" in sys.argv or os.environ.get("A8_PREMAX") == "1"  # supplied maxima (a8_encode_premax)
 
 
 def main():
@@ -96,6 +100,7 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--spec", default="dynamic-tree/absmax")
     ap.add_argument("--trace", action="store_true")
+    ap.add_argument("--premax", action="store_true")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     spec = A.parse_spec(a.spec)
