@@ -84,6 +84,9 @@ def main():
         if len(r):
             print(f"  switch {name}: {len(r)} x mean {np.mean(r[:, 7] - r[:, 3]) / 1e3:.2f} us "
                   f"(sum {np.sum(r[:, 7] - r[:, 3]) / 1e3:.0f} us)")
+            if md in (1, 3) and (r[:, 5] > 0).all() and (r[:, 6] > 0).all():
+                print(f"    phases: thresholds {np.mean(r[:, 5] - r[:, 3]) / 1e3:.2f} fill "
+                      f"{np.mean(r[:, 6] - r[:, 5]) / 1e3:.2f} end {np.mean(r[:, 7] - r[:, 6]) / 1e3:.2f} us")
 
 
 if __name__ == "__main__":
