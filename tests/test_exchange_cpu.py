@@ -372,3 +372,23 @@ def test_ddp_comm_hook_onebit_gloo_world_size_2():
         p.join(timeout=300)
     results = dict(q.get(timeout=5) for _ in range(2))
     assert results == {0: True, 1: True}
+
+
+def test_amax_validation():
+    """Producer maxima (GradientExchange(...)(..., amax=)): absmax specs only,
+    one float32 per tensor on the tensors' device, CUDA only -- all checked
+    before any codec work."""
+    spec = A.DataTypeSpec("dynamic-tree", "absmax")
+    ex = A.GradientExchange(spec, check="sync", codec=NumpyCodec(spec))
+    ts = [torch.zeros(10), torch.zeros(3)]
+    with pytest.raises(A.UsageError, match="CUDA"):
+        ex(ts, amax=torch.zeros(2))
+    with pytest.raises(A.UsageError, match="2 maxima"):
+        ex(ts, amax=torch.zeros(3))
+    with pytest.raises(A.UsageError, match="2 maxima"):
+        ex(ts, amax=torch.zeros(2, dtype=torch.float64))
+    fixed = A.DataTypeSpec("mantissa", "none")
+    with pytest.raises(A.UsageError, match="absmax"):
+        A.GradientExchange(fixed, check="sync", codec=NumpyCodec(fixed))(ts, amax=torch.zeros(2))
+    with pytest.raises(A.ConfigError):
+        A.ModelParallelFC(torch.zeros(4, 2), spec, activation="gelu")

@@ -182,3 +182,33 @@ def test_model_parallel_relu_ships_relu_activation(cuda):
     dx, dw = fc.backward(dy)
     dz = dy * ((x @ w) > 0).float() * mask
     assert torch.allclose(dw, x.t() @ dz, rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("mode", ["allgather", "two_round"])
+def test_peer_exchange_premax_matches_oracle(cuda, mode):
+    """PeerExchange (virtual ranks on one GPU) with every rank's maxima from
+    its producer pass: bit-exact against the composed oracle."""
+    from helpers import run_virtual_peers
+
+    sizes = [5, 4096, 70001, 300_000]
+
+    def per(rank, step):
+        return [O.sample_normal(n, 100 * rank + 10 * step + i, 0.0, 1e-3) for i, n in enumerate(sizes)]
+
+    def body(rank, peers):
+        ex = A.PeerExchange(SPEC, peers, mode=mode, check="sync")
+        res = []
+        for step in range(2):
+            ts = [torch.from_numpy(g).to(cuda) for g in per(rank, step)]
+            ex(ts, amax=A.scale_absmax_(ts, 1.0))
+            res.append([t.cpu().numpy() for t in ts])
+        return res
+
+    res = run_virtual_peers(3, body)
+    for step in range(2):
+        ins = [per(r, step) for r in range(3)]
+        want = (O.exchange_allgather(ins, "dynamic-tree", "absmax") if mode == "allgather"
+                else O.exchange_two_round(ins, "dynamic-tree", "absmax"))
+        for r in range(3):
+            for a, b in zip(res[r][step], want):
+                assert a.tobytes() == b.astype(np.float32).tobytes(), (r, step)
