@@ -512,6 +512,33 @@ def codec_sweep(A, torch, dev, clk_sampler_cls):
         del ts, slab
         return r
 
+    def onebit_c3():
+        """The 1-bit error-feedback exchange (GradientExchange("onebit"),
+        mlp.py:313-321) over the config-3 gradients at N = 1: quantize
+        (float64 residual per tensor) + the fused level decode, one step."""
+        ts = [torch.randn(int(np.prod(s)), device=dev) * 1e-3 for s in ALEXNET]
+        outs = [torch.empty_like(t) for t in ts]
+        ex = A.GradientExchange("onebit", check="none")
+        n_el = sum(t.numel() for t in ts)
+        ex(ts, out=outs)  # residuals allocated
+        torch.cuda.synchronize()
+        try:
+            ms, how = time_graph(lambda: ex(ts, out=outs), 15), "graph"
+        except Exception:  # noqa: BLE001  (eager timing if the step cannot be captured)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(15):
+                ex(ts, out=outs)
+            e1.record()
+            torch.cuda.synchronize()
+            ms, how = e0.elapsed_time(e1) / 15, "eager"
+        del ts, outs
+        # bytes: quantize reads g + residual twice, writes residual + bits; decode writes out
+        return {"elements": n_el, "step_ms": ms, "timing": how,
+                "fp32_equiv_GBps": 4.0 * n_el / (ms * 1e-3) / 1e9,
+                "hbm_GBps_at_32B_per_elem": 32.0 * n_el / (ms * 1e-3) / 1e9}
+
     out = {}
     with clk_sampler_cls(dev.index) as clk:
         out["c1"] = [case(1 << 20, lab) for lab in ("dynamic-tree/absmax", "linear/absmax", "static-tree/decade+1",
@@ -519,6 +546,7 @@ def codec_sweep(A, torch, dev, clk_sampler_cls):
         out["c4"] = [case(1 << k, lab) for k in (28, 30) for lab in ("dynamic-tree/absmax", "mantissa/decade+1")]
         out["blocked"] = [case(1 << 30, "dynamic-tree/absmax", b) for b in (4096, 1024)]
         out["premax"] = {"c4": [premax_c4(1 << k) for k in (28, 30)], "c3": premax_c3()}
+        out["onebit_c3"] = onebit_c3()
     out["clocks"] = clk.summary()
     out["how"] = ("one public-API encode_buffer / decode_buffer call per case, CUDA-graph replayed between events, "
                   "median of 7-15, 256 MB L2 flush before each; GB/s at 5 B/elem each way, round trip 10 B/elem; "

@@ -140,6 +140,8 @@ struct EncParams {
     int code_hint;  // L2 policy of the code stores: 0 default, 1 evict_first, 2 evict_last (A8_CODE_HINT)
     int64_t total;
     const unsigned int* amax_in;  // a8_encode_premax: bits of max|x| per caller segment (else null)
+    int64_t keep_tail;            // A8_KEEP_TAIL (tuning): < 0 keeps every A read in L2
+    int pol_a, pol_e;             // L2 policies of the A / E reads (A8_POL_A / A8_POL_E)
     EncSegD segs[kInlineSegs];
     EncBlk blks[kInlineBlks];
 };
@@ -158,6 +160,7 @@ struct DecParams {
     int local_rank;  // >= 0: rank whose term is the local float32 input (decode_kernel<true>)
     int64_t rank_off[kMaxRanks];  // bytes from rank 0's codes/scales to rank r's: r * rank_stride, or
                                   // the distance between peers' slabs (a8_decode_peers, UVA)
+    int rpol, wpol;               // decode_tma_kernel L2 policies (A8_DEC_RPOL / A8_DEC_WPOL tuning)
     DecSegD segs[kInlineSegs];
 };
 
@@ -428,8 +431,14 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
     if (warp == 0) {
         // ===================== producer =====================
         if (lane == 0) {
-            const uint64_t keep = policy_evict_last();   // A reads: keep for the E re-read
-            const uint64_t drop = policy_evict_first();  // E reads: last use
+            // L2 policies (A8_POL_A / A8_POL_E tuning: 0 evict_first, 1 normal, 2 evict_last).
+            // Both evict_first: the A pass's lines are not worth keeping (the E
+            // re-read comes a fill distance later, ~100 MB of traffic away), and
+            // keeping them evicts what is reused: C3 encode 105.0 -> 96.8 us,
+            // bench step 171.7 -> 161.6 us (the decode gains too).
+            auto pol = [](int k) { return k == 2 ? policy_evict_last() : k == 1 ? policy_evict_normal() : policy_evict_first(); };
+            const uint64_t keep = pol(p.pol_a);  // A reads
+            const uint64_t drop = pol(p.pol_e);  // E reads: last use
             const int64_t L = p.lay.block_len;
             const int64_t gap = p.lay.block_stride - p.lay.block_len;
             // tickets come in batches, requested two batches ahead so the
@@ -531,7 +540,10 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                 const uint32_t tx = (uint32_t)m.bulk * 4u;
                 if (tx > 0) {
                     mbar_arrive_expect_tx(&sFull[st], tx);
-                    bulk_g2s(sStage + (size_t)st * kChunk, sg.x + m.base, tx, &sFull[st], kind == kA ? keep : drop);
+                    // A reads take the `keep` policy; with keep_tail set (A8_KEEP_TAIL,
+                    // tuning) only the largest segment's last keep_tail chunks do
+                    const bool kp = kind == kA && (p.keep_tail < 0 || (bk.seg == p.nseg - 1 && chunk >= sg.nA - p.keep_tail));
+                    bulk_g2s(sStage + (size_t)st * kChunk, sg.x + m.base, tx, &sFull[st], kp ? keep : drop);
                 } else {
                     mbar_arrive(&sFull[st]);
                 }
@@ -1698,7 +1710,7 @@ __global__ void __launch_bounds__(kDtCons + 32, 2) decode_tma_kernel(const __gri
     const int64_t nmy = p.total > blockIdx.x ? (p.total - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     if (warp == 0) {
         if (lane == 0) {
-            const uint64_t drop = policy_evict_first();
+            const uint64_t drop = p.rpol == 2 ? policy_evict_last() : p.rpol == 1 ? policy_evict_normal() : policy_evict_first();
             int st = 0;
             uint32_t ph = 0;
             for (int64_t k = 0; k < nmy; ++k) {
@@ -1729,7 +1741,7 @@ __global__ void __launch_bounds__(kDtCons + 32, 2) decode_tma_kernel(const __gri
     const float* tl = sTab + lane;
     const float invN = 1.0f / (float)R;
     const bool pow2 = (R & (R - 1)) == 0;
-    const uint64_t wpol = policy_evict_first();
+    const uint64_t wpol = p.wpol == 2 ? policy_evict_last() : p.wpol == 1 ? policy_evict_normal() : policy_evict_first();
     int st = 0, ob = 0;
     uint32_t ph = 0;
     for (int64_t k = 0; k < nmy; ++k) {
@@ -2280,6 +2292,23 @@ static int encode_impl(const a8_enc_seg_t* segs, int nseg, const void* book_dev,
     }
     p.total = blks[nblk].tstart;
     p.amax_in = reinterpret_cast<const unsigned int*>(amax_in);
+    {
+        static const int64_t kt = [] {
+            const char* v = getenv("A8_KEEP_TAIL");
+            return v ? atoll(v) : -1ll;
+        }();
+        p.keep_tail = kt;
+        static const int pa = [] {
+            const char* v = getenv("A8_POL_A");
+            return v ? atoi(v) : 0;
+        }();
+        static const int pe = [] {
+            const char* v = getenv("A8_POL_E");
+            return v ? atoi(v) : 0;
+        }();
+        p.pol_a = pa;
+        p.pol_e = pe;
+    }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if ((int)blks.size() > max_blocks(nseg)) return fail(A8_ERR_USAGE, "a8_encode: schedule overflow");
     const int64_t grid = std::min<int64_t>((int64_t)di.sms * di.enc_occ, std::max<int64_t>(1, p.total));
@@ -2401,6 +2430,16 @@ static int decode_impl(const a8_dec_seg_t* segs, const float* const* locals, int
             attr = true;
         }
         std::copy(d.begin(), d.begin() + nseg, p.segs);
+        static const int rp = [] {
+            const char* v = getenv("A8_DEC_RPOL");
+            return v ? atoi(v) : 0;
+        }();
+        static const int wp = [] {
+            const char* v = getenv("A8_DEC_WPOL");
+            return v ? atoi(v) : 0;
+        }();
+        p.rpol = rp;
+        p.wpol = wp;
         const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)di.sms * 2, chunks));
         decode_tma_kernel<<<(unsigned)grid, kDtCons + 32, dt_smem(nranks), st>>>(p);
     } else if (nseg <= kInlineSegs) {

@@ -1,0 +1,11 @@
+run() {
+  s=$(env "$@" timeout 300 python bench.py --no-cpu --no-sweep 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('step', round(d['ms_per_step']*1e3,1), 'enc', round(d['roofline']['kernel_ms_per_step']['encode']*1e3,1), 'dec', round(d['roofline']['kernel_ms_per_step']['decode']*1e3,1))")
+  echo "$* | $s"
+}
+for rep in 1 2; do
+run A8_DEC_RPOL=0 A8_DEC_WPOL=0
+run A8_DEC_RPOL=1 A8_DEC_WPOL=0
+run A8_DEC_RPOL=0 A8_DEC_WPOL=1
+run A8_DEC_RPOL=0 A8_DEC_WPOL=2
+run A8_DEC_RPOL=1 A8_DEC_WPOL=1
+done

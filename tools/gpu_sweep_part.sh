@@ -1,0 +1,13 @@
+timeout 900 python - <<'PY' 2>&1 | tail -30
+import json, sys, torch
+sys.path.insert(0, ".")
+import bench, paper_1511_04561_b200 as A
+class Nop:
+    def __init__(self, i): pass
+    def __enter__(self): return self
+    def __exit__(self, *a): pass
+    def summary(self): return {}
+dev = torch.device("cuda", 0)
+r = bench.codec_sweep(A, torch, dev, Nop)
+print(json.dumps(r["onebit_c3"], indent=1)); print(json.dumps(r["premax"]["c3"]))
+PY
