@@ -273,6 +273,24 @@ int a8_onebit_quantize(const void* g, int g_is_f64, double* residual, int64_t n,
                        float* levels, uint32_t* status_out, void* workspace, size_t workspace_bytes,
                        void* stream);
 
+/* a8_onebit_quantize for up to 32 tensors in two launches (stats, apply)
+ * instead of two per tensor: the 1-bit exchange quantizes every gradient of
+ * a step at once.  Each segment is computed exactly as a8_onebit_quantize
+ * computes it alone (same partial layout and summation order), so the
+ * results are bit-identical.  workspace: a8_onebit_multi_workspace_bytes(nseg)
+ * bytes.                                                                    */
+typedef struct a8_ob_q_seg {
+    const void* g;
+    double* residual;
+    int64_t n;
+    uint8_t* bits;
+    float* levels;
+    uint32_t* status;
+} a8_ob_q_seg_t;
+size_t a8_onebit_multi_workspace_bytes(int nseg);
+int a8_onebit_quantize_multi(const a8_ob_q_seg_t* segs, int nseg, int g_is_f64, void* workspace,
+                             size_t workspace_bytes, void* stream);
+
 /* onebit_decode (codecs.py:342-348): out[i] = bit ? levels[0] : levels[1]. */
 int a8_onebit_decode(const uint8_t* bits, int64_t n, const float* levels, float* out, void* stream);
 
@@ -284,7 +302,7 @@ int a8_onebit_decode(const uint8_t* bits, int64_t n, const float* levels, float*
  *   out_s[i] = sum_r (bit_r(i) ? pos_r : neg_r), rank order, float32
  *   (round-to-nearest); op = 1 then divides by float32(nranks).
  * status_out (optional, device uint32): OR of every rank's first nstatus
- * status words.  At most 32 segments per call.                              */
+ * status words.  At most 32 segments per call; bit_off a multiple of 16.   */
 typedef struct a8_ob_seg {
     float* out;
     int64_t n;

@@ -83,6 +83,11 @@ class ProdSeg(C.Structure):
     _fields_ = [("x", C.c_void_p), ("y", C.c_void_p), ("mask", C.c_void_p), ("n", C.c_int64)]
 
 
+class ObQSeg(C.Structure):
+    _fields_ = [("g", C.c_void_p), ("residual", C.c_void_p), ("n", C.c_int64), ("bits", C.c_void_p),
+                ("levels", C.c_void_p), ("status", C.c_void_p)]
+
+
 class ObSeg(C.Structure):
     _fields_ = [("out", C.c_void_p), ("n", C.c_int64), ("bit_off", C.c_int64)]
 
@@ -143,6 +148,8 @@ SIGNATURES = {
         [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
          C.c_size_t, C.c_void_p],
     ),
+    "a8_onebit_multi_workspace_bytes": (C.c_size_t, [C.c_int]),
+    "a8_onebit_quantize_multi": (C.c_int, [C.POINTER(ObQSeg), C.c_int, C.c_int, C.c_void_p, C.c_size_t, C.c_void_p]),
     "a8_onebit_decode": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
     "a8_onebit_reduce": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int,
                                    C.c_int, C.c_void_p, C.c_void_p]),

@@ -57,8 +57,11 @@ __device__ __forceinline__ T block_sum(T v, T* red) {
     return s;  // valid in thread 0
 }
 
-__global__ void __launch_bounds__(kThreads) onebit_stats(const void* g, int f64, const double* res, int64_t n,
-                                                          Partial* part) {
+// One tensor's stats as block j of a G-block grid (the single-tensor launch
+// has j = blockIdx.x, G = gridDim.x; the multi-tensor launch gives each
+// tensor its own range of blocks with the same G, so the sums match).
+__device__ __forceinline__ void stats_body(const void* g, int f64, const double* res, int64_t n, int j, int G,
+                                           Partial* out) {
     __shared__ double rd[kThreads / 32];
     __shared__ unsigned long long ru[kThreads / 32];
     double sp = 0.0, sn = 0.0;
@@ -67,9 +70,9 @@ __global__ void __launch_bounds__(kThreads) onebit_stats(const void* g, int f64,
     // the same per-thread element order (i, i+S, i+2S, ...) as a plain
     // grid-stride loop -- so the sums are bit-identical to it -- with the
     // loads of 4 elements issued before any of them is accumulated
-    constexpr int U = 4;
-    const int64_t S = (int64_t)gridDim.x * kThreads;
-    for (int64_t i0 = (int64_t)blockIdx.x * kThreads + threadIdx.x; i0 < n; i0 += U * S) {
+    constexpr int U = 8;
+    const int64_t S = (int64_t)G * kThreads;
+    for (int64_t i0 = (int64_t)j * kThreads + threadIdx.x; i0 < n; i0 += U * S) {
         double gv[U], rv[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -96,12 +99,18 @@ __global__ void __launch_bounds__(kThreads) onebit_stats(const void* g, int f64,
     const unsigned long long CP = block_sum(cp, ru);
     const unsigned long long CN = block_sum(cn, ru);
     const int B = __syncthreads_or(bad);
-    if (threadIdx.x == 0) part[blockIdx.x] = Partial{SP, SN, CP, CN, (unsigned)B, {0, 0, 0}};
+    if (threadIdx.x == 0) *out = Partial{SP, SN, CP, CN, (unsigned)B, {0, 0, 0}};
 }
 
-__global__ void __launch_bounds__(kThreads) onebit_apply(const void* g, int f64, double* res, int64_t n,
-                                                          const Partial* part, int nparts, uint8_t* bits,
-                                                          float* levels, uint32_t* status) {
+__global__ void __launch_bounds__(kThreads) onebit_stats(const void* g, int f64, const double* res, int64_t n,
+                                                          Partial* part) {
+    stats_body(g, f64, res, n, blockIdx.x, gridDim.x, part + blockIdx.x);
+}
+
+// One tensor's apply as block j of a G-block grid; part = its G partials.
+__device__ __forceinline__ void apply_body(const void* g, int f64, double* res, int64_t n, const Partial* part,
+                                           int nparts, uint8_t* bits, float* levels, uint32_t* status, int j,
+                                           int G) {
     __shared__ double rd[kThreads / 32];
     __shared__ unsigned long long ru[kThreads / 32];
     __shared__ float sLv[2];
@@ -124,7 +133,7 @@ __global__ void __launch_bounds__(kThreads) onebit_apply(const void* g, int f64,
         // codecs.py:327-328: float32 of the float64 mean, 0.0 for an empty side
         sLv[0] = CP ? __double2float_rn(__ddiv_rn(SP, (double)CP)) : 0.0f;
         sLv[1] = CN ? __double2float_rn(__ddiv_rn(SN, (double)CN)) : 0.0f;
-        if (blockIdx.x == 0) {
+        if (j == 0) {
             levels[0] = sLv[0];
             levels[1] = sLv[1];
             *status = B ? A8_STATUS_NONFINITE : 0u;
@@ -140,9 +149,9 @@ __global__ void __launch_bounds__(kThreads) onebit_apply(const void* g, int f64,
     // the ballot gives those 32 sign bits, and lane k keeps them; at the end
     // every lane stores its 4 bytes (128 coalesced bytes of bits per warp)
     const int lane = threadIdx.x & 31;
-    const int64_t warps = (int64_t)gridDim.x * (kThreads / 32);
+    const int64_t warps = (int64_t)G * (kThreads / 32);
     const int64_t nbytes = (n + 7) / 8;
-    for (int64_t wc = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); wc * 1024 < n; wc += warps) {
+    for (int64_t wc = (int64_t)j * (kThreads / 32) + (threadIdx.x >> 5); wc * 1024 < n; wc += warps) {
         const int64_t base = wc * 1024;
         uint32_t mine = 0;
         constexpr int U = 8;  // steps whose loads are issued together
@@ -174,6 +183,40 @@ __global__ void __launch_bounds__(kThreads) onebit_apply(const void* g, int f64,
                 if (b0 + t < nbytes) bits[b0 + t] = (uint8_t)(w >> (8 * t));
         }
     }
+}
+
+__global__ void __launch_bounds__(kThreads) onebit_apply(const void* g, int f64, double* res, int64_t n,
+                                                          const Partial* part, int nparts, uint8_t* bits,
+                                                          float* levels, uint32_t* status) {
+    apply_body(g, f64, res, n, part, nparts, bits, levels, status, blockIdx.x, gridDim.x);
+}
+
+// The multi-tensor launches: tensor s owns blocks [p0[s], p0[s+1]).
+constexpr int kQSegs = 32;
+struct QParams {
+    a8_ob_q_seg_t segs[kQSegs];
+    int p0[kQSegs + 1];
+    int nseg, f64;
+    Partial* part;
+};
+
+__device__ __forceinline__ int qseg_of(const QParams& p, int b) {
+    int s = 0;
+    while (s + 1 < p.nseg && p.p0[s + 1] <= b) ++s;
+    return s;
+}
+
+__global__ void __launch_bounds__(kThreads) onebit_stats_multi(const __grid_constant__ QParams p) {
+    const int s = qseg_of(p, blockIdx.x);
+    const a8_ob_q_seg_t& q = p.segs[s];
+    stats_body(q.g, p.f64, q.residual, q.n, blockIdx.x - p.p0[s], p.p0[s + 1] - p.p0[s], p.part + blockIdx.x);
+}
+
+__global__ void __launch_bounds__(kThreads) onebit_apply_multi(const __grid_constant__ QParams p) {
+    const int s = qseg_of(p, blockIdx.x);
+    const a8_ob_q_seg_t& q = p.segs[s];
+    const int G = p.p0[s + 1] - p.p0[s];
+    apply_body(q.g, p.f64, q.residual, q.n, p.part + p.p0[s], G, q.bits, q.levels, q.status, blockIdx.x - p.p0[s], G);
 }
 
 __global__ void __launch_bounds__(kThreads) onebit_decode_k(const uint8_t* bits, int64_t n, const float* levels,
@@ -213,13 +256,16 @@ __global__ void __launch_bounds__(kThreads) onebit_decode_k(const uint8_t* bits,
 constexpr int kObSegs = 32;
 struct ObParams {
     a8_ob_seg_t segs[kObSegs];
-    int64_t byte_start[kObSegs + 1];  // prefix sums of ceil(n/8)
+    int64_t word_start[kObSegs + 1];  // prefix sums of ceil(ceil(n/8)/4): 4 bytes of bits per thread
     const uint8_t* slabs;
     int64_t rank_stride, levels_off, status_off;
     int nseg, nranks, op, nstatus;
     uint32_t* status_out;
 };
 
+// One thread per 4 bytes of bits (32 elements): one 32-bit load per rank
+// (segments' bits start 16-byte aligned in the slabs and are padded to 16
+// bytes, so the word never leaves the segment's area), 8 float4 stores.
 __global__ void __launch_bounds__(kThreads) onebit_reduce_k(const __grid_constant__ ObParams p) {
     if (p.status_out && blockIdx.x == 0) {
         __shared__ unsigned int sSt;
@@ -232,40 +278,43 @@ __global__ void __launch_bounds__(kThreads) onebit_reduce_k(const __grid_constan
         __syncthreads();
         if (threadIdx.x == 0) *p.status_out = sSt;
     }
-    const int64_t total = p.byte_start[p.nseg];
+    const int64_t total = p.word_start[p.nseg];
     const float invn = 1.0f / (float)p.nranks;
     const bool pow2 = (p.nranks & (p.nranks - 1)) == 0;
     for (int64_t u = (int64_t)blockIdx.x * kThreads + threadIdx.x; u < total; u += (int64_t)gridDim.x * kThreads) {
         int lo = 0, hi = p.nseg;
         while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
-            if (p.byte_start[mid] <= u) lo = mid; else hi = mid;
+            if (p.word_start[mid] <= u) lo = mid; else hi = mid;
         }
         const a8_ob_seg_t sg = p.segs[lo];
-        const int64_t j = u - p.byte_start[lo];
-        float acc[8];
+        const int64_t j = u - p.word_start[lo];
+        float acc[32];
         for (int r = 0; r < p.nranks; ++r) {
             const uint8_t* slab = p.slabs + r * p.rank_stride;
-            const uint32_t b = slab[sg.bit_off + j];
+            const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(slab + sg.bit_off) + j);
             const float* lv = reinterpret_cast<const float*>(slab + p.levels_off) + 2 * lo;
             const float pl = lv[0], nl = lv[1];
 #pragma unroll
-            for (int t = 0; t < 8; ++t) {
-                const float d = (b >> (7 - t)) & 1u ? pl : nl;  // np.packbits order
+            for (int t = 0; t < 32; ++t) {
+                // element 8k + e is bit 7 - e of byte k (np.packbits order)
+                const float d = (w >> (8 * (t >> 3) + 7 - (t & 7))) & 1u ? pl : nl;
                 acc[t] = r == 0 ? d : __fadd_rn(acc[t], d);
             }
         }
         if (p.op == 1) {
 #pragma unroll
-            for (int t = 0; t < 8; ++t) acc[t] = pow2 ? __fmul_rn(acc[t], invn) : __fdiv_rn(acc[t], (float)p.nranks);
+            for (int t = 0; t < 32; ++t) acc[t] = pow2 ? __fmul_rn(acc[t], invn) : __fdiv_rn(acc[t], (float)p.nranks);
         }
-        const int64_t e0 = 8 * j;
-        if (e0 + 8 <= sg.n && (reinterpret_cast<uintptr_t>(sg.out) & 15) == 0) {
+        const int64_t e0 = 32 * j;
+        if (e0 + 32 <= sg.n && (reinterpret_cast<uintptr_t>(sg.out) & 15) == 0) {
             float4* o = reinterpret_cast<float4*>(sg.out + e0);
-            o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-            o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) o[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
         } else {
-            for (int t = 0; t < 8 && e0 + t < sg.n; ++t) sg.out[e0 + t] = acc[t];
+#pragma unroll
+            for (int t = 0; t < 32; ++t)
+                if (e0 + t < sg.n) sg.out[e0 + t] = acc[t];
         }
     }
 }
@@ -311,6 +360,40 @@ extern "C" int a8_onebit_quantize(const void* g, int g_is_f64, double* residual,
     return check("a8_onebit_quantize(apply)");
 }
 
+extern "C" size_t a8_onebit_multi_workspace_bytes(int nseg) {
+    return sizeof(Partial) * (size_t)kMaxGrid * (size_t)std::max(1, std::min(nseg, kQSegs));
+}
+
+extern "C" int a8_onebit_quantize_multi(const a8_ob_q_seg_t* segs, int nseg, int g_is_f64, void* workspace,
+                                        size_t workspace_bytes, void* stream) {
+    if (nseg < 0 || nseg > kQSegs || (nseg > 0 && !segs) || !workspace)
+        return fail(A8_ERR_USAGE, "a8_onebit_quantize_multi: bad argument (at most 32 segments per call)");
+    QParams p{};
+    int b = 0;
+    for (int i = 0; i < nseg; ++i) {
+        const a8_ob_q_seg_t& q = segs[i];
+        if (q.n < 0 || (q.n > 0 && (!q.g || !q.residual || !q.bits)) || !q.levels || !q.status)
+            return fail(A8_ERR_USAGE, "a8_onebit_quantize_multi: bad segment");
+        p.segs[i] = q;
+        p.p0[i] = b;
+        b += grid_for(q.n);  // the single-tensor grid: identical partials and sums
+    }
+    p.p0[nseg] = b;
+    p.nseg = nseg;
+    p.f64 = g_is_f64 ? 1 : 0;
+    p.part = static_cast<Partial*>(workspace);
+    if (nseg == 0) return A8_OK;
+    if (workspace_bytes < sizeof(Partial) * (size_t)b)
+        return fail(A8_ERR_USAGE, "a8_onebit_quantize_multi: workspace too small");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    static std::mutex mu;  // stats -> apply share the partials (see a8_onebit_quantize)
+    std::lock_guard<std::mutex> lk(mu);
+    onebit_stats_multi<<<b, kThreads, 0, st>>>(p);
+    if (int rc = check("a8_onebit_quantize_multi(stats)")) return rc;
+    onebit_apply_multi<<<b, kThreads, 0, st>>>(p);
+    return check("a8_onebit_quantize_multi(apply)");
+}
+
 extern "C" int a8_onebit_decode(const uint8_t* bits, int64_t n, const float* levels, float* out, void* stream) {
     if (n < 0 || (n > 0 && (!bits || !out)) || !levels) return fail(A8_ERR_USAGE, "a8_onebit_decode: bad argument");
     if (n == 0) return A8_OK;
@@ -328,11 +411,12 @@ extern "C" int a8_onebit_reduce(const a8_ob_seg_t* segs, int nseg, const uint8_t
     int64_t acc = 0;
     for (int i = 0; i < nseg; ++i) {
         if (segs[i].n < 0 || (segs[i].n > 0 && !segs[i].out)) return fail(A8_ERR_USAGE, "a8_onebit_reduce: bad segment");
+        if (segs[i].bit_off % 16) return fail(A8_ERR_USAGE, "a8_onebit_reduce: bit_off must be a multiple of 16");
         p.segs[i] = segs[i];
-        p.byte_start[i] = acc;
-        acc += (segs[i].n + 7) / 8;
+        p.word_start[i] = acc;
+        acc += ((segs[i].n + 7) / 8 + 3) / 4;
     }
-    p.byte_start[nseg] = acc;
+    p.word_start[nseg] = acc;
     p.slabs = slabs;
     p.rank_stride = rank_stride;
     p.levels_off = levels_off;

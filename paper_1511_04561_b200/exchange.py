@@ -124,6 +124,27 @@ class CudaSegmentCodec(SegmentCodec):
                                          base + bits_off, base + levels_off, base + status_off, ws.data_ptr(),
                                          ws.numel(), stream))
 
+    def onebit_quantize_many(self, xs, residuals, buf: torch.Tensor, bits_offs, levels_offs, status_offs) -> None:
+        """onebit_quantize of every tensor in two launches per 32 tensors of
+        one dtype (a8_onebit_quantize_multi; bit-identical per tensor)."""
+        dev = buf.device
+        base = buf.data_ptr()
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        groups: dict = {}
+        for i, x in enumerate(xs):
+            groups.setdefault(x.dtype == torch.float64, []).append(i)
+        for f64, idx in groups.items():
+            for c0 in range(0, len(idx), 32):
+                chunk = idx[c0:c0 + 32]
+                segs = (N.ObQSeg * len(chunk))()
+                for k, i in enumerate(chunk):
+                    x = xs[i]
+                    segs[k] = N.ObQSeg(x.data_ptr() if x.numel() else 0, residuals[i].data_ptr() if x.numel() else 0,
+                                       x.numel(), base + bits_offs[i], base + levels_offs[i], base + status_offs[i])
+                ws = _ob_multi_ws(dev, len(chunk))
+                N.check(self._lib.a8_onebit_quantize_multi(segs, len(chunk), 1 if f64 else 0, ws.data_ptr(),
+                                                           ws.numel(), stream))
+
     def onebit_reduce(self, outs, bit_offs, buf: torch.Tensor, rank_stride: int, levels_off: int, status_off: int,
                       nranks: int, op: int, status_out: Optional[torch.Tensor] = None) -> None:
         dev = buf.device
@@ -189,6 +210,17 @@ class CudaSegmentCodec(SegmentCodec):
 
 # ---------------------------------------------------------------------------
 # collectives
+
+
+_ob_multi: dict = {}  # device index -> workspace of a8_onebit_quantize_multi (32 segments)
+
+
+def _ob_multi_ws(dev, nseg: int) -> torch.Tensor:
+    ws = _ob_multi.get(dev.index)
+    if ws is None:
+        ws = _ob_multi[dev.index] = torch.empty(N.lib.a8_onebit_multi_workspace_bytes(32), dtype=torch.uint8,
+                                                device=dev)
+    return ws
 
 
 class TorchDistComm:
@@ -931,9 +963,14 @@ class OneBitExchange(GradientExchange):
         # iff its own input is finite (the kernel leaves it untouched otherwise,
         # codecs.py:317-318); a non-finite input on any rank raises InputError
         # on every rank (the status words travel in the slabs)
-        for i, t in enumerate(tensors):
-            self.codec.onebit_quantize(t.reshape(-1), res[i], buf, mine + offs[i], mine + lev + 8 * i,
-                                       mine + st + 4 * i)
+        many = getattr(self.codec, "onebit_quantize_many", None)
+        if many is not None:  # all tensors in two launches
+            many([t.reshape(-1) for t in tensors], res, buf, [mine + o for o in offs],
+                 [mine + lev + 8 * i for i in range(len(tensors))], [mine + st + 4 * i for i in range(len(tensors))])
+        else:
+            for i, t in enumerate(tensors):
+                self.codec.onebit_quantize(t.reshape(-1), res[i], buf, mine + offs[i], mine + lev + 8 * i,
+                                           mine + st + 4 * i)
         if nranks > 1:
             self.comm.all_gather(buf, buf[mine:mine + P])
         status = self._status_word(dev)

@@ -123,3 +123,30 @@ def test_host_state_numpy_in_numpy_out(cuda):
     with pytest.raises(A.InputError):
         A.onebit_quantize(np.full(3000, np.nan), st)
     assert np.array_equal(st.residual, prev)
+
+
+def test_quantize_multi_bit_identical_to_per_tensor(cuda):
+    """a8_onebit_quantize_multi (the 1-bit exchange's two launches for all
+    tensors) gives each tensor exactly what a8_onebit_quantize gives it
+    alone: bits, levels, status and the updated residual, over 3 chained
+    steps, float32 and float64 inputs, empty and ragged tensors."""
+    from paper_1511_04561_b200.exchange import CudaSegmentCodec, OneBitExchange
+
+    sizes = [0, 1, 7, 8, 1000, 4097, 70001, 1 << 20, 3_000_001]
+    rng = np.random.default_rng(3)
+    codec = CudaSegmentCodec()
+    offs, lev, st, P = OneBitExchange.layout(sizes)
+    for dt in (torch.float32, torch.float64):
+        ra = [torch.zeros(n, dtype=torch.float64, device=cuda) for n in sizes]
+        rb = [torch.zeros(n, dtype=torch.float64, device=cuda) for n in sizes]
+        for step in range(3):
+            xs = [torch.from_numpy(rng.normal(size=n)).to(device=cuda, dtype=dt) for n in sizes]
+            ba = torch.zeros(P, dtype=torch.uint8, device=cuda)
+            bb = torch.zeros(P, dtype=torch.uint8, device=cuda)
+            for i, x in enumerate(xs):
+                codec.onebit_quantize(x, ra[i], ba, offs[i], lev + 8 * i, st + 4 * i)
+            codec.onebit_quantize_many(xs, rb, bb, offs, [lev + 8 * i for i in range(len(sizes))],
+                                       [st + 4 * i for i in range(len(sizes))])
+            assert torch.equal(ba, bb), (dt, step)
+            for a, b in zip(ra, rb):
+                assert torch.equal(a, b), (dt, step)
