@@ -256,16 +256,17 @@ __global__ void __launch_bounds__(kThreads) onebit_decode_k(const uint8_t* bits,
 constexpr int kObSegs = 32;
 struct ObParams {
     a8_ob_seg_t segs[kObSegs];
-    int64_t word_start[kObSegs + 1];  // prefix sums of ceil(ceil(n/8)/4): 4 bytes of bits per thread
+    int64_t unit_start[kObSegs + 1];  // prefix sums of ceil(n / 1024): one warp per 1024 elements
     const uint8_t* slabs;
     int64_t rank_stride, levels_off, status_off;
     int nseg, nranks, op, nstatus;
     uint32_t* status_out;
 };
 
-// One thread per 4 bytes of bits (32 elements): one 32-bit load per rank
-// (segments' bits start 16-byte aligned in the slabs and are padded to 16
-// bytes, so the word never leaves the segment's area), 8 float4 stores.
+// One warp per 1024 elements (128 bytes of bits): lane l loads bit word l
+// of each rank (128 coalesced bytes), then for store q in 0..7 takes, by a
+// shuffle, the word holding float4 number 32 q + l and writes that float4 --
+// every store instruction covers 512 contiguous bytes.
 __global__ void __launch_bounds__(kThreads) onebit_reduce_k(const __grid_constant__ ObParams p) {
     if (p.status_out && blockIdx.x == 0) {
         __shared__ unsigned int sSt;
@@ -278,43 +279,55 @@ __global__ void __launch_bounds__(kThreads) onebit_reduce_k(const __grid_constan
         __syncthreads();
         if (threadIdx.x == 0) *p.status_out = sSt;
     }
-    const int64_t total = p.word_start[p.nseg];
+    const int lane = threadIdx.x & 31;
+    const int64_t total = p.unit_start[p.nseg];
     const float invn = 1.0f / (float)p.nranks;
     const bool pow2 = (p.nranks & (p.nranks - 1)) == 0;
-    for (int64_t u = (int64_t)blockIdx.x * kThreads + threadIdx.x; u < total; u += (int64_t)gridDim.x * kThreads) {
+    const int64_t warps = (int64_t)gridDim.x * (kThreads / 32);
+    for (int64_t u = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); u < total; u += warps) {
         int lo = 0, hi = p.nseg;
         while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
-            if (p.word_start[mid] <= u) lo = mid; else hi = mid;
+            if (p.unit_start[mid] <= u) lo = mid; else hi = mid;
         }
         const a8_ob_seg_t sg = p.segs[lo];
-        const int64_t j = u - p.word_start[lo];
-        float acc[32];
+        const int64_t e_unit = (u - p.unit_start[lo]) * 1024;  // first element of this unit
+        const int64_t nwords = ((sg.n + 7) / 8 + 3) / 4;
+        const int64_t wj = e_unit / 32 + lane;                 // this lane's bit word
+        float acc[8][4];
         for (int r = 0; r < p.nranks; ++r) {
             const uint8_t* slab = p.slabs + r * p.rank_stride;
-            const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(slab + sg.bit_off) + j);
+            const uint32_t w = wj < nwords ? __ldg(reinterpret_cast<const uint32_t*>(slab + sg.bit_off) + wj) : 0u;
             const float* lv = reinterpret_cast<const float*>(slab + p.levels_off) + 2 * lo;
             const float pl = lv[0], nl = lv[1];
 #pragma unroll
-            for (int t = 0; t < 32; ++t) {
-                // element 8k + e is bit 7 - e of byte k (np.packbits order)
-                const float d = (w >> (8 * (t >> 3) + 7 - (t & 7))) & 1u ? pl : nl;
-                acc[t] = r == 0 ? d : __fadd_rn(acc[t], d);
+            for (int q = 0; q < 8; ++q) {
+                // float4 number 32 q + lane = elements 4 (32 q + lane) .. +3: byte (lane & 7) >> 1 of
+                // word 4 q + (lane >> 3), high nibble for even lanes (np.packbits: first element in the MSB)
+                const uint32_t ww = __shfl_sync(0xffffffffu, w, 4 * q + (lane >> 3));
+                const uint32_t nib = (ww >> (8 * ((lane & 7) >> 1) + ((lane & 1) ? 0 : 4))) & 15u;
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const float d = (nib >> (3 - t)) & 1u ? pl : nl;
+                    acc[q][t] = r == 0 ? d : __fadd_rn(acc[q][t], d);
+                }
             }
         }
-        if (p.op == 1) {
 #pragma unroll
-            for (int t = 0; t < 32; ++t) acc[t] = pow2 ? __fmul_rn(acc[t], invn) : __fdiv_rn(acc[t], (float)p.nranks);
-        }
-        const int64_t e0 = 32 * j;
-        if (e0 + 32 <= sg.n && (reinterpret_cast<uintptr_t>(sg.out) & 15) == 0) {
-            float4* o = reinterpret_cast<float4*>(sg.out + e0);
+        for (int q = 0; q < 8; ++q) {
+            if (p.op == 1) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q) o[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
-        } else {
+                for (int t = 0; t < 4; ++t)
+                    acc[q][t] = pow2 ? __fmul_rn(acc[q][t], invn) : __fdiv_rn(acc[q][t], (float)p.nranks);
+            }
+            const int64_t e = e_unit + 4 * (32 * q + lane);
+            if (e + 4 <= sg.n && (reinterpret_cast<uintptr_t>(sg.out) & 15) == 0) {
+                *reinterpret_cast<float4*>(sg.out + e) = make_float4(acc[q][0], acc[q][1], acc[q][2], acc[q][3]);
+            } else {
 #pragma unroll
-            for (int t = 0; t < 32; ++t)
-                if (e0 + t < sg.n) sg.out[e0 + t] = acc[t];
+                for (int t = 0; t < 4; ++t)
+                    if (e + t < sg.n) sg.out[e + t] = acc[q][t];
+            }
         }
     }
 }
@@ -413,10 +426,10 @@ extern "C" int a8_onebit_reduce(const a8_ob_seg_t* segs, int nseg, const uint8_t
         if (segs[i].n < 0 || (segs[i].n > 0 && !segs[i].out)) return fail(A8_ERR_USAGE, "a8_onebit_reduce: bad segment");
         if (segs[i].bit_off % 16) return fail(A8_ERR_USAGE, "a8_onebit_reduce: bit_off must be a multiple of 16");
         p.segs[i] = segs[i];
-        p.word_start[i] = acc;
-        acc += ((segs[i].n + 7) / 8 + 3) / 4;
+        p.unit_start[i] = acc;
+        acc += (segs[i].n + 1023) / 1024;
     }
-    p.word_start[nseg] = acc;
+    p.unit_start[nseg] = acc;
     p.slabs = slabs;
     p.rank_stride = rank_stride;
     p.levels_off = levels_off;
@@ -427,7 +440,7 @@ extern "C" int a8_onebit_reduce(const a8_ob_seg_t* segs, int nseg, const uint8_t
     p.nstatus = nstatus;
     p.status_out = status_out;
     if (acc == 0 && !status_out) return A8_OK;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((acc + kThreads - 1) / kThreads, 148 * 4));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((acc + kThreads / 32 - 1) / (kThreads / 32), 148 * 8));
     onebit_reduce_k<<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(p);
     return check("a8_onebit_reduce");
 }
