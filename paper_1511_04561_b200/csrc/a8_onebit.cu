@@ -70,7 +70,10 @@ __device__ __forceinline__ void stats_body(const void* g, int f64, const double*
     // the same per-thread element order (i, i+S, i+2S, ...) as a plain
     // grid-stride loop -- so the sums are bit-identical to it -- with the
     // loads of 4 elements issued before any of them is accumulated
-    constexpr int U = 8;
+    #ifndef A8_OB_STATS_U
+#define A8_OB_STATS_U 4  // 4 loads in flight: 138 us for the C3 stats; 2: 227, 6: 161, 8: 160, 16: 227
+#endif
+    constexpr int U = A8_OB_STATS_U;
     const int64_t S = (int64_t)G * kThreads;
     for (int64_t i0 = (int64_t)j * kThreads + threadIdx.x; i0 < n; i0 += U * S) {
         double gv[U], rv[U];
