@@ -688,6 +688,10 @@ def run_b200(args, nranks, rank, local_rank):
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
                 "algorithmic_bytes_per_launch": per_launch_bytes,
+                "traffic_note": ("encode: per-tensor absmax is two passes, so the inputs are read twice "
+                                 f"({4.0 * n / 1e6:.0f} MB of re-read beyond the algorithmic 5 B/elem; L2 keeps "
+                                 "little of it, DESIGN.md §3); traffic = ncu dram bytes of one launch "
+                                 "(profiles/ncu_traffic.json, cold L2)") if dom == "encode" else None,
                 "kernel_ms_per_step": kms,
                 "codec_roundtrip_GBps": (alg["encode"] + alg["decode"]) / ((kms["encode"] + kms["decode"]) * 1e-3) / 1e9}
 
