@@ -1663,41 +1663,8 @@ __global__ void __launch_bounds__(kDtCons + 32, 2) decode_tma_kernel(const __gri
         }
         mbar_fence_init();
     }
-    if (tid >= 32) {
-        const int t = tid - 32;
-        const float v = p.book->table[t];
-        float4* d = reinterpret_cast<float4*>(sTab + t * 32);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) d[q] = make_float4(v, v, v, v);
-    }
-    for (int i = tid; i < R * p.nseg; i += blockDim.x) {
-        const int sgi = i / R, r = i % R;
-        const DecSegD& d = segs[sgi];
-        sScale[i] = __ldcg(reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.lay.scales) + p.rank_off[r]) +
-                           (d.flat_off / L) * p.lay.scale_block_stride + d.scale_idx);
-    }
-    if (p.status_out && blockIdx.x == 0) {
-        __shared__ unsigned int sSt;
-        if (tid == 0) sSt = 0u;
-        __syncthreads();
-        for (int i = tid; i < R * p.status_blocks; i += blockDim.x) {
-            const int r = i / p.status_blocks, j = i % p.status_blocks;
-            const unsigned int* w = reinterpret_cast<const unsigned int*>(
-                                        reinterpret_cast<const uint8_t*>(p.lay.scales) + p.rank_off[r]) +
-                                    (int64_t)j * p.lay.scale_block_stride + p.status_idx;
-            atomicOr(&sSt, __ldcg(w));
-        }
-        __syncthreads();
-        if (tid == 0) {
-            if (p.lay.flags & A8_LAYOUT_STATUS_COUNT) {
-                volatile unsigned int* w = p.status_out;
-                if (sSt) *w = *w + 1u;
-            } else {
-                *p.status_out = sSt;
-            }
-        }
-    }
-    __syncthreads();
+    __syncthreads();  // the ring barriers are initialised: the producer starts at once, the
+                      // consumers' prologue (tables, scales, status) overlaps its first loads
     auto seg_of = [&](int64_t c) {
         int lo = 0, hi = p.nseg;
         while (hi - lo > 1) {
@@ -1738,6 +1705,40 @@ __global__ void __launch_bounds__(kDtCons + 32, 2) decode_tma_kernel(const __gri
         return;
     }
     const int ct = tid - 32;
+    {
+        const float v = p.book->table[ct];
+        float4* d = reinterpret_cast<float4*>(sTab + ct * 32);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) d[q] = make_float4(v, v, v, v);
+    }
+    for (int i = ct; i < R * p.nseg; i += kDtCons) {
+        const int sgi = i / R, r = i % R;
+        const DecSegD& d = segs[sgi];
+        sScale[i] = __ldcg(reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.lay.scales) + p.rank_off[r]) +
+                           (d.flat_off / L) * p.lay.scale_block_stride + d.scale_idx);
+    }
+    if (p.status_out && blockIdx.x == 0) {
+        __shared__ unsigned int sSt;
+        if (ct == 0) sSt = 0u;
+        nbar_sync(2, kDtCons);
+        for (int i = ct; i < R * p.status_blocks; i += kDtCons) {
+            const int r = i / p.status_blocks, j = i % p.status_blocks;
+            const unsigned int* w = reinterpret_cast<const unsigned int*>(
+                                        reinterpret_cast<const uint8_t*>(p.lay.scales) + p.rank_off[r]) +
+                                    (int64_t)j * p.lay.scale_block_stride + p.status_idx;
+            atomicOr(&sSt, __ldcg(w));
+        }
+        nbar_sync(2, kDtCons);
+        if (ct == 0) {
+            if (p.lay.flags & A8_LAYOUT_STATUS_COUNT) {
+                volatile unsigned int* w = p.status_out;
+                if (sSt) *w = *w + 1u;
+            } else {
+                *p.status_out = sSt;
+            }
+        }
+    }
+    nbar_sync(2, kDtCons);  // tables and scales complete
     const float* tl = sTab + lane;
     const float invN = 1.0f / (float)R;
     const bool pow2 = (R & (R - 1)) == 0;
