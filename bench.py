@@ -550,7 +550,7 @@ def codec_sweep(A, torch, dev, clk_sampler_cls):
         out["c1"] = [case(1 << 20, lab) for lab in ("dynamic-tree/absmax", "linear/absmax", "static-tree/decade+1",
                                                     "mantissa/decade+1")]
         out["c4"] = [case(1 << k, lab) for k in (28, 30) for lab in ("dynamic-tree/absmax", "mantissa/decade+1")]
-        out["blocked"] = [case(1 << 30, "dynamic-tree/absmax", b) for b in (4096, 1024)]
+        out["blocked"] = [case(1 << k, "dynamic-tree/absmax", b) for k in (28, 30) for b in (4096, 1024)]
         out["premax"] = {"c4": [premax_c4(1 << k) for k in (28, 30)], "c3": premax_c3()}
         out["onebit_c3"] = onebit_c3()
     out["clocks"] = clk.summary()

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <string>
@@ -371,6 +372,104 @@ __global__ void __launch_bounds__(kThreads) blocked_decode_kernel(const uint8_t*
     }
 }
 
+// Per-block decode of full 4096-element chunks, staged like the exchange's
+// decode_tma_kernel: a producer lane bulk-copies each chunk's 4 KB of codes
+// into a 3-stage ring; 8 consumer warps decode (the 256-entry table
+// replicated per lane, one scale per block of the chunk) into a 16 KB
+// output buffer that one thread bulk-stores (3 buffers in flight).
+constexpr int kDbStages = 3, kDbOut = 3;
+constexpr size_t kDbDynSmem = 256u * 32u * sizeof(float) + (size_t)kDbStages * kBChunk +
+                              (size_t)kDbOut * kBChunk * sizeof(float);
+
+template <int V>  // B = 1024 * V; NB = 4 / V blocks per chunk
+__global__ void __launch_bounds__(kBCons + 32, 2) blocked_decode_stream(const uint8_t* __restrict__ codes,
+                                                                       int64_t nchunks,
+                                                                       const float* __restrict__ scales,
+                                                                       const a8_book_t* book, float* out) {
+    constexpr int NB = 4 / V;
+    extern __shared__ __align__(128) float sDyn[];
+    float* const sTab = sDyn;                                                       // [256][32]
+    uint8_t* const sCodes = reinterpret_cast<uint8_t*>(sDyn + 256 * 32);           // [stage][4096]
+    float* const sOut = reinterpret_cast<float*>(sCodes + (size_t)kDbStages * kBChunk);  // [3][4096]
+    __shared__ __align__(8) uint64_t sFull[kDbStages];
+    __shared__ __align__(8) uint64_t sEmpty[kDbStages];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int i = 0; i < kDbStages; ++i) {
+            mbar_init(&sFull[i], 1);
+            mbar_init(&sEmpty[i], kBWarps);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const int64_t nmy = nchunks > blockIdx.x ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const uint32_t full0 = smem_addr(&sFull[0]), empty0 = smem_addr(&sEmpty[0]);
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint64_t drop = policy_evict_first();
+            int st = 0;
+            uint32_t ph = 0;
+            for (int64_t k = 0; k < nmy; ++k) {
+                const int64_t c = blockIdx.x + k * gridDim.x;
+                mbar_wait_a(empty0 + 8u * st, ph ^ 1u);
+                mbar_arrive_expect_tx(&sFull[st], kBChunk);
+                bulk_g2s(sCodes + (size_t)st * kBChunk, codes + c * kBChunk, kBChunk, &sFull[st], drop);
+                if (++st == kDbStages) {
+                    st = 0;
+                    ph ^= 1u;
+                }
+            }
+        }
+        return;
+    }
+    const int ct = tid - 32;
+    {
+        const float v = book->table[ct];
+        float4* d = reinterpret_cast<float4*>(sTab + ct * 32);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) d[q] = make_float4(v, v, v, v);
+    }
+    nbar_sync(2, kBCons);
+    const float* tl = sTab + lane;
+    const uint64_t wpol = policy_evict_first();
+    int st = 0, ob = 0;
+    uint32_t ph = 0;
+    for (int64_t k = 0; k < nmy; ++k) {
+        const int64_t c = blockIdx.x + k * gridDim.x;
+        float sc[NB];
+#pragma unroll
+        for (int j = 0; j < NB; ++j) sc[j] = __ldg(scales + c * NB + j);  // issued before the wait
+        mbar_wait_a(full0 + 8u * st, ph);
+        const uint8_t* cs = sCodes + (size_t)st * kBChunk;
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) w[q] = *reinterpret_cast<const uint32_t*>(cs + q * 1024 + ct * 4);
+        __syncwarp();
+        if (lane == 0) mbar_arrive_a(empty0 + 8u * st);  // this warp is done with the codes
+        float* o = sOut + (size_t)ob * kBChunk;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float s = sc[q / V];  // element q * 1024 + 4 ct + t lies in block q / V (codecs.py:281)
+            reinterpret_cast<float4*>(o)[q * kBCons + ct] =
+                make_float4(__fmul_rn(tl[(w[q] & 255u) * 32u], s), __fmul_rn(tl[((w[q] >> 8) & 255u) * 32u], s),
+                            __fmul_rn(tl[((w[q] >> 16) & 255u) * 32u], s), __fmul_rn(tl[(w[q] >> 24) * 32u], s));
+        }
+        fence_proxy_async_smem();
+        nbar_sync(1, kBCons);
+        if (ct == 0) {
+            bulk_s2g(out + c * kBChunk, o, kBChunk * 4u, wpol);
+            bulk_commit();
+            bulk_wait_read<kDbOut - 2>();  // the buffer of the next chunk (used 2 stores ago) is free
+        }
+        if (++st == kDbStages) {
+            st = 0;
+            ph ^= 1u;
+        }
+        if (++ob == kDbOut) ob = 0;
+    }
+    if (ct == 0) bulk_wait_all();
+}
+
 int grid_for(int64_t nblk, int per_sm) {
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
@@ -442,9 +541,42 @@ extern "C" int a8_decode_blocked(const uint8_t* codes, int64_t n, int64_t block,
         return fail(A8_ERR_USAGE, "a8_decode_blocked: block must be 1024, 2048 or 4096");
     if (reinterpret_cast<uintptr_t>(codes) & 3) return fail(A8_ERR_USAGE, "a8_decode_blocked: codes must be 4-byte aligned");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const a8_book_t* book = static_cast<const a8_book_t*>(book_dev);
+    // full chunks of 16-byte aligned codes and output, B >= 2048: the staged
+    // kernel (2^30: B = 4096 1026 -> 907 us, 2048 1012 -> 920 us; for
+    // B = 1024 the register kernel stays ahead, 985 vs 1022 us)
+    static const bool tma = [] {
+        const char* e = getenv("A8_BLK_DEC_TMA");
+        return !(e && e[0] == '0');
+    }();
+    const int64_t nchunks = (!tma || block < 2048 ||
+                             ((reinterpret_cast<uintptr_t>(codes) | reinterpret_cast<uintptr_t>(out)) & 15))
+                                ? 0 : n / kBChunk;
+    if (nchunks > 0) {
+        static int sms = 0;
+        if (!sms) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaFuncSetAttribute(blocked_decode_stream<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDbDynSmem);
+            cudaFuncSetAttribute(blocked_decode_stream<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDbDynSmem);
+            cudaFuncSetAttribute(blocked_decode_stream<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDbDynSmem);
+        }
+        const int g = (int)std::min<int64_t>(nchunks, (int64_t)sms * 2);
+        if (block == 1024)
+            blocked_decode_stream<1><<<g, kBCons + 32, kDbDynSmem, st>>>(codes, nchunks, scales, book, out);
+        else if (block == 2048)
+            blocked_decode_stream<2><<<g, kBCons + 32, kDbDynSmem, st>>>(codes, nchunks, scales, book, out);
+        else
+            blocked_decode_stream<4><<<g, kBCons + 32, kDbDynSmem, st>>>(codes, nchunks, scales, book, out);
+        const int64_t done = nchunks * kBChunk;
+        codes += done;
+        n -= done;
+        out += done;
+        scales += done / block;
+    }
     const int64_t nblk = (n + block - 1) / block;
     if (nblk > 0) {
-        const a8_book_t* book = static_cast<const a8_book_t*>(book_dev);
         const int g = grid_for(nblk, 8);
         if (block == 1024)
             blocked_decode_kernel<1><<<g, kThreads, 0, st>>>(codes, n, scales, book, out);

@@ -9,5 +9,5 @@ class Nop:
     def summary(self): return {}
 dev = torch.device("cuda", 0)
 r = bench.codec_sweep(A, torch, dev, Nop)
-print(json.dumps(r["onebit_c3"], indent=1)); print(json.dumps(r["premax"]["c3"]))
+for x in r["blocked"]: print(x["n"], x["block"], round(x["encode_ms"]*1e3,1), round(x["decode_ms"]*1e3,1), round(x["roundtrip_frac"],3))
 PY
