@@ -155,3 +155,27 @@ def test_guess_verify_restated_matches_reference(kind):
         p = c + ((x.view(np.uint32) & 0x7FFFFFFF) >= Tp[c])
         code = (p | np.where((x < 0) & (p != 0), 0x80, 0)).astype(np.uint8)
         assert np.array_equal(code, ref), trial
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("block", [2048, 4096])
+def test_blocked_decode_staged_kernel_edges(cuda, block):
+    """The staged per-block decode (full 4096-element chunks, aligned) plus
+    the register kernel for the ragged tail and for unaligned outputs."""
+    n = 4096 * 37 + 1234
+    x = torch.randn(n, device=cuda) * 1e-2
+    cb = A.build_codebook(A.DataTypeSpec("dynamic-tree", "absmax"))
+    q = A.encode_buffer(x, cb, block_size=block)
+    y = A.decode_buffer(q, cb)
+    codes = q.codes_device.cpu().numpy()
+    scales = q.block_scales.cpu().numpy()
+    ref = np.empty(n, dtype=np.float32)
+    tab = np.asarray(O.book("dynamic-tree").table, dtype=np.float32)
+    for j in range(len(scales)):
+        sl = slice(j * block, min(n, (j + 1) * block))
+        ref[sl] = (tab[codes[sl]] * np.float32(scales[j])).astype(np.float32)
+    assert y.cpu().numpy().tobytes() == ref.tobytes()
+    buf = torch.empty(n + 1, device=cuda)  # an output 4 bytes off 16-byte alignment
+    out = buf[1:]
+    A.decode_buffer(q, cb, out=out)
+    assert out.cpu().numpy().tobytes() == ref.tobytes()

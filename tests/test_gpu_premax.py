@@ -212,3 +212,20 @@ def test_peer_exchange_premax_matches_oracle(cuda, mode):
         for r in range(3):
             for a, b in zip(res[r][step], want):
                 assert a.tobytes() == b.astype(np.float32).tobytes(), (r, step)
+
+
+def test_premax_many_segments(cuda):
+    """More tensors than the launch-inline plan (32) and the shared-memory
+    maxima (64): the plan and the maxima go through global memory."""
+    sizes = [(7 * i * i + 3) % 20000 + 1 for i in range(70)] + [300_000, 4096 * 3]
+    xs = [g.to(cuda) for g in grads(sizes, seed=11)]
+    want = [x.clone() for x in xs]
+    A.GradientExchange(SPEC, check="sync")(want)
+    got = [x.clone() for x in xs]
+    A.GradientExchange(SPEC, check="sync")(got, amax=A.scale_absmax_(got, 1.0))
+    for a, b in zip(got, want):
+        assert torch.equal(a, b)
+    bad = A.scale_absmax_(got, 1.0)
+    bad[69] = bad[69] * 0.5
+    with pytest.raises(A.UsageError):
+        A.GradientExchange(SPEC, check="sync")([x.clone() for x in xs], amax=bad)
