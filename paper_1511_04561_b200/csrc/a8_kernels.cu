@@ -1394,360 +1394,6 @@ __global__ void __launch_bounds__(kRThreads, 1) resident_encode_kernel(const __g
 }
 
 // ---------------------------------------------------------------------------
-// K1+K2+K3 "grid-barrier" two-pass encode: absmax calls larger than the
-// resident kernel's shared-memory capacity (config 3: 244 MB of gradients).
-//
-// The ticket kernel overlaps the per-segment table dependency with other
-// segments' work, but its E pass re-reads each chunk ~100 MB of traffic after
-// the A pass read it, so the re-read comes from DRAM (9 B/element).  Here one
-// CTA per SM owns a static, contiguous range of the call's chunks: it streams
-// them once for the max (A pass), keeping its last kGbKeep chunks in shared
-// memory and the kGbL2 chunks before those in L2 (evict_last); one grid
-// barrier makes every segment's max final; each CTA then builds the tables of
-// the segments in its range and encodes its chunks in REVERSE order -- the
-// shared-memory chunks first (no reads), then the L2-resident ones, then the
-// rest.  The E pass's first ring loads are issued before the barrier.
-#ifndef A8_GB_CONS
-#define A8_GB_CONS 256
-#endif
-constexpr int kGbCons = A8_GB_CONS;               // consumer threads (8 warps)
-constexpr int kGbMinB = kGbCons >= 512 ? 1 : 2;   // CTAs per SM
-constexpr int kGbThreads = kGbCons + 32;           // + producer warp
-#ifndef A8_GB_RING
-#define A8_GB_RING 4
-#endif
-constexpr int kGbRing = A8_GB_RING;                // streaming stages
-#ifndef A8_GB_KEEP
-#define A8_GB_KEEP 1
-#endif
-constexpr int kGbKeep = A8_GB_KEEP;                // chunks kept in shared memory across the barrier
-constexpr int kGbMaxCtas = 320;
-constexpr int kGbBarC = 2;                         // named barrier of the consumer warps
-constexpr int kGbClaim = 4;                        // own E chunks per claim
-constexpr int kGbReach = 4;                        // right neighbours a CTA may take chunks from
-constexpr size_t kGbDynSmem = (size_t)(kGbRing + kGbKeep) * kChunk * sizeof(float) + (size_t)kLutMax * 4;
-
-struct GbSeg {
-    const float* x;
-    int64_t n;
-    int64_t flat_off;
-    int64_t cstart;  // first chunk of the segment in the call's chunk list
-    int32_t scale_idx;
-    int32_t pad;
-};
-
-struct GbParams {
-    a8_layout_t lay;  // one block (codes at flat_off + i)
-    const a8_book_t* book;
-    WsHead* head;
-    SegCtl* ctl;
-    const unsigned int* status_in;
-    unsigned int* status_out;
-    int nseg;
-    int l2keep;  // ring chunks per CTA read with evict_last (re-read first by the E pass)
-    unsigned long long* steal;  // per CTA: E-pass claims, owner count << 32 | thieves' count
-    GbSeg segs[kInlineSegs + 1];  // segs[nseg].cstart = total chunks
-    int32_t cta_c0[kGbMaxCtas + 1];  // chunk range of CTA b: [cta_c0[b], cta_c0[b + 1])
-};
-
-#ifdef A8_TICKET_TRACE
-__device__ unsigned long long g_gb_trace[kGbMaxCtas][6];  // start, A done, barrier left, first table, end, chunks
-#define GB_STAMP(i)                                                  \
-    do {                                                             \
-        if (ctid == 0) g_gb_trace[blockIdx.x][i] = gtime();          \
-    } while (0)
-#else
-#define GB_STAMP(i) \
-    do {            \
-    } while (0)
-#endif
-
-__global__ void __launch_bounds__(kGbThreads, kGbMinB) gb_encode_kernel(const __grid_constant__ GbParams p) {
-    extern __shared__ __align__(128) float sSlot[];  // [kGbRing + kGbKeep][kChunk], then the bucket table
-    uint32_t* const sE = reinterpret_cast<uint32_t*>(sSlot + (size_t)(kGbRing + kGbKeep) * kChunk);
-    __shared__ uint32_t sT[128];
-    __shared__ uint8_t sCanon[128];
-    __shared__ unsigned int sRed[2][kGbCons / 32];
-    __shared__ __align__(8) uint64_t sFull[kGbRing];
-    __shared__ __align__(8) uint64_t sEmpty[kGbRing];
-    __shared__ __align__(8) uint64_t sKeep[kGbKeep > 0 ? kGbKeep : 1];
-    __shared__ int sFinal;
-    __shared__ int64_t sMc[kGbRing];  // chunk of each ring stage in the E pass (-1: end)
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t c_lo = p.cta_c0[blockIdx.x], c_hi = p.cta_c0[blockIdx.x + 1];
-    const int64_t nloc = c_hi - c_lo;
-    const int64_t nkeep = min((int64_t)kGbKeep, nloc);
-    const int64_t nring = nloc - nkeep;  // chunks j < nring go through the ring, j >= nring stay
-    if (tid == 0) {
-        for (int s = 0; s < kGbRing; ++s) {
-            mbar_init(&sFull[s], 1);
-            mbar_init(&sEmpty[s], kGbCons / 32);
-        }
-        for (int s = 0; s < kGbKeep; ++s) mbar_init(&sKeep[s], 1);
-        mbar_fence_init();
-    }
-    if (tid >= 32 && tid < 32 + 128) sCanon[tid - 32] = p.book->codes[tid - 32];
-    if (tid == 0) p.steal[blockIdx.x] = 0ull;  // ordered before any claim by the grid barrier
-    __syncthreads();
-
-    // chunk c of the call -> segment (c only moves by one per step: walk)
-    auto seg_step = [&](int s, int64_t c) {
-        while (c >= p.segs[s + 1].cstart) ++s;
-        while (c < p.segs[s].cstart) --s;
-        return s;
-    };
-    int s0 = 0;
-    if (nloc > 0) {
-        while (c_lo >= p.segs[s0 + 1].cstart) ++s0;
-    }
-
-    if (warp == 0) {
-        // ===================== producer =====================
-        if (lane == 0) {
-            const uint64_t first = policy_evict_first(), last = policy_evict_last();
-            int s = s0;
-            int64_t it = 0;
-            auto load = [&](int64_t c, uint64_t* bar, float* dst, uint64_t pol) {
-                s = seg_step(s, c);
-                const GbSeg& g = p.segs[s];
-                const int64_t base = (c - g.cstart) * kChunk;
-                const uint32_t bytes = (uint32_t)min((int64_t)kChunk, g.n - base) * 4u;
-                mbar_arrive_expect_tx(bar, bytes);
-                bulk_g2s(dst, g.x + base, bytes, bar, pol);
-            };
-            auto ring = [&](int64_t c, uint64_t pol) {  // c < 0: end of the E pass
-                const int st = (int)(it % kGbRing);
-                mbar_wait(&sEmpty[st], (uint32_t)(((it / kGbRing) & 1) ^ 1));
-                sMc[st] = c;
-                if (c >= 0)
-                    load(c, &sFull[st], sSlot + (size_t)st * kChunk, pol);
-                else
-                    mbar_arrive(&sFull[st]);
-                ++it;
-            };
-            for (int64_t j = 0; j < nloc; ++j) {  // A pass
-                if (j < nring) {
-                    ring(c_lo + j, j >= nring - p.l2keep ? last : first);
-                } else {
-                    const int k = (int)(j - nring);
-                    load(c_lo + j, &sKeep[k], sSlot + (size_t)(kGbRing + k) * kChunk, first);
-                }
-            }
-            // E pass re-reads, most recent first.  The ring chunks are claimed
-            // from the top of this CTA's steal word (kGbClaim at a time, two
-            // requests in flight); a CTA out of work takes chunks from the
-            // bottom of other CTAs' ranges (their L2-cold chunks).  A claim is valid iff
-            // the word's two counts were below the range's ring chunks.
-            unsigned long long* const W = p.steal + blockIdx.x;
-            constexpr unsigned long long kTop = 1ull << 32;
-            unsigned long long r0 = atomicAdd(W, kGbClaim * kTop), r1 = atomicAdd(W, kGbClaim * kTop);
-            for (;;) {
-                const int64_t own = (int64_t)(r0 >> 32), thf = (int64_t)(r0 & 0xffffffffu);
-                const int64_t avail = nring - own - thf;
-                if (avail <= 0) break;
-                r0 = r1;
-                r1 = atomicAdd(W, kGbClaim * kTop);
-                for (int64_t q = 0; q < min((int64_t)kGbClaim, avail); ++q) ring(c_lo + nring - 1 - own - q, first);
-            }
-            // victims: the CTAs G/2 on, which share SMs with the first half
-            // and finish later (the SM's warp scheduler favours the older CTA)
-            for (int k = 0; k < kGbReach; ++k) {
-                const int v = (int)((blockIdx.x + gridDim.x / 2 + k) % gridDim.x);
-                if (v == (int)blockIdx.x) continue;
-                const int64_t vlo = p.cta_c0[v], vn = p.cta_c0[v + 1] - vlo;
-                const int64_t vring = vn - min((int64_t)kGbKeep, vn);
-                for (;;) {
-                    const unsigned long long r = atomicAdd(p.steal + v, 1ull);
-                    const int64_t thf = (int64_t)(r & 0xffffffffu);
-                    if ((int64_t)(r >> 32) + thf >= vring) break;
-                    ring(vlo + thf, first);
-                }
-            }
-            ring(-1, first);
-        }
-        return;  // the producer warp takes no part in the consumers' barriers
-    }
-
-    // ===================== consumers =====================
-    const int ctid = tid - 32, cw = warp - 1;
-    int64_t it = 0;
-    GB_STAMP(0);
-#ifdef A8_TICKET_TRACE
-    if (ctid == 0) g_gb_trace[blockIdx.x][5] = (unsigned long long)nloc;
-#endif
-    // ---- A pass: per-segment max |x| of this CTA's range ----
-    {
-        int s = s0, fpar = 0;
-        unsigned int amx = 0;  // bits * 2 (drops the sign)
-        auto flush = [&](int seg) {
-            const unsigned int wm = __reduce_max_sync(0xffffffffu, amx) >> 1;
-            if (lane == 0) sRed[fpar][cw] = wm;
-            nbar_sync(kGbBarC, kGbCons);
-            if (ctid == 0) {
-                unsigned int m = 0;
-#pragma unroll
-                for (int w = 0; w < kGbCons / 32; ++w) m = max(m, sRed[fpar][w]);
-                if (m) red_max_u32(&p.ctl[seg].amax, m);
-            }
-            fpar ^= 1;
-            amx = 0;
-        };
-        for (int64_t j = 0; j < nloc; ++j) {
-            const int64_t c = c_lo + j;
-            const int sn = seg_step(s, c);
-            if (sn != s) {
-                flush(s);
-                s = sn;
-            }
-            const GbSeg& g = p.segs[s];
-            const int cnt = (int)min((int64_t)kChunk, g.n - (c - g.cstart) * kChunk);
-            const float* stage;
-            int st = -1;
-            if (j < nring) {
-                st = (int)(it % kGbRing);
-                mbar_wait(&sFull[st], (uint32_t)((it / kGbRing) & 1));
-                stage = sSlot + (size_t)st * kChunk;
-                ++it;
-            } else {
-                const int k = (int)(j - nring);
-                mbar_wait(&sKeep[k], 0u);
-                stage = sSlot + (size_t)(kGbRing + k) * kChunk;
-            }
-            const uint4* in = reinterpret_cast<const uint4*>(stage);
-            if (cnt == kChunk) {
-#pragma unroll
-                for (int q = 0; q < kChunk / (kGbCons * 4); ++q) {
-                    const uint4 v = in[q * kGbCons + ctid];
-                    amx = __vimax3_u32(amx, v.x * 2u, v.y * 2u);
-                    amx = __vimax3_u32(amx, v.z * 2u, v.w * 2u);
-                }
-            } else {
-                for (int i = ctid; 4 * i < cnt; i += kGbCons) {
-                    const uint4 v = in[i];
-                    amx = __vimax3_u32(amx, v.x * 2u, v.y * 2u);
-                    amx = __vimax3_u32(amx, v.z * 2u, v.w * 2u);
-                }
-            }
-            if (st >= 0) {
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&sEmpty[st]);
-            }
-        }
-        if (nloc > 0) flush(s);
-    }
-
-    // ---- grid barrier: every segment's max is final (cooperative launch) ----
-    nbar_sync(kGbBarC, kGbCons);
-    GB_STAMP(1);
-    if (ctid == 0) {
-        __threadfence();
-        atomicAdd(&p.head->ticket, 1u);
-        unsigned int ns = 32;
-        while (ld_acquire(&p.head->ticket) < gridDim.x) {
-            __nanosleep(ns);
-            ns = min(ns * 2u, 256u);
-        }
-    }
-    nbar_sync(kGbBarC, kGbCons);
-    GB_STAMP(2);
-
-    // ---- E pass: the kept chunks, then the ring's (own re-reads, steals) ----
-    {
-        int s = -1;
-        int valid = 0;
-        int32_t kb = 0;
-        uint32_t emin = 0, eb = 0;
-        unsigned int amax = 0;
-        float scale = 1.0f;
-        auto encode_chunk = [&](int64_t c, const float* stage) {
-            const int sn = seg_step(s < 0 ? s0 : s, c);
-            if (sn != s) {
-                s = sn;
-                // K2: thresholds and, for segments of 3+ chunks, the carry
-                // bucket table; shorter ones search the thresholds
-                amax = __ldcg(&p.ctl[s].amax);
-                scale = amax == 0u ? 1.0f : __uint_as_float(amax);
-                nbar_sync(kGbBarC, kGbCons);  // everyone is done with the previous table
-                if (kGbCons >= 512) {
-                    threshold_parallel(scale, p.book, sT, ctid);
-                } else if (ctid < 128) {
-                    uint32_t t = kInfBits;
-                    if (scale_ok(scale) && ctid + 1 < p.book->ndistinct)
-                        t = threshold_fast((double)scale, p.book->values[ctid], p.book->values[ctid + 1]);
-                    sT[ctid] = t;
-                }
-                const int nf = nbar_popc(kGbBarC, kGbCons, ctid < 127 && sT[ctid] < kInfBits);
-                uint32_t len;
-                lut_geometry(sT, (uint32_t)nf, &kb, &len);
-                len = max((int32_t)len, (int32_t)(amax >> kKeyShift) - kb + 1);
-                bool ok = p.segs[s + 1].cstart - p.segs[s].cstart >= 3 && amax < kInfBits && len <= (uint32_t)kLutMax;
-                if (ok && ctid < kLutMax / 16) ok = fill_lut_carry(sT, (uint32_t)nf, kb, len, sE, ctid);
-                valid = nbar_and(kGbBarC, kGbCons, ok);
-                emin = smem_addr(sE);
-                eb = emin - (uint32_t)kb * 4u;
-                GB_STAMP(3);
-            }
-            const GbSeg& g = p.segs[s];
-            const int64_t base = (c - g.cstart) * kChunk;
-            const int cnt = (int)min((int64_t)kChunk, g.n - base);
-            if (base == 0) {  // chunk 0 of the segment: its scale and status
-                if (ctid < p.lay.scale_reps) p.lay.scales[ctid * p.lay.scale_block_stride + g.scale_idx] = scale;
-                if (ctid == 0 && amax >= kInfBits) atomicOr(&p.head->status, A8_STATUS_NONFINITE);
-            }
-            const uint4* in = reinterpret_cast<const uint4*>(stage);
-            uint32_t* out = reinterpret_cast<uint32_t*>(p.lay.codes + g.flat_off + base);
-            if (valid && cnt == kChunk) {
-#pragma unroll
-                for (int q = 0; q < kChunk / (kGbCons * 4); ++q)
-                    out[q * kGbCons + ctid] = encode4_carry(in[q * kGbCons + ctid], eb, (int32_t)emin);
-            } else if (valid) {
-                for (int i = ctid; 4 * i < cnt; i += kGbCons) out[i] = encode4_carry(in[i], eb, (int32_t)emin);
-            } else {
-                for (int i = ctid; 4 * i < cnt; i += kGbCons) out[i] = encode4_search(in[i], sT, sCanon);
-            }
-        };
-        for (int64_t j = nloc - 1; j >= nring; --j) encode_chunk(c_lo + j, sSlot + (size_t)(kGbRing + (j - nring)) * kChunk);
-        for (int64_t kit = it;; ++kit) {  // kit: ring iteration (the A pass used `it` of them)
-            const int st = (int)(kit % kGbRing);
-            mbar_wait(&sFull[st], (uint32_t)((kit / kGbRing) & 1));
-            const int64_t c = sMc[st];
-            if (c < 0) break;
-            encode_chunk(c, sSlot + (size_t)st * kChunk);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sEmpty[st]);
-        }
-    }
-
-    // ---- last CTA out: empty segments' scales, status, zeroed workspace ----
-    nbar_sync(kGbBarC, kGbCons);
-    GB_STAMP(4);
-    if (ctid == 0) {
-        __threadfence();
-        sFinal = atomicAdd(&p.head->ctas_done, 1u) == gridDim.x - 1;
-    }
-    nbar_sync(kGbBarC, kGbCons);
-    if (sFinal) {
-        __threadfence();
-        for (int e = 0; e < p.nseg; ++e)  // scale of an empty buffer (codecs.py:257-258)
-            if (p.segs[e].n == 0 && ctid < p.lay.scale_reps)
-                p.lay.scales[ctid * p.lay.scale_block_stride + p.segs[e].scale_idx] = 1.0f;
-        for (int i = ctid; i < p.nseg; i += kGbCons) p.ctl[i].amax = 0u;
-        nbar_sync(kGbBarC, kGbCons);
-        if (ctid < p.lay.scale_reps) {
-            const unsigned int stt = atomicAdd(&p.head->status, 0u) | (p.status_in ? *p.status_in : 0u);
-            p.status_out[(int64_t)ctid * p.lay.scale_block_stride] = stt;
-        }
-        nbar_sync(kGbBarC, kGbCons);
-        if (ctid == 0) {
-            p.head->ticket = 0u;
-            p.head->ctas_done = 0u;
-            p.head->status = 0u;
-        }
-        __threadfence();
-    }
-}
-
-// ---------------------------------------------------------------------------
 // K4/K5: decode (+ rank-ordered sum, + 1/N average).
 //
 // Per segment, each CTA keeps pre-scaled tables fl(table[c] * s_r) for every
@@ -2171,7 +1817,6 @@ struct DevInfo {
     int enc_occ = 0;
     int dec_occ = 0;
     int res_occ = 0;  // resident encode: CTAs per SM (1, or 0 if it cannot run)
-    int gb_occ = 0;   // grid-barrier encode: CTAs per SM (1, or 0)
 };
 
 static std::mutex g_mu;
@@ -2203,10 +1848,6 @@ static int dev_info(int device, DevInfo* out) {
         e = cudaFuncSetAttribute(resident_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRDynSmem);
         if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.res_occ, resident_encode_kernel, kRThreads, kRDynSmem);
-        if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
-        e = cudaFuncSetAttribute(gb_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGbDynSmem);
-        if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.gb_occ, gb_encode_kernel, kGbThreads, kGbDynSmem);
         if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
         d.enc_occ = std::max(1, d.enc_occ);
         d.dec_occ = std::max(1, d.dec_occ);
@@ -2424,10 +2065,6 @@ extern "C" int a8_debug_ticket_trace(uint64_t* out, int64_t n) {
     cudaError_t e = cudaMemcpyFromSymbol(out, a8::g_ticket_trace, sizeof(uint64_t) * 5 * n);
     return e == cudaSuccess ? A8_OK : fail(A8_ERR_CUDA, cudaGetErrorString(e));
 }
-extern "C" int a8_debug_gb_trace(uint64_t* out) {  // [kGbMaxCtas][6]
-    cudaError_t e = cudaMemcpyFromSymbol(out, a8::g_gb_trace, sizeof(a8::g_gb_trace));
-    return e == cudaSuccess ? A8_OK : fail(A8_ERR_CUDA, cudaGetErrorString(e));
-}
 extern "C" int a8_debug_res_trace(uint64_t* out) {  // [2][8]
     cudaError_t e = cudaMemcpyFromSymbol(out, a8::g_res_trace, sizeof(a8::g_res_trace));
     return e == cudaSuccess ? A8_OK : fail(A8_ERR_CUDA, cudaGetErrorString(e));
@@ -2541,88 +2178,6 @@ static int encode_resident(const a8_enc_seg_t* segs, int nseg, const void* book_
     return cuda_check("a8_encode (resident)");
 }
 
-// Grid-barrier two-pass encode (gb_encode_kernel) for absmax calls beyond
-// the resident kernel: every tensor 16-byte aligned with n % 4 == 0, codes
-// in one block.  A8_GB=0 disables it (A/B measurements); *done = false when
-// the call does not qualify.
-static bool gb_enabled() {
-    static const bool on = [] {
-        const char* e = getenv("A8_GB");
-        return !(e && e[0] == '0');
-    }();
-    return on;
-}
-
-static int encode_gb(const a8_enc_seg_t* segs, int nseg, const void* book_dev, const a8_layout_t& layout,
-                     void* workspace, size_t workspace_bytes, const uint32_t* status_in, uint32_t* status_out, const DevInfo& di,
-                     cudaStream_t st, bool* done) {
-    *done = false;
-    if (!gb_enabled() || di.gb_occ < 1 || nseg > kInlineSegs) return A8_OK;
-    const int64_t G = (int64_t)di.sms * di.gb_occ;  // all CTAs co-resident
-    if (G > kGbMaxCtas) return A8_OK;
-    static_assert(sizeof(a8_lut_t) >= kGbMaxCtas * sizeof(unsigned long long), "steal words fit one table slot");
-    int64_t nch = 0;
-    for (int i = 0; i < nseg; ++i) {
-        const a8_enc_seg_t& s = segs[i];
-        if (s.n % 4 || (s.n > 0 && reinterpret_cast<uintptr_t>(s.x) % 16)) return A8_OK;
-        if (s.flat_off + s.n > layout.block_len) return A8_OK;  // codes must not cross a block
-        nch += (s.n + kChunk - 1) / kChunk;
-    }
-    if (nch < 4 * G) return A8_OK;  // small calls: the ticket kernel's dynamic balance wins
-    GbParams p;
-    memset(&p, 0, sizeof(p));
-    p.lay = layout;
-    p.book = static_cast<const a8_book_t*>(book_dev);
-    uint8_t* ws = static_cast<uint8_t*>(workspace);
-    p.head = reinterpret_cast<WsHead*>(ws);
-    p.ctl = reinterpret_cast<SegCtl*>(ws + ctl_off());
-    p.status_in = status_in;
-    p.status_out = status_out;
-    p.nseg = nseg;
-    p.steal = reinterpret_cast<unsigned long long*>(ws + lut_off(ws_capacity(workspace_bytes)));
-    {
-        // evict_last ring chunks per CTA: the E pass re-reads them first
-        static const int64_t mb = [] {
-            const char* v = getenv("A8_GB_L2MB");
-            return v ? atoll(v) : 80ll;
-        }();
-        p.l2keep = (int)std::min<int64_t>(INT32_MAX, (mb << 20) / (G * kChunk * 4));
-    }
-    // chunk ranges of equal cost: a chunk costs 1, a segment run starting in
-    // a CTA adds its table build (about 4 chunk-times with a bucket table)
-    std::vector<double> pre(nch + 1, 0.0);
-    int64_t c = 0;
-    for (int i = 0; i < nseg; ++i) {
-        p.segs[i].x = segs[i].x;
-        p.segs[i].n = segs[i].n;
-        p.segs[i].flat_off = segs[i].flat_off;
-        p.segs[i].scale_idx = segs[i].scale_idx;
-        p.segs[i].cstart = c;
-        const int64_t k = (segs[i].n + kChunk - 1) / kChunk;
-        for (int64_t q = 0; q < k; ++q, ++c) pre[c + 1] = pre[c] + 1.0 + (q == 0 ? (k >= 3 ? 4.0 : 1.0) : 0.0);
-    }
-    p.segs[nseg].cstart = nch;
-    int64_t at = 0;
-    for (int64_t b = 0; b <= G; ++b) {
-        const double target = pre[nch] * (double)b / (double)G;
-        while (at < nch && pre[at] < target) ++at;
-        p.cta_c0[b] = (int32_t)(b == G ? nch : at);
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)G);
-    cfg.blockDim = dim3(kGbThreads);
-    cfg.dynamicSmemBytes = kGbDynSmem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;  // the grid barrier needs every CTA resident
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, gb_encode_kernel, p);
-    *done = true;
-    return cuda_check("a8_encode (grid barrier)");
-}
-
 extern "C" int a8_roundtrip(const a8_enc_seg_t* segs, float* const* outs, int nseg, const void* book_dev, int norm,
                             const void* static_lut_dev, float* scales_out, uint32_t* status_out, void* workspace,
                             size_t workspace_bytes, void* stream) {
@@ -2680,11 +2235,6 @@ static int encode_impl(const a8_enc_seg_t* segs, int nseg, const void* book_dev,
                                        status_in, status_out, di, static_cast<cudaStream_t>(stream), &done,
                                        nullptr, amax_in);
         if (rc || done) return rc;
-        if (absmax && !amax_in) {
-            const int rg = encode_gb(segs, nseg, book_dev, layout, workspace, workspace_bytes, status_in, status_out, di,
-                                     static_cast<cudaStream_t>(stream), &done);
-            if (rg || done) return rg;
-        }
     }
 
     std::vector<int> order(nseg);

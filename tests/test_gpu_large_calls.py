@@ -1,13 +1,13 @@
-"""The grid-barrier two-pass encode (``gb_encode_kernel``).
+"""Large absmax calls (beyond the resident kernel's shared-memory capacity)
+through the ticket encode kernel: segments of one chunk or a ragged last
+chunk, empty segments, many small segments between large ones, a segment
+whose bucket table is invalid (threshold search), all-zero and subnormal
+segments, non-finite input and recovery.  Every case is checked element for
+element against the C oracle's round trip (oracle/approx8_oracle.c, the
+restatement of codecs.py:244-288).
 
-Absmax calls too large for the resident kernel, with every tensor 16-byte
-aligned and a multiple of 4 elements, take one CTA per SM over static chunk
-ranges with one grid barrier between the max pass and the encode pass.  Its
-edges: segments of one chunk or a ragged last chunk, empty segments, runs of
-1-2 chunks in a CTA (threshold search instead of a bucket table), chunk
-ranges that start or end inside a segment, non-finite input.  Every case is
-checked element for element against the C oracle's round trip
-(oracle/approx8_oracle.c, the restatement of codecs.py:244-288).
+(Written for the grid-barrier encode experiment, whose kernel
+was not kept; the cases stay as coverage of the product kernel.)
 """
 
 from __future__ import annotations
