@@ -142,6 +142,7 @@ struct EncParams {
     const unsigned int* amax_in;  // a8_encode_premax: bits of max|x| per caller segment (else null)
     int64_t keep_tail;            // A8_KEEP_TAIL (tuning): < 0 keeps every A read in L2
     int pol_a, pol_e;             // L2 policies of the A / E reads (A8_POL_A / A8_POL_E)
+    int pre_tables;               // a8_encode_premax: tables published by premax_tables_kernel
     EncSegD segs[kInlineSegs];
     EncBlk blks[kInlineBlks];
 };
@@ -369,6 +370,55 @@ constexpr int kSmemBlks = 6 * kSmemSegs + 8;  // larger plans are read from glob
 
 // kPremax: a8_encode_premax (maxima supplied; a separate instance so the
 // two-pass kernel's code is unchanged by the check)
+// a8_encode_premax prologue: with the maxima supplied, every multi-chunk
+// segment's thresholds and carry table are built and published (ready = 2)
+// by one CTA each before the encode starts, so the encode's producers
+// prefetch published tables from its first E ticket on (no ramp of local
+// builds).  CTA b builds segment nseg-1-b (plans are sorted by size).
+__global__ void __launch_bounds__(kConsumers) premax_tables_kernel(const __grid_constant__ EncParams p) {
+    __shared__ uint32_t sT[128];
+    __shared__ __align__(16) uint32_t sE[kLutMax];
+    const int ctid = threadIdx.x;
+    const int seg = p.nseg - 1 - (int)blockIdx.x;
+    const EncSegD* segs = p.segs_dev ? p.segs_dev : p.segs;
+    const unsigned int amax = __ldg(p.amax_in + segs[seg].src);
+    const float scale = amax == 0u ? 1.0f : __uint_as_float(amax);
+    uint32_t t = kInfBits;
+    if (ctid < 128) {
+        if (scale_ok(scale) && ctid + 1 < p.book->ndistinct)
+            t = threshold_fast((double)scale, p.book->values[ctid], p.book->values[ctid + 1]);
+        sT[ctid] = t;
+    }
+    const int nf = __syncthreads_count(ctid < 127 && t < kInfBits);
+    int32_t kb;
+    uint32_t len;
+    lut_geometry(sT, (uint32_t)nf, &kb, &len);
+    len = max((int32_t)len, (int32_t)(amax >> kKeyShift) - kb + 1);
+    const bool ok = len <= (uint32_t)kLutMax && fill_lut_carry(sT, (uint32_t)nf, kb, len, sE, ctid);
+    const int valid = __syncthreads_and(ok);
+    a8_lut_t* G = p.luts + seg;
+    if (ctid < 128) G->T[ctid] = sT[ctid];
+    if (valid) {
+        uint4* d4 = reinterpret_cast<uint4*>(G->e);
+        const uint4* s4 = reinterpret_cast<const uint4*>(sE);
+        for (uint32_t j = ctid; j < (len + 3) >> 2; j += kConsumers) d4[j] = s4[j];
+    }
+    if (ctid == 0) {
+        G->len = len;
+        G->kbase = kb;
+        G->valid = (uint32_t)valid;
+        G->nfinite = (uint32_t)nf;
+        G->scale = scale;
+        p.ctl[seg].len = len;
+        p.ctl[seg].ready = 1u;  // claimed: no encode CTA builds and publishes it again
+    }
+    __syncthreads();
+    if (ctid == 0) {
+        __threadfence();
+        st_release(&p.ctl[seg].ready, 2u);
+    }
+}
+
 template <bool kPremax>
 __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_constant__ EncParams p) {
     extern __shared__ __align__(128) float sStage[];  // [kStages][kChunk], then a8_lut_t[2] (table slots)
@@ -620,6 +670,20 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
 #ifdef A8_TICKET_TRACE
             unsigned long long sw[5] = {gtime(), 0, 0, 0, 0};
 #endif
+            if (kPremax && p.pre_tables) {
+                // published by premax_tables_kernel before this launch: copy
+                if (btk) return;
+                load_lut_smem(p.luts + seg, E, T, sCanon, p.book, sHdr, ctid, kConsumers);
+                nbar_sync(kBarC, kConsumers);
+                if (ctid == 0) {
+                    Lt->valid = (uint32_t)sHdr[0];
+                    Lt->kbase = sHdr[1];
+                    Lt->len = (uint32_t)sHdr[2] + 1u;
+                    Lt->scale = __ldcg(&p.luts[seg].scale);
+                }
+                nbar_sync(kBarC, kConsumers);
+                return;
+            }
             if (kPremax) {
                 // The max is known (shared memory): build at once, no global
                 // round trip on the critical path.  The CAS that elects the
@@ -1626,8 +1690,14 @@ __global__ void __launch_bounds__(kDecThreads, 4) decode_kernel(const __grid_con
 // barrier, so with 3 buffers no chunk overwrites a buffer still being read.
 constexpr int kDtWarps = 8;
 constexpr int kDtCons = kDtWarps * 32;
-constexpr int kDtStages = 3;
-constexpr int kDtOut = 3;
+#ifndef A8_DT_STAGES
+#define A8_DT_STAGES 3
+#endif
+#ifndef A8_DT_OUT
+#define A8_DT_OUT 3
+#endif
+constexpr int kDtStages = A8_DT_STAGES;
+constexpr int kDtOut = A8_DT_OUT;
 constexpr int kDtMaxRanks = 2;
 constexpr int kDtChunk = 4096;  // elements (16 KB out)
 static size_t dt_smem(int R) {
@@ -1978,7 +2048,7 @@ static void schedule(const std::vector<EncSegD>& d, bool absmax, int64_t wf, std
 // then the E passes, largest segment first -- except that the last `hold`
 // chunks of the largest segment end the launch: every CTA finishes on a
 // long run whose table is published (no table switches in the tail).
-static void schedule_premax(const std::vector<EncSegD>& d, int64_t ctas, std::vector<EncBlk>* blks) {
+static void schedule_premax(const std::vector<EncSegD>& d, int64_t ctas, bool build_tickets, std::vector<EncBlk>* blks) {
     int64_t t = 0;
     auto emit = [&](int s, int kind, int64_t c0, int64_t cnt) {
         if (cnt <= 0) return;
@@ -1988,7 +2058,8 @@ static void schedule_premax(const std::vector<EncSegD>& d, int64_t ctas, std::ve
     const int nseg = (int)d.size();
     for (int s = 0; s < nseg; ++s)
         if (d[s].n <= kChunk) emit(s, kF, 0, 1);
-    for (int s = nseg - 1; s >= 0 && d[s].n > kChunk; --s) emit(s, kB, 0, 1);
+    if (build_tickets)
+        for (int s = nseg - 1; s >= 0 && d[s].n > kChunk; --s) emit(s, kB, 0, 1);
     const int big = nseg - 1;
     const bool several = nseg >= 2 && d[nseg - 2].n > kChunk;
     static const int64_t hold_per_cta = [] {  // A8_PREMAX_HOLD: tail chunks per CTA (tuning)
@@ -2261,9 +2332,18 @@ static int encode_impl(const a8_enc_seg_t* segs, int nseg, const void* book_dev,
         d[i].src = order[i];
         d[i].pad = 0;
     }
+    // a8_encode_premax: the tables are built by a prologue launch (A8_PREMAX_TABLES=0:
+    // by B tickets inside the encode, the round-2 form)
+    static const bool pre_tables = [] {
+        const char* v = getenv("A8_PREMAX_TABLES");
+        return !(v && v[0] == '0');
+    }();
+    int nbig = 0;
+    for (int i = 0; i < nseg; ++i) nbig += d[i].n > kChunk;
+    const bool pre = amax_in && pre_tables && nbig > 0;
     std::vector<EncBlk> blks;
     if (amax_in)
-        schedule_premax(d, (int64_t)di.sms * di.enc_occ, &blks);
+        schedule_premax(d, (int64_t)di.sms * di.enc_occ, !pre, &blks);
     else
         schedule(d, absmax, fill_distance((int64_t)di.sms * di.enc_occ), &blks);
     const int nblk = (int)blks.size() - 1;
@@ -2309,6 +2389,7 @@ static int encode_impl(const a8_enc_seg_t* segs, int nseg, const void* book_dev,
         }();
         p.pol_a = pa;
         p.pol_e = pe;
+        p.pre_tables = pre ? 1 : 0;
     }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if ((int)blks.size() > max_blocks(nseg)) return fail(A8_ERR_USAGE, "a8_encode: schedule overflow");
@@ -2316,6 +2397,7 @@ static int encode_impl(const a8_enc_seg_t* segs, int nseg, const void* book_dev,
     if (nseg <= kInlineSegs && (int)blks.size() <= kInlineBlks) {
         std::copy(d.begin(), d.end(), p.segs);
         std::copy(blks.begin(), blks.end(), p.blks);
+        if (pre) premax_tables_kernel<<<nbig, kConsumers, 0, st>>>(p);
         if (amax_in)
             encode_kernel<true><<<(unsigned)grid, kEncThreads, kEncDynSmem, st>>>(p);
         else
@@ -2330,6 +2412,7 @@ static int encode_impl(const a8_enc_seg_t* segs, int nseg, const void* book_dev,
         cudaMemcpyAsync(plan + sb, blks.data(), sizeof(EncBlk) * blks.size(), cudaMemcpyHostToDevice, st);
         p.segs_dev = reinterpret_cast<const EncSegD*>(plan);
         p.blks_dev = reinterpret_cast<const EncBlk*>(plan + sb);
+        if (pre) premax_tables_kernel<<<nbig, kConsumers, 0, st>>>(p);
         if (amax_in)
             encode_kernel<true><<<(unsigned)grid, kEncThreads, kEncDynSmem, st>>>(p);
         else
