@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(kConsumers) premax_tables_kernel(const __grid_
         G->valid = (uint32_t)valid;
         G->nfinite = (uint32_t)nf;
         G->scale = scale;
-        p.ctl[seg].len = len;
+        p.ctl[seg].len = valid ? len : 0u;  // the producers copy header + e[len]: none when invalid
         p.ctl[seg].ready = 1u;  // claimed: no encode CTA builds and publishes it again
     }
     __syncthreads();
@@ -730,7 +730,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                         G->valid = (uint32_t)valid;
                         G->nfinite = (uint32_t)nf;
                         G->scale = scale;
-                        p.ctl[seg].len = len;
+                        p.ctl[seg].len = valid ? len : 0u;  // the producers copy header + e[len]: none when invalid
                     }
                     nbar_sync(kBarC, kConsumers);
                     if (ctid == 0) {
@@ -853,7 +853,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                     G->valid = (uint32_t)valid;
                     G->nfinite = (uint32_t)nf;
                     G->scale = scale;
-                    p.ctl[seg].len = len;
+                    p.ctl[seg].len = valid ? len : 0u;  // the producers copy header + e[len]: none when invalid
                 }
                 nbar_sync(kBarC, kConsumers);
                 if (ctid == 0) {
