@@ -1696,12 +1696,20 @@ constexpr int kDtCons = kDtWarps * 32;
 #ifndef A8_DT_OUT
 #define A8_DT_OUT 3
 #endif
+#ifndef A8_DT_REP
+#define A8_DT_REP 32
+#endif
+#ifndef A8_DT_CTAS
+#define A8_DT_CTAS 2
+#endif
 constexpr int kDtStages = A8_DT_STAGES;
+constexpr int kDtRep = A8_DT_REP;    // copies of the decode table (lane-private at 32)
+constexpr int kDtCtas = A8_DT_CTAS;  // CTAs per SM
 constexpr int kDtOut = A8_DT_OUT;
 constexpr int kDtMaxRanks = 2;
 constexpr int kDtChunk = 4096;  // elements (16 KB out)
 static size_t dt_smem(int R) {
-    return 256u * 32u * sizeof(float) + (size_t)kDtStages * R * kDtChunk + (size_t)kDtOut * kDtChunk * sizeof(float);
+    return 256u * kDtRep * sizeof(float) + (size_t)kDtStages * R * kDtChunk + (size_t)kDtOut * kDtChunk * sizeof(float);
 }
 
 struct DtMeta {
@@ -1712,10 +1720,10 @@ struct DtMeta {
     int32_t pad2;
 };
 
-__global__ void __launch_bounds__(kDtCons + 32, 2) decode_tma_kernel(const __grid_constant__ DecParams p) {
+__global__ void __launch_bounds__(kDtCons + 32, kDtCtas) decode_tma_kernel(const __grid_constant__ DecParams p) {
     extern __shared__ __align__(128) float sDyn[];
-    float* const sTab = sDyn;                                                              // [256][32]
-    uint8_t* const sCodes = reinterpret_cast<uint8_t*>(sDyn + 256 * 32);                  // [stage][rank][4096]
+    float* const sTab = sDyn;                                                              // [256][kDtRep]
+    uint8_t* const sCodes = reinterpret_cast<uint8_t*>(sDyn + 256 * kDtRep);                  // [stage][rank][4096]
     float* const sOut = reinterpret_cast<float*>(sCodes + (size_t)kDtStages * p.nranks * kDtChunk);  // [3][4096]
     __shared__ float sScale[kInlineSegs * kDtMaxRanks];
     __shared__ __align__(8) uint64_t sFull[kDtStages];
@@ -1777,9 +1785,9 @@ __global__ void __launch_bounds__(kDtCons + 32, 2) decode_tma_kernel(const __gri
     const int ct = tid - 32;
     {
         const float v = p.book->table[ct];
-        float4* d = reinterpret_cast<float4*>(sTab + ct * 32);
+        float4* d = reinterpret_cast<float4*>(sTab + ct * kDtRep);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) d[q] = make_float4(v, v, v, v);
+        for (int q = 0; q < kDtRep / 4; ++q) d[q] = make_float4(v, v, v, v);
     }
     for (int i = ct; i < R * p.nseg; i += kDtCons) {
         const int sgi = i / R, r = i % R;
@@ -1809,7 +1817,7 @@ __global__ void __launch_bounds__(kDtCons + 32, 2) decode_tma_kernel(const __gri
         }
     }
     nbar_sync(2, kDtCons);  // tables and scales complete
-    const float* tl = sTab + lane;
+    const float* tl = sTab + (lane & (kDtRep - 1));
     const float invN = 1.0f / (float)R;
     const bool pow2 = (R & (R - 1)) == 0;
     const uint64_t wpol = p.wpol == 2 ? policy_evict_last() : p.wpol == 1 ? policy_evict_normal() : policy_evict_first();
@@ -1830,8 +1838,8 @@ __global__ void __launch_bounds__(kDtCons + 32, 2) decode_tma_kernel(const __gri
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const uint32_t w = *reinterpret_cast<const uint32_t*>(cs + q * 1024 + ct * 4);
-                const float d0 = __fmul_rn(tl[(w & 255u) * 32u], s), d1 = __fmul_rn(tl[((w >> 8) & 255u) * 32u], s);
-                const float d2 = __fmul_rn(tl[((w >> 16) & 255u) * 32u], s), d3 = __fmul_rn(tl[(w >> 24) * 32u], s);
+                const float d0 = __fmul_rn(tl[(w & 255u) * kDtRep], s), d1 = __fmul_rn(tl[((w >> 8) & 255u) * kDtRep], s);
+                const float d2 = __fmul_rn(tl[((w >> 16) & 255u) * kDtRep], s), d3 = __fmul_rn(tl[(w >> 24) * kDtRep], s);
                 if (r == 0) {
                     acc[q][0] = d0; acc[q][1] = d1; acc[q][2] = d2; acc[q][3] = d3;
                 } else {
@@ -2524,7 +2532,7 @@ static int decode_impl(const a8_dec_seg_t* segs, const float* const* locals, int
         }();
         p.rpol = rp;
         p.wpol = wp;
-        const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)di.sms * 2, chunks));
+        const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)di.sms * kDtCtas, chunks));
         decode_tma_kernel<<<(unsigned)grid, kDtCons + 32, dt_smem(nranks), st>>>(p);
     } else if (nseg <= kInlineSegs) {
         std::copy(d.begin(), d.begin() + nseg, p.segs);
