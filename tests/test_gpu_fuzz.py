@@ -8,7 +8,9 @@ tails), magnitudes from subnormal to 1e30, several distributions, and
 pointers that are not 16-byte aligned (views into a larger buffer).  The
 N = 1 exchange (one encode launch for all tensors, one decode launch) must
 reproduce the oracle's round trip of every tensor bit for bit, and
-``encode_buffer`` its codes and scale.  Cases with a NaN / Inf planted in
+``encode_buffer`` its codes and scale; likewise the per-block codec, the
+producer-fused maxima + one-pass encode, and N = 2..5 virtual-rank
+exchanges.  Cases with a NaN / Inf planted in
 one tensor must raise ``InputError`` and leave the codec usable.
 """
 
@@ -160,3 +162,51 @@ def test_virtual_ranks_match_oracle(cuda, case):
     for r in range(nranks):
         for i, (a, b) in enumerate(zip(res[r], want)):
             assert a.tobytes() == b.tobytes(), (label, mode, op, nranks, r, i)
+
+
+@pytest.mark.parametrize("case", range(9))
+def test_blocked_matches_oracle(cuda, case):
+    """Per-block max-abs (not a reference feature: encode_buffer applied to
+    every block alone, oracle.encode_blocked): random sizes, block sizes,
+    magnitudes per region (all-zero and subnormal blocks included)."""
+    rng = np.random.default_rng(9600 + case)
+    block = (1024, 2048, 4096)[case % 3]
+    kind = ("dynamic-tree", "linear")[case % 2]
+    n = int(np.exp(rng.uniform(np.log(1), np.log(3_000_000))))
+    x = np.zeros(n, np.float32)
+    pos = 0
+    while pos < n:  # regions of random length and magnitude
+        m = int(rng.integers(1, 3 * block))
+        mag = float(rng.choice([0.0, 1e-42, 1e-3, 1.0, 1e20, 10.0 ** rng.uniform(-30, 30)]))
+        x[pos:pos + m] = (rng.standard_normal(min(m, n - pos)) * mag).astype(np.float32)
+        pos += m
+    (xd,) = _to_device(rng, [x], cuda)
+    cb = A.build_codebook(A.DataTypeSpec(kind, "absmax"))
+    q = A.encode_buffer(xd, cb, block_size=block)
+    codes = q.codes.view(-1).cpu().numpy()
+    scales = q.block_scales.view(-1).cpu().numpy()
+    y = A.decode_buffer(q, cb).view(-1).cpu().numpy()
+    for b, b0 in enumerate(range(0, n, block)):
+        c, s = O.c_encode(x[b0:b0 + block], kind, "absmax")
+        assert codes[b0:b0 + block].tobytes() == c.tobytes(), (block, b)
+        assert np.float32(scales[b]) == np.float32(s), (block, b)
+        assert y[b0:b0 + block].tobytes() == O.c_decode(c, s, kind).tobytes(), (block, b)
+
+
+@pytest.mark.parametrize("case", range(6))
+def test_premax_exchange_matches_oracle(cuda, case):
+    """Producer-fused maxima (scale_absmax_: y = fl(alpha x) and max|y|) and
+    the one-pass encode: the same bits as the oracle's round trip of y."""
+    rng = np.random.default_rng(9400 + case)
+    label = ("dynamic-tree/absmax", "linear/absmax")[case % 2]
+    kind, norm, dec = _oracle_args(label)
+    host = _draw(rng, int(rng.integers(1, 20)), 12_000_000 if case < 2 else 2_000_000)
+    alpha = float(np.float32(rng.choice([1.0, 0.5, 0.125, 1 / 3])))
+    grads = _to_device(rng, host, cuda)
+    outs = [torch.empty_like(g) for g in grads]
+    ex = A.GradientExchange(A.parse_spec(label), check="sync")
+    ex(grads, out=outs, amax=A.scale_absmax_(grads, alpha))
+    for h, o in zip(host, outs):
+        y = (h * np.float32(alpha)).astype(np.float32)
+        c, s = O.c_encode(y, kind, norm, dec)
+        assert o.cpu().numpy().tobytes() == O.c_decode(c, s, kind).tobytes(), (alpha, h.size)
