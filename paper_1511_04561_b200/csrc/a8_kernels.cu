@@ -1458,373 +1458,6 @@ __global__ void __launch_bounds__(kRThreads, 1) resident_encode_kernel(const __g
 }
 
 // ---------------------------------------------------------------------------
-// K1+K2+K3 grid-barrier two-pass encode for absmax calls beyond the resident
-// kernel (config 3: 244 MB of gradients).
-//
-// The ticket kernel's E pass re-reads each chunk ~100 MB of traffic after
-// its A pass, from DRAM.  Here one CTA per SM owns a static, contiguous range
-// of the call's chunks: it streams them once for the max (A pass), keeping
-// the last kGbKeep chunks in shared memory and the kGbL2 chunks before them
-// in L2 (evict_last); one grid barrier makes every segment's max final; then
-// the CTA encodes its range in REVERSE order (shared-memory chunks, then the
-// L2-hot ones, then the rest).  Two independent groups per CTA -- each one
-// producer lane + 8 consumer warps + its own ring and table -- claim chunks
-// from shared counters, so the SM's two pipelines share the range
-// dynamically (two separate CTAs per SM ended ≈6 µs apart: the warp
-// scheduler favours the older CTA).  The E pass's first loads are issued
-// before the barrier.
-constexpr int kGbGroups = 2;
-constexpr int kGbGW = 8;                               // consumer warps per group
-constexpr int kGbGCons = kGbGW * 32;                   // consumer threads per group
-constexpr int kGbThreads = kGbGroups * (32 + kGbGCons);
-#ifndef A8_GB_RING
-#define A8_GB_RING 4
-#endif
-#ifndef A8_GB_KEEP
-#define A8_GB_KEEP 3
-#endif
-#ifndef A8_GB_DEMOTE
-#define A8_GB_DEMOTE 1
-#endif
-#ifndef A8_GB_CODE_HINT
-#define A8_GB_CODE_HINT 0
-#endif
-constexpr int kGbRing = A8_GB_RING;                    // stages per group
-constexpr int kGbKeep = A8_GB_KEEP;                    // chunks kept in shared memory across the barrier
-constexpr int kGbMaxCtas = 160;
-constexpr size_t kGbDynSmem =
-    (size_t)(kGbGroups * kGbRing + kGbKeep) * kChunk * sizeof(float) + (size_t)kGbGroups * kLutMax * 4;
-static_assert(kLutMax / 16 == kGbGCons, "one table-fill thread per 16 buckets");
-
-struct GbSeg {
-    const float* x;
-    int64_t n;
-    int64_t flat_off;
-    int64_t cstart;  // first chunk of the segment in the call's chunk list
-    int32_t scale_idx;
-    int32_t pad;
-};
-
-struct GbParams {
-    a8_layout_t lay;  // one block (codes at flat_off + i)
-    const a8_book_t* book;
-    WsHead* head;
-    SegCtl* ctl;
-    const unsigned int* status_in;
-    unsigned int* status_out;
-    int nseg;
-    int l2keep;  // ring chunks per CTA read with evict_last (the E pass re-reads them first)
-    GbSeg segs[kInlineSegs + 1];  // segs[nseg].cstart = total chunks
-    int32_t cta_c0[kGbMaxCtas + 1];  // chunk range of CTA b: [cta_c0[b], cta_c0[b + 1])
-};
-
-#ifdef A8_TICKET_TRACE
-__device__ unsigned long long g_gb_trace[kGbMaxCtas][6];  // start, A done, barrier left, E kept done, end, chunks
-#define GB_STAMP(i)                                          \
-    do {                                                     \
-        if (ctid == 0) g_gb_trace[blockIdx.x][i] = gtime();  \
-    } while (0)
-#else
-#define GB_STAMP(i) \
-    do {            \
-    } while (0)
-#endif
-
-__global__ void __launch_bounds__(kGbThreads, 1) gb_encode_kernel(const __grid_constant__ GbParams p) {
-    // [group][kGbRing] ring stages, then kGbKeep kept chunks, then [group] tables
-    extern __shared__ __align__(128) float sSlot[];
-    __shared__ uint32_t sT[kGbGroups][128];
-    __shared__ uint8_t sCanon[128];
-    __shared__ unsigned int sRed[kGbGroups][2][kGbGW];
-    __shared__ __align__(8) uint64_t sFull[kGbGroups][kGbRing];
-    __shared__ __align__(8) uint64_t sEmpty[kGbGroups][kGbRing];
-    __shared__ __align__(8) uint64_t sKeep[kGbKeep > 0 ? kGbKeep : 1];
-    __shared__ int64_t sMc[kGbGroups][kGbRing];  // chunk j of the stage; -1 ends a pass
-    __shared__ unsigned int sNextA, sNextE;      // the groups' claims (A ascending, E descending)
-    __shared__ int sFinal;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t c_lo = p.cta_c0[blockIdx.x], c_hi = p.cta_c0[blockIdx.x + 1];
-    const int64_t nloc = c_hi - c_lo;
-    const int64_t nkeep = min((int64_t)kGbKeep, nloc);
-    const int64_t nring = nloc - nkeep;  // chunks j >= nring stay in shared memory
-    float* const sKeepData = sSlot + (size_t)kGbGroups * kGbRing * kChunk;
-    if (tid == 0) {
-        for (int g = 0; g < kGbGroups; ++g)
-            for (int s = 0; s < kGbRing; ++s) {
-                mbar_init(&sFull[g][s], 1);
-                mbar_init(&sEmpty[g][s], kGbGW);
-            }
-        for (int s = 0; s < kGbKeep; ++s) mbar_init(&sKeep[s], 1);
-        sNextA = 0u;
-        sNextE = 0u;
-        mbar_fence_init();
-    }
-    if (tid >= 64 && tid < 64 + 128) sCanon[tid - 64] = p.book->codes[tid - 64];
-    __syncthreads();
-
-    auto seg_step = [&](int s, int64_t c) {  // chunk c of the call -> its segment, walking from s
-        while (c >= p.segs[s + 1].cstart) ++s;
-        while (c < p.segs[s].cstart) --s;
-        return s;
-    };
-    int s0 = 0;
-    if (nloc > 0)
-        while (c_lo >= p.segs[s0 + 1].cstart) ++s0;
-
-    if (warp < kGbGroups) {
-        // ===================== producers (lane 0 of warp g) =====================
-        if (lane == 0) {
-            const int g = warp;
-            const uint64_t first = policy_evict_first(), last = policy_evict_last();
-            int s = s0;
-            int64_t it = 0;
-            auto load = [&](int64_t j, uint64_t* bar, float* dst, uint64_t pol) {
-                const int64_t c = c_lo + j;
-                s = seg_step(s, c);
-                const GbSeg& sg = p.segs[s];
-                const int64_t base = (c - sg.cstart) * kChunk;
-                const uint32_t bytes = (uint32_t)min((int64_t)kChunk, sg.n - base) * 4u;
-                mbar_arrive_expect_tx(bar, bytes);
-                bulk_g2s(dst, sg.x + base, bytes, bar, pol);
-            };
-            // one ring stage: chunk j's data (ring chunks), or only its index
-            // (kept chunks arrive on their own barrier), or -1 (end of a pass)
-            auto stage = [&](int64_t j, bool data, uint64_t pol) {
-                const int st = (int)(it % kGbRing);
-                mbar_wait(&sEmpty[g][st], (uint32_t)(((it / kGbRing) & 1) ^ 1));
-                sMc[g][st] = j;
-                if (data)
-                    load(j, &sFull[g][st], sSlot + (size_t)(g * kGbRing + st) * kChunk, pol);
-                else
-                    mbar_arrive(&sFull[g][st]);
-                ++it;
-            };
-            for (;;) {  // A pass
-                const int64_t j = (int64_t)atomicAdd(&sNextA, 1u);
-                if (j >= nloc) break;
-                if (j < nring) {
-                    stage(j, true, j >= nring - p.l2keep ? last : first);
-                } else {
-                    const int k = (int)(j - nring);
-                    load(j, &sKeep[k], sKeepData + (size_t)k * kChunk, first);
-                    stage(j, false, first);
-                }
-            }
-            stage(-1, false, first);
-            for (;;) {  // E pass re-reads, most recent first
-                const int64_t j = nring - 1 - (int64_t)atomicAdd(&sNextE, 1u);
-                if (j < 0) break;
-                stage(j, true, first);
-            }
-            stage(-1, false, first);
-        }
-        return;  // the producer warps take no part in the consumers' barriers
-    }
-
-    // ===================== consumers =====================
-    const int g = (warp - kGbGroups) / kGbGW;          // group
-    const int cw = (warp - kGbGroups) % kGbGW;         // warp in the group
-    const int gt = tid - kGbGroups * 32 - g * kGbGCons;  // thread in the group
-    const int ctid = tid - kGbGroups * 32;             // thread among all consumers
-    const int barG = 2 + g;                            // named barrier of the group
-    constexpr int kBarAll = 1;                         // named barrier of all consumers
-    uint32_t* const sE = reinterpret_cast<uint32_t*>(sKeepData + (size_t)kGbKeep * kChunk) + g * kLutMax;
-    uint32_t* const T = sT[g];
-    int64_t it = 0;
-    GB_STAMP(0);
-    auto next_stage = [&](int& st) -> int64_t {
-        st = (int)(it % kGbRing);
-        mbar_wait(&sFull[g][st], (uint32_t)((it / kGbRing) & 1));
-        ++it;
-        return sMc[g][st];
-    };
-    auto release = [&](int st) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sEmpty[g][st]);
-    };
-    auto chunk_data = [&](int64_t j, int st) -> const float* {
-        if (j < nring) return sSlot + (size_t)(g * kGbRing + st) * kChunk;
-        const int k = (int)(j - nring);
-        mbar_wait(&sKeep[k], 0u);
-        return sKeepData + (size_t)k * kChunk;
-    };
-
-    // ---- A pass: per-segment max |x| of the chunks this group took ----
-    {
-        int s = -1, fpar = 0;
-        unsigned int amx = 0;  // bits * 2 (drops the sign)
-        auto flush = [&]() {
-            const unsigned int wm = __reduce_max_sync(0xffffffffu, amx) >> 1;
-            if (lane == 0) sRed[g][fpar][cw] = wm;
-            nbar_sync(barG, kGbGCons);
-            if (gt == 0) {
-                unsigned int m = 0;
-#pragma unroll
-                for (int w = 0; w < kGbGW; ++w) m = max(m, sRed[g][fpar][w]);
-                if (m) red_max_u32(&p.ctl[s].amax, m);
-            }
-            fpar ^= 1;
-            amx = 0;
-        };
-        for (;;) {
-            int st;
-            const int64_t j = next_stage(st);
-            if (j < 0) {
-                release(st);
-                break;
-            }
-            const int64_t c = c_lo + j;
-            const int sn = seg_step(s < 0 ? s0 : s, c);
-            if (sn != s) {
-                if (s >= 0) flush();
-                s = sn;
-            }
-            const GbSeg& sg = p.segs[s];
-            const int cnt = (int)min((int64_t)kChunk, sg.n - (c - sg.cstart) * kChunk);
-            const uint4* in = reinterpret_cast<const uint4*>(chunk_data(j, st));
-            if (cnt == kChunk) {
-#pragma unroll
-                for (int q = 0; q < kChunk / (kGbGCons * 4); ++q) {
-                    const uint4 v = in[q * kGbGCons + gt];
-                    amx = __vimax3_u32(amx, v.x * 2u, v.y * 2u);
-                    amx = __vimax3_u32(amx, v.z * 2u, v.w * 2u);
-                }
-            } else {
-                for (int i = gt; 4 * i < cnt; i += kGbGCons) {
-                    const uint4 v = in[i];
-                    amx = __vimax3_u32(amx, v.x * 2u, v.y * 2u);
-                    amx = __vimax3_u32(amx, v.z * 2u, v.w * 2u);
-                }
-            }
-            release(st);
-        }
-        if (s >= 0) flush();
-    }
-
-    // ---- grid barrier: every segment's max is final (cooperative launch) ----
-    nbar_sync(kBarAll, kGbGroups * kGbGCons);
-    GB_STAMP(1);
-    if (ctid == 0) {
-        __threadfence();
-        atomicAdd(&p.head->ticket, 1u);
-        unsigned int ns = 32;
-        while (ld_acquire(&p.head->ticket) < gridDim.x) {
-            __nanosleep(ns);
-            ns = min(ns * 2u, 256u);
-        }
-    }
-    nbar_sync(kBarAll, kGbGroups * kGbGCons);
-    GB_STAMP(2);
-
-    // ---- E pass: this group's kept chunks, then its ring's re-reads ----
-    {
-        int s = -1, valid = 0;
-        int32_t kb = 0;
-        uint32_t emin = 0, eb = 0;
-        unsigned int amax = 0;
-        float scale = 1.0f;
-        auto encode_chunk = [&](int64_t j, const float* data) {
-            const int64_t c = c_lo + j;
-            const int sn = seg_step(s < 0 ? s0 : s, c);
-            if (sn != s) {
-                // K2: thresholds and, for segments of 3+ chunks, the carry
-                // bucket table (shorter ones search the thresholds)
-                s = sn;
-                amax = __ldcg(&p.ctl[s].amax);
-                scale = amax == 0u ? 1.0f : __uint_as_float(amax);
-                nbar_sync(barG, kGbGCons);  // the group is done with its previous table
-                uint32_t t = kInfBits;
-                if (gt < 128) {
-                    if (scale_ok(scale) && gt + 1 < p.book->ndistinct)
-                        t = threshold_fast((double)scale, p.book->values[gt], p.book->values[gt + 1]);
-                    T[gt] = t;
-                }
-                const int nf = nbar_popc(barG, kGbGCons, gt < 127 && t < kInfBits);
-                uint32_t len;
-                lut_geometry(T, (uint32_t)nf, &kb, &len);
-                len = max((int32_t)len, (int32_t)(amax >> kKeyShift) - kb + 1);
-                bool ok = p.segs[s + 1].cstart - p.segs[s].cstart >= 3 && amax < kInfBits && len <= (uint32_t)kLutMax;
-                if (ok) ok = fill_lut_carry(T, (uint32_t)nf, kb, len, sE, gt);
-                valid = nbar_and(barG, kGbGCons, ok);
-                emin = smem_addr(sE);
-                eb = emin - (uint32_t)kb * 4u;
-            }
-            const GbSeg& sg = p.segs[s];
-            const int64_t base = (c - sg.cstart) * kChunk;
-            const int cnt = (int)min((int64_t)kChunk, sg.n - base);
-            if (base == 0) {  // chunk 0 of the segment: its scale and status
-                if (gt < p.lay.scale_reps) p.lay.scales[gt * p.lay.scale_block_stride + sg.scale_idx] = scale;
-                if (gt == 0 && amax >= kInfBits) atomicOr(&p.head->status, A8_STATUS_NONFINITE);
-            }
-            const uint4* in = reinterpret_cast<const uint4*>(data);
-            uint32_t* out = reinterpret_cast<uint32_t*>(p.lay.codes + sg.flat_off + base);
-            if (valid && cnt == kChunk && A8_GB_CODE_HINT) {  // codes kept in L2 for the decode
-                const uint64_t pol = policy_evict_last();
-#pragma unroll
-                for (int q = 0; q < kChunk / (kGbGCons * 4); ++q)
-                    st_hint_u32(out + q * kGbGCons + gt, encode4_carry(in[q * kGbGCons + gt], eb, (int32_t)emin), pol);
-            } else if (valid && cnt == kChunk) {
-#pragma unroll
-                for (int q = 0; q < kChunk / (kGbGCons * 4); ++q)
-                    out[q * kGbGCons + gt] = encode4_carry(in[q * kGbGCons + gt], eb, (int32_t)emin);
-            } else if (valid) {
-                for (int i = gt; 4 * i < cnt; i += kGbGCons) out[i] = encode4_carry(in[i], eb, (int32_t)emin);
-            } else {
-                for (int i = gt; 4 * i < cnt; i += kGbGCons) out[i] = encode4_search(in[i], T, sCanon);
-            }
-        };
-        auto s_cur = [&](int64_t j) { return seg_step(s < 0 ? s0 : s, c_lo + j); };
-        for (int64_t j = nloc - 1 - g; j >= nring; j -= kGbGroups) encode_chunk(j, chunk_data(j, 0));
-        GB_STAMP(3);
-        for (;;) {
-            int st;
-            const int64_t j = next_stage(st);
-            if (j < 0) break;
-            encode_chunk(j, sSlot + (size_t)(g * kGbRing + st) * kChunk);
-            release(st);
-            if (A8_GB_DEMOTE && j >= nring - p.l2keep && gt <= kChunk * 4 / 128) {
-                // the chunk's lines were read with evict_last: back to normal
-                // priority now that they are dead, so they do not crowd the L2
-                // the decode writes through
-                const GbSeg& sg = p.segs[s_cur(j)];
-                const uintptr_t a0 = reinterpret_cast<uintptr_t>(sg.x + (c_lo + j - sg.cstart) * kChunk) & ~(uintptr_t)127;
-                const uintptr_t a = a0 + (uintptr_t)gt * 128u;  // lines holding bytes of the chunk only
-                if (a < reinterpret_cast<uintptr_t>(sg.x + min(sg.n, (c_lo + j - sg.cstart + 1) * kChunk)))
-                    asm volatile("applypriority.global.L2::evict_normal [%0], 128;" ::"l"(a) : "memory");
-            }
-        }
-    }
-
-    // ---- last CTA out: empty segments' scales, status, zeroed workspace ----
-    nbar_sync(kBarAll, kGbGroups * kGbGCons);
-    GB_STAMP(4);
-    if (ctid == 0) {
-        __threadfence();
-        sFinal = atomicAdd(&p.head->ctas_done, 1u) == gridDim.x - 1;
-    }
-    nbar_sync(kBarAll, kGbGroups * kGbGCons);
-    if (sFinal) {
-        __threadfence();
-        for (int e = 0; e < p.nseg; ++e)  // scale of an empty buffer (codecs.py:257-258)
-            if (p.segs[e].n == 0 && ctid < p.lay.scale_reps)
-                p.lay.scales[ctid * p.lay.scale_block_stride + p.segs[e].scale_idx] = 1.0f;
-        for (int i = ctid; i < p.nseg; i += kGbGroups * kGbGCons) p.ctl[i].amax = 0u;
-        nbar_sync(kBarAll, kGbGroups * kGbGCons);
-        if (ctid < p.lay.scale_reps) {
-            const unsigned int stt = atomicAdd(&p.head->status, 0u) | (p.status_in ? *p.status_in : 0u);
-            p.status_out[(int64_t)ctid * p.lay.scale_block_stride] = stt;
-        }
-        nbar_sync(kBarAll, kGbGroups * kGbGCons);
-        if (ctid == 0) {
-            p.head->ticket = 0u;
-            p.head->ctas_done = 0u;
-            p.head->status = 0u;
-        }
-        __threadfence();
-    }
-}
-
-// ---------------------------------------------------------------------------
 // K4/K5: decode (+ rank-ordered sum, + 1/N average).
 //
 // Per segment, each CTA keeps pre-scaled tables fl(table[c] * s_r) for every
@@ -2262,7 +1895,6 @@ struct DevInfo {
     int enc_occ = 0;
     int dec_occ = 0;
     int res_occ = 0;  // resident encode: CTAs per SM (1, or 0 if it cannot run)
-    int gb_occ = 0;   // grid-barrier encode: CTAs per SM (1, or 0)
 };
 
 static std::mutex g_mu;
@@ -2294,10 +1926,6 @@ static int dev_info(int device, DevInfo* out) {
         e = cudaFuncSetAttribute(resident_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRDynSmem);
         if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.res_occ, resident_encode_kernel, kRThreads, kRDynSmem);
-        if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
-        e = cudaFuncSetAttribute(gb_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGbDynSmem);
-        if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.gb_occ, gb_encode_kernel, kGbThreads, kGbDynSmem);
         if (e != cudaSuccess) return fail(A8_ERR_CUDA, cudaGetErrorString(e));
         d.enc_occ = std::max(1, d.enc_occ);
         d.dec_occ = std::max(1, d.dec_occ);
@@ -2516,10 +2144,6 @@ extern "C" int a8_debug_ticket_trace(uint64_t* out, int64_t n) {
     cudaError_t e = cudaMemcpyFromSymbol(out, a8::g_ticket_trace, sizeof(uint64_t) * 5 * n);
     return e == cudaSuccess ? A8_OK : fail(A8_ERR_CUDA, cudaGetErrorString(e));
 }
-extern "C" int a8_debug_gb_trace(uint64_t* out) {  // [kGbMaxCtas][6]
-    cudaError_t e = cudaMemcpyFromSymbol(out, a8::g_gb_trace, sizeof(a8::g_gb_trace));
-    return e == cudaSuccess ? A8_OK : fail(A8_ERR_CUDA, cudaGetErrorString(e));
-}
 extern "C" int a8_debug_res_trace(uint64_t* out) {  // [2][8]
     cudaError_t e = cudaMemcpyFromSymbol(out, a8::g_res_trace, sizeof(a8::g_res_trace));
     return e == cudaSuccess ? A8_OK : fail(A8_ERR_CUDA, cudaGetErrorString(e));
@@ -2633,87 +2257,6 @@ static int encode_resident(const a8_enc_seg_t* segs, int nseg, const void* book_
     return cuda_check("a8_encode (resident)");
 }
 
-// Grid-barrier two-pass encode (gb_encode_kernel) for absmax calls beyond
-// the resident kernel: every tensor 16-byte aligned with n % 4 == 0, codes
-// in one block.  A8_GB=0 disables it (A/B measurements); *done = false when
-// the call does not qualify.
-static bool gb_enabled() {
-    static const bool on = [] {
-        const char* e = getenv("A8_GB");
-        return !(e && e[0] == '0');
-    }();
-    return on;
-}
-
-static int encode_gb(const a8_enc_seg_t* segs, int nseg, const void* book_dev, const a8_layout_t& layout,
-                     void* workspace, const uint32_t* status_in, uint32_t* status_out, const DevInfo& di,
-                     cudaStream_t st, bool* done) {
-    *done = false;
-    if (!gb_enabled() || di.gb_occ < 1 || nseg > kInlineSegs) return A8_OK;
-    const int64_t G = (int64_t)di.sms;  // one CTA per SM, all co-resident
-    if (G > kGbMaxCtas) return A8_OK;
-    int64_t nch = 0;
-    for (int i = 0; i < nseg; ++i) {
-        const a8_enc_seg_t& s = segs[i];
-        if (s.n % 4 || (s.n > 0 && reinterpret_cast<uintptr_t>(s.x) % 16)) return A8_OK;
-        if (s.flat_off + s.n > layout.block_len) return A8_OK;  // codes must not cross a block
-        nch += (s.n + kChunk - 1) / kChunk;
-    }
-    if (nch < 4 * G) return A8_OK;  // small calls: the ticket kernel's dynamic balance wins
-    GbParams p;
-    memset(&p, 0, sizeof(p));
-    p.lay = layout;
-    p.book = static_cast<const a8_book_t*>(book_dev);
-    uint8_t* ws = static_cast<uint8_t*>(workspace);
-    p.head = reinterpret_cast<WsHead*>(ws);
-    p.ctl = reinterpret_cast<SegCtl*>(ws + ctl_off());
-    p.status_in = status_in;
-    p.status_out = status_out;
-    p.nseg = nseg;
-    {
-        // evict_last ring chunks per CTA: the E pass re-reads them first
-        static const int64_t mb = [] {
-            const char* v = getenv("A8_GB_L2MB");
-            return v ? atoll(v) : 80ll;
-        }();
-        p.l2keep = (int)std::min<int64_t>(INT32_MAX, (mb << 20) / (G * kChunk * 4));
-    }
-    // chunk ranges of equal cost: a chunk costs 1, a segment run starting in
-    // a CTA adds its table build (about 4 chunk-times with a bucket table)
-    std::vector<double> pre(nch + 1, 0.0);
-    int64_t c = 0;
-    for (int i = 0; i < nseg; ++i) {
-        p.segs[i].x = segs[i].x;
-        p.segs[i].n = segs[i].n;
-        p.segs[i].flat_off = segs[i].flat_off;
-        p.segs[i].scale_idx = segs[i].scale_idx;
-        p.segs[i].cstart = c;
-        const int64_t k = (segs[i].n + kChunk - 1) / kChunk;
-        for (int64_t q = 0; q < k; ++q, ++c) pre[c + 1] = pre[c] + 1.0 + (q == 0 ? (k >= 3 ? 4.0 : 1.0) : 0.0);
-    }
-    p.segs[nseg].cstart = nch;
-    int64_t at = 0;
-    for (int64_t b = 0; b <= G; ++b) {
-        const double target = pre[nch] * (double)b / (double)G;
-        while (at < nch && pre[at] < target) ++at;
-        p.cta_c0[b] = (int32_t)(b == G ? nch : at);
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)G);
-    cfg.blockDim = dim3(kGbThreads);
-    cfg.dynamicSmemBytes = kGbDynSmem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;  // the grid barrier needs every CTA resident
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, gb_encode_kernel, p);
-    *done = true;
-    return cuda_check("a8_encode (grid barrier)");
-}
-
-
 extern "C" int a8_roundtrip(const a8_enc_seg_t* segs, float* const* outs, int nseg, const void* book_dev, int norm,
                             const void* static_lut_dev, float* scales_out, uint32_t* status_out, void* workspace,
                             size_t workspace_bytes, void* stream) {
@@ -2771,11 +2314,6 @@ static int encode_impl(const a8_enc_seg_t* segs, int nseg, const void* book_dev,
                                        status_in, status_out, di, static_cast<cudaStream_t>(stream), &done,
                                        nullptr, amax_in);
         if (rc || done) return rc;
-        if (absmax && !amax_in) {
-            const int rg = encode_gb(segs, nseg, book_dev, layout, workspace, status_in, status_out, di,
-                                     static_cast<cudaStream_t>(stream), &done);
-            if (rg || done) return rg;
-        }
     }
 
     std::vector<int> order(nseg);
