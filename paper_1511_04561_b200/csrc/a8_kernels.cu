@@ -2072,7 +2072,7 @@ static void schedule_premax(const std::vector<EncSegD>& d, int64_t ctas, bool bu
     const bool several = nseg >= 2 && d[nseg - 2].n > kChunk;
     static const int64_t hold_per_cta = [] {  // A8_PREMAX_HOLD: tail chunks per CTA (tuning)
         const char* v = getenv("A8_PREMAX_HOLD");
-        return v ? std::max(0ll, atoll(v)) : 4ll;
+        return v ? std::max(0ll, atoll(v)) : 32ll;
     }();
     const int64_t hold = several && d[big].n > kChunk ? std::min<int64_t>(d[big].nE / 2, hold_per_cta * ctas) : 0;
     for (int s = nseg - 1; s >= 0 && d[s].n > kChunk; --s)
