@@ -410,9 +410,13 @@ def codec_sweep(A, torch, dev, clk_sampler_cls):
     (dynamic-tree/absmax and mantissa/decade+1) and the per-block absmax codec
     at 2^30 (blocks of 4096 and 1024): encode / decode kernel time of one
     public-API call each (captured in a CUDA graph, replayed between CUDA
-    events; L2 flushed before every replay), with its own clocks record.
+    events; L2 flushed before every replay by READING a 256 MB buffer, so the
+    flush leaves clean lines and adds no write-back of its own to the timed
+    region -- a written flush buffer left ~126 MB dirty in L2 that every
+    measurement then wrote back, ~19 us), with its own clocks record.
     Synthetic N(0, 1) inputs generated on the device."""
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    flush = torch.zeros(64 << 20, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
+    sink = torch.zeros((), dtype=torch.float32, device=dev)
     peak, _ = peaks()
 
     def time_graph(fn, reps):
@@ -427,7 +431,7 @@ def codec_sweep(A, torch, dev, clk_sampler_cls):
             fn()
         ts = []
         for _ in range(reps):
-            flush.zero_()
+            torch.sum(flush, 0, out=sink)  # read flush: evicts L2 (and writes back its dirty lines) before e0
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             g.replay()
@@ -555,7 +559,7 @@ def codec_sweep(A, torch, dev, clk_sampler_cls):
         out["onebit_c3"] = onebit_c3()
     out["clocks"] = clk.summary()
     out["how"] = ("one public-API encode_buffer / decode_buffer call per case, CUDA-graph replayed between events, "
-                  "median of 7-15, 256 MB L2 flush before each; GB/s at 5 B/elem each way, round trip 10 B/elem; "
+                  "median of 7-15, L2 flushed before each by reading 256 MB (clean lines: no flush write-back in the timed region); GB/s at 5 B/elem each way, round trip 10 B/elem; "
                   "frac against MEASURED_PEAKS hbm_gbs")
     del flush
     torch.cuda.empty_cache()

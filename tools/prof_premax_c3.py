@@ -10,7 +10,10 @@ import bench  # noqa
 import paper_1511_04561_b200 as A  # noqa
 from paper_1511_04561_b200.exchange import CudaSegmentCodec, make_plan  # noqa
 dev = torch.device("cuda", 0)
-flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
+import os  # noqa
+FLUSH_READ = os.environ.get("FLUSH", "read") == "read"  # FLUSH=write: the old written flush
+flush = torch.zeros(64 << 20, dtype=torch.float32, device=dev)
+sink = torch.zeros((), dtype=torch.float32, device=dev)
 
 
 def time_graph(fn, reps=40):
@@ -25,7 +28,10 @@ def time_graph(fn, reps=40):
         fn()
     ts = []
     for _ in range(reps):
-        flush.zero_()
+        if FLUSH_READ:
+            torch.sum(flush, 0, out=sink)
+        else:
+            flush.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         g.replay()
