@@ -370,12 +370,18 @@ constexpr int kSmemBlks = 6 * kSmemSegs + 8;  // larger plans are read from glob
 
 // kPremax: a8_encode_premax (maxima supplied; a separate instance so the
 // two-pass kernel's code is unchanged by the check)
+// Programmatic dependent launch: wait until the preceding grid (the premax
+// table prologue) has completed and its writes are visible; a no-op when the
+// kernel was launched without the PDL attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // a8_encode_premax prologue: with the maxima supplied, every multi-chunk
 // segment's thresholds and carry table are built and published (ready = 2)
 // by one CTA each before the encode starts, so the encode's producers
 // prefetch published tables from its first E ticket on (no ramp of local
 // builds).  CTA b builds segment nseg-1-b (plans are sorted by size).
 __global__ void __launch_bounds__(kConsumers) premax_tables_kernel(const __grid_constant__ EncParams p) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the encode may start streaming now
     __shared__ uint32_t sT[128];
     __shared__ __align__(16) uint32_t sE[kLutMax];
     const int ctid = threadIdx.x;
@@ -559,6 +565,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
                     m.last = !(tn < blks[lo + 1].tstart);
                 }
                 if (p.absmax && kind == kE && bk.seg != pseg) {
+                    if (kPremax && p.pre_tables && pseg < 0) pdl_wait();  // tables of the prologue launch
                     pseg = bk.seg;
                     pslot ^= 1;
                     const unsigned int u = pslot ? uses1++ : uses0++;
@@ -673,6 +680,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
             if (kPremax && p.pre_tables) {
                 // published by premax_tables_kernel before this launch: copy
                 if (btk) return;
+                pdl_wait();
                 load_lut_smem(p.luts + seg, E, T, sCanon, p.book, sHdr, ctid, kConsumers);
                 nbar_sync(kBarC, kConsumers);
                 if (ctid == 0) {
@@ -1105,6 +1113,7 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_kernel(const __grid_con
     }
 
     // last CTA out publishes the status and leaves the workspace zeroed
+    if (kPremax && p.pre_tables) pdl_wait();  // (it resets the prologue's table flags)
     __syncthreads();
     if (tid == 0) {
         __threadfence();
@@ -2285,6 +2294,31 @@ extern "C" int a8_roundtrip(const a8_enc_seg_t* segs, float* const* outs, int ns
     return done ? A8_OK : fail(A8_ERR_USAGE, "a8_roundtrip: call does not fit the fused path (use a8_encode + a8_decode)");
 }
 
+// encode_kernel<true>; after the table prologue it is launched as a
+// programmatic dependent (PDL): its CTAs start streaming while the prologue
+// runs and wait for it (griddepcontrol.wait) only before reading a table.
+static void launch_premax(const EncParams& p, unsigned grid, bool pre, cudaStream_t st) {
+    static const bool pdl = [] {
+        const char* v = getenv("A8_PREMAX_PDL");
+        return !(v && v[0] == '0');
+    }();
+    if (!pre || !pdl) {
+        encode_kernel<true><<<grid, kEncThreads, kEncDynSmem, st>>>(p);
+        return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kEncThreads);
+    cfg.dynamicSmemBytes = kEncDynSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, encode_kernel<true>, p);
+}
+
 static int encode_impl(const a8_enc_seg_t* segs, int nseg, const void* book_dev, int norm,
                        const void* static_lut_dev, a8_layout_t layout, void* workspace,
                        size_t workspace_bytes, const uint32_t* status_in, uint32_t* status_out,
@@ -2407,7 +2441,7 @@ static int encode_impl(const a8_enc_seg_t* segs, int nseg, const void* book_dev,
         std::copy(blks.begin(), blks.end(), p.blks);
         if (pre) premax_tables_kernel<<<nbig, kConsumers, 0, st>>>(p);
         if (amax_in)
-            encode_kernel<true><<<(unsigned)grid, kEncThreads, kEncDynSmem, st>>>(p);
+            launch_premax(p, (unsigned)grid, pre, st);
         else
             encode_kernel<false><<<(unsigned)grid, kEncThreads, kEncDynSmem, st>>>(p);
     } else {
@@ -2422,7 +2456,7 @@ static int encode_impl(const a8_enc_seg_t* segs, int nseg, const void* book_dev,
         p.blks_dev = reinterpret_cast<const EncBlk*>(plan + sb);
         if (pre) premax_tables_kernel<<<nbig, kConsumers, 0, st>>>(p);
         if (amax_in)
-            encode_kernel<true><<<(unsigned)grid, kEncThreads, kEncDynSmem, st>>>(p);
+            launch_premax(p, (unsigned)grid, pre, st);
         else
             encode_kernel<false><<<(unsigned)grid, kEncThreads, kEncDynSmem, st>>>(p);
     }
