@@ -96,7 +96,13 @@ def test_blocked_beyond_2_to_31_elements(cuda):
     del x
     y = A.decode_buffer(q, cb).view(-1)
     db = A.decode_buffer(qb, cb).view(-1)
-    assert bool((y[:P * reps].view(reps, P) == db.view(1, P)).all())
+    bad = y[:P * reps].view(reps, P) != db.view(1, P)
+    if bool(bad.any()):  # report where (one intermittent failure seen in round 2, not reproduced)
+        idx = bad.nonzero()[:8].tolist()
+        flat = [r * P + c for r, c in idx]
+        pytest.fail(f"{int(bad.sum())} decoded values differ; first at {flat} (chunks "
+                    f"{sorted({f // 4096 for f in flat})}): got {[y[f].item() for f in flat[:3]]}, "
+                    f"want {[db[f % P].item() for f in flat[:3]]}")
     del y, q, c, s
     torch.cuda.empty_cache()
 

@@ -1,0 +1,32 @@
+"""Repeat the per-block decode of tests/test_blocked.py::test_blocked_beyond_2_to_31_elements
+(2^31 + 4099 elements) and report mismatching positions: one intermittent failure
+was seen in a full-suite run in round 2 and not reproduced since."""
+import sys, torch, numpy as np
+sys.path.insert(0, "tests"); sys.path.insert(0, ".")
+from helpers import O
+import paper_1511_04561_b200 as A
+cuda = torch.device("cuda", 0)
+P, reps, tail, block = 1 << 20, 2048, 4099, 4096
+base_np = O.sample_normal(P, 33, 0.0, 0.3); base_np[::7] *= 1e-3
+cb = A.build_codebook(A.DataTypeSpec("dynamic-tree", "absmax"))
+base = torch.from_numpy(base_np).to(cuda)
+qb = A.encode_buffer(base, cb, block_size=block)
+db = A.decode_buffer(qb, cb).view(-1)
+x = torch.empty(P * reps + tail, device=cuda)
+x[:P * reps].view(reps, P).copy_(base.expand(reps, P)); x[P * reps:] = base[:tail]
+q = A.encode_buffer(x, cb, block_size=block)
+del x
+for it in range(6):
+    y = A.decode_buffer(q, cb).view(-1)
+    bad = (y[:P * reps].view(reps, P) != db.view(1, P))
+    nb = int(bad.sum())
+    if nb:
+        idx = bad.nonzero()[:5].tolist()
+        flat = [r * P + c for r, c in idx]
+        print("iter", it, "mismatches", nb, "first", flat, "chunks", sorted(set(f // 4096 for f in flat))[:5], flush=True)
+        r, c = idx[0]
+        print("  got", y[r * P + c].item(), "want", db[c].item(), flush=True)
+    else:
+        print("iter", it, "ok", flush=True)
+    del y
+    torch.cuda.synchronize()
