@@ -16,7 +16,7 @@ x = torch.empty(P * reps + tail, device=cuda)
 x[:P * reps].view(reps, P).copy_(base.expand(reps, P)); x[P * reps:] = base[:tail]
 q = A.encode_buffer(x, cb, block_size=block)
 del x
-for it in range(6):
+for it in range(int(sys.argv[1]) if len(sys.argv) > 1 else 6):
     y = A.decode_buffer(q, cb).view(-1)
     bad = (y[:P * reps].view(reps, P) != db.view(1, P))
     nb = int(bad.sum())
