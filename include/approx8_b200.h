@@ -180,7 +180,9 @@ int a8_encode(const a8_enc_seg_t* segs, int nseg, const void* book_dev, int norm
  * call are then unspecified, but every access stays in bounds).  Two
  * non-finite maxima (Inf / any NaN) agree: that input is reported with
  * A8_STATUS_NONFINITE as by a8_encode.  Same
- * layout / workspace / status conventions as a8_encode.
+ * layout / workspace / status conventions as a8_encode.  Launches: one, or
+ * for calls beyond the resident kernel a table prologue (one CTA per
+ * multi-chunk segment) plus the encode as its programmatic dependent.
  * Replaces the max pass of codecs.py:237-241 when the producer supplies it
  * (the encode fused with its producer).                  */
 int a8_encode_premax(const a8_enc_seg_t* segs, int nseg, const void* book_dev, const uint32_t* amax_dev,
